@@ -1,0 +1,299 @@
+"""CPU ORACLE for the Sirius decode hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
+``--impl reference`` legs may import this module.  It shares no code with the CUDA
+path (``paper_2409_03856_b200``) and never takes an input or expected value from it.
+
+Layers:
+  * ``oracle.cpp`` (fp64, plain loops): one decoder row (``forward_row``), the layer MLP
+    with CATS thresholding, KV rewrite.  See its header for the citations and the
+    numeric contract (D15).
+  * this file: the Sirius loop, Algorithm 1 with the readings
+    D5-D14, D17-D18 of DESIGN.md §2, written out step by step; plus the paper's
+    efficiency formulas (Eq. 1-3) and the SD expected-AAL formula
+    (PAPER.md:100-104).
+
+Pins (tests/test_oracle_*.py): HF LlamaForCausalLM fp64; KV identity; chunk == sequential;
+brute-force masked MLP; t=0 == dense; r=0 accepts all; EXACT_ARGMAX == dense greedy;
+rewrite equivalence; accounting identities; Table 2 / §5.2 / §2.3 printed arithmetic.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+ACCEPT_THRESHOLD = 0  # keep d_{i+1} iff q_i = softmax(l_i)[d_{i+1}] >= r  (reading D14)
+ACCEPT_EXACT_ARGMAX = 1  # keep d_{i+1} iff d_{i+1} == argmax l_i (speculative-decoding greedy match)
+
+
+def build() -> str:
+    out = os.path.join(_HERE, "liboracle.so")
+    src = os.path.join(_HERE, "oracle.cpp")
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
+                               "-o", out, src])
+    return out
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        lib.oracle_create.argtypes = [ctypes.c_int] * 7 + [ctypes.c_double, ctypes.c_double] + [ctypes.c_int] * 4
+        lib.oracle_create.restype = P
+        lib.oracle_destroy.argtypes = [P]
+        lib.oracle_set_global.argtypes = [P, P, P, P]
+        lib.oracle_set_layer.argtypes = [P, ctypes.c_int] + [P] * 7
+        lib.oracle_forward_row.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P, P, P]
+        lib.oracle_mlp.argtypes = [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_float, P, P, P]
+        lib.oracle_kv_rewrite.argtypes = [P, ctypes.c_int, ctypes.c_int]
+        lib.oracle_read_cache.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
+        lib.oracle_round_bf16.argtypes = [ctypes.c_double]
+        lib.oracle_round_bf16.restype = ctypes.c_double
+        _LIB = lib
+    return _LIB
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def round_bf16(x: float) -> float:
+    return float(_lib().oracle_round_bf16(float(x)))
+
+
+@dataclass
+class RowOut:
+    logits: np.ndarray  # fp64 [vocab]
+    gate: Optional[np.ndarray] = None  # a = SiLU(g), fp64 [L, ffn]
+    mask: Optional[np.ndarray] = None  # uint8 [L, ffn]
+    n_active: Optional[np.ndarray] = None  # int32 [L]
+
+
+class OracleModel:
+    """One sequence's oracle state: borrowed weights + its own KV cache and staging."""
+
+    def __init__(self, cfg, weights: Dict[str, np.ndarray], max_seq: int, max_gamma: int = 64,
+                 threads: Optional[int] = None, round_acts: bool = True):
+        self.cfg = cfg
+        self.w = weights  # keep alive
+        self.max_seq, self.max_gamma = max_seq, max_gamma
+        self.threads = threads or max(1, os.cpu_count() or 1)
+        lib = _lib()
+        self.h = lib.oracle_create(cfg.vocab, cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                                   cfg.ffn_dim, cfg.rope_theta, cfg.rms_eps, max_seq, max_gamma, self.threads,
+                                   1 if round_acts else 0)
+        for k in weights:
+            assert weights[k].dtype == np.uint16 and weights[k].flags["C_CONTIGUOUS"], k
+        lib.oracle_set_global(self.h, _ptr(weights["embed"]), _ptr(weights["final_norm"]), _ptr(weights["lm_head"]))
+        for l in range(cfg.n_layers):
+            g = lambda n: _ptr(weights[f"layers.{l}.{n}"])
+            lib.oracle_set_layer(self.h, l, g("attn_norm"), g("w_qkv"), g("w_o"), g("ffn_norm"), g("w_gate"),
+                                 g("w_up"), g("w_down"))
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h and _LIB is not None:
+            try:
+                _LIB.oracle_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
+    # ------------------------------------------------------------ one row
+    def forward_row(self, tok: int, pos: int, sparse: bool = False, thresholds: Optional[np.ndarray] = None,
+                    stage_row: int = -1, want_gate: bool = False, want_mask: bool = False) -> RowOut:
+        cfg = self.cfg
+        assert 0 <= tok < cfg.vocab and 0 <= pos < self.max_seq
+        assert stage_row < self.max_gamma
+        logits = np.empty(cfg.vocab, dtype=np.float64)
+        gate = np.empty((cfg.n_layers, cfg.ffn_dim), dtype=np.float64) if want_gate else None
+        mask = np.empty((cfg.n_layers, cfg.ffn_dim), dtype=np.uint8) if want_mask else None
+        nact = np.empty(cfg.n_layers, dtype=np.int32)
+        thr = None
+        if sparse:
+            thr = np.ascontiguousarray(thresholds, dtype=np.float32)
+            assert thr.shape == (cfg.n_layers,)
+        _lib().oracle_forward_row(self.h, int(tok), int(pos), 1 if sparse else 0, _ptr(thr), int(stage_row),
+                                  _ptr(logits), _ptr(gate), _ptr(mask), _ptr(nact), None)
+        return RowOut(logits, gate, mask, nact)
+
+    def mlp(self, layer: int, x: np.ndarray, sparse: bool, threshold: float = 0.0):
+        """Layer-isolated MLP on residual x (fp64 [d]); returns (x_out, a, mask, n_active)."""
+        cfg = self.cfg
+        xx = np.ascontiguousarray(x, dtype=np.float64).copy()
+        gate = np.empty(cfg.ffn_dim, dtype=np.float64)
+        mask = np.empty(cfg.ffn_dim, dtype=np.uint8)
+        n = np.empty(1, dtype=np.int32)
+        _lib().oracle_mlp(self.h, layer, _ptr(xx), 1 if sparse else 0, float(threshold), _ptr(gate), _ptr(mask),
+                          _ptr(n))
+        return xx, gate, mask, int(n[0])
+
+    def kv_rewrite(self, T: int, n: int) -> None:
+        assert 1 <= n <= self.max_gamma and T + n <= self.max_seq
+        _lib().oracle_kv_rewrite(self.h, int(T), int(n))
+
+    def read_cache(self, layer: int, n: int):
+        cfg = self.cfg
+        k = np.empty((n, cfg.n_kv_heads, cfg.head_dim), dtype=np.float64)
+        v = np.empty_like(k)
+        _lib().oracle_read_cache(self.h, layer, n, _ptr(k), _ptr(v))
+        return k, v
+
+    # ------------------------------------------------------------ model-level steps
+    def prefill(self, tokens: Sequence[int]) -> np.ndarray:
+        """Dense prefill (PAPER.md:471 'most use full weights for prefilling', reading D17).
+        Writes the cache rows [0, P); returns the logits of every prompt position [P, vocab]."""
+        return np.stack([self.forward_row(t, i).logits for i, t in enumerate(tokens)])
+
+    def decode(self, tok: int, pos: int, sparse: bool, thresholds=None, **kw) -> RowOut:
+        """One decode step of M_S (sparse) or M_F (dense): writes K/V at cache slot pos."""
+        return self.forward_row(tok, pos, sparse, thresholds, -1, **kw)
+
+    def verify(self, kernel_tokens: Sequence[int], T: int) -> np.ndarray:
+        """Full-model parallel verification of one kernel (Alg. 1 line 'FORWARD(M_F, C, kernel)',
+        PAPER.md:258; §4.2): rows [pending, d_1..d_{g-1}] at positions T..T+g-1,
+        K/V into staging, each row attends to cache[0,T) + staging[0..i].  Returns logits [g, vocab]."""
+        return np.stack([self.forward_row(t, T + i, False, None, i).logits for i, t in enumerate(kernel_tokens)])
+
+
+def argmax_lowest(l: np.ndarray) -> int:
+    """argmax with the lowest token id on exact ties (reading D13)."""
+    return int(np.flatnonzero(l == l.max())[0])
+
+
+def softmax_prob(l: np.ndarray, tok: int) -> float:
+    """q = softmax(l)[tok] at temperature 1 (reading D12)."""
+    m = l.max()
+    return float(np.exp(l[tok] - m) / np.exp(l - m).sum())
+
+
+def accept_scan(lf: np.ndarray, kernel_tokens: Sequence[int], r: float, mode: int = ACCEPT_THRESHOLD):
+    """Algorithm 1 lines 'for j from 0, n: if q_{t+j} < r: break', reading D8/D14.
+    Returns (j, q): j = first rejected index in [0, g-2], or g-1 if all g-1 drafts are accepted;
+    q[i] = full-model probability of draft d_{i+1} for i < g-1, q[g-1] = probability of argmax row g-1."""
+    g = len(kernel_tokens)
+    q = np.empty(g, dtype=np.float64)
+    j = g - 1
+    for i in range(g - 1):
+        q[i] = softmax_prob(lf[i], kernel_tokens[i + 1])
+    q[g - 1] = softmax_prob(lf[g - 1], argmax_lowest(lf[g - 1]))
+    for i in range(g - 1):
+        ok = q[i] >= r if mode == ACCEPT_THRESHOLD else kernel_tokens[i + 1] == argmax_lowest(lf[i])
+        if not ok:
+            j = i
+            break
+    return j, q
+
+
+@dataclass
+class KernelRecord:
+    T: int  # cache length before the kernel (position of the pending token)
+    tokens: List[int]  # [pending, d_1..d_{g-1}]
+    j: int  # accepted drafts (= first rejected index, or g-1)
+    q: np.ndarray  # full-model likelihoods
+    next_token: int  # interleaved / bonus token = argmax of verify row j
+    n_active: np.ndarray  # [g-1, L] active neurons per sparse step
+
+
+@dataclass
+class GenerateResult:
+    tokens: List[int]
+    kernels: List[KernelRecord] = field(default_factory=list)
+    all_tokens: List[int] = field(default_factory=list)  # untruncated (includes the last kernel's surplus)
+
+    @property
+    def advances(self) -> List[int]:
+        return [k.j + 1 for k in self.kernels]
+
+
+def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: int, r: float,
+             thresholds: np.ndarray, accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True) -> GenerateResult:
+    """The Sirius loop, Algorithm 1, readings D5-D18:
+      * dense prefill of the prompt; the first generated token is the dense argmax (D17);
+      * kernel size n = gamma: the sparse model drafts gamma-1 tokens after the pending token,
+        writing its K/V at T..T+gamma-2 (Alg. 1 lines 6-11, 'Running sparse model');
+      * the full model verifies [pending, d_1..d_{g-1}] at T..T+g-1 in one pass (line 'FORWARD(M_F..)');
+      * accept scan with threshold r (lines 12-16); rollback to T+j+1 (line 'cache_pos <- j+1');
+      * KV rewrite of the committed span [T, T+j] with the full model's K/V;
+      * interleave the full model's argmax of row j (line 'Interleaving Key Token', reading D10/D11).
+    Generates exactly n_tokens tokens (D18); the final kernel's surplus is truncated."""
+    P = len(prompt)
+    assert P + n_tokens + gamma <= model.max_seq and gamma >= 1
+    logits = model.prefill(prompt)
+    out = [argmax_lowest(logits[-1])]  # out[-1] is the pending token at position T
+    T = P
+    res = GenerateResult(out)
+    while len(out) < n_tokens:
+        ins = [out[-1]]
+        nact = []
+        for i in range(gamma - 1):  # sparse drafting, greedy (D13)
+            row = model.decode(ins[i], T + i, True, thresholds)
+            nact.append(row.n_active)
+            ins.append(argmax_lowest(row.logits))
+        lf = model.verify(ins, T)  # full model over the kernel, K/V -> staging
+        j, q = accept_scan(lf, ins, r, accept_mode)
+        if rewrite:
+            model.kv_rewrite(T, j + 1)  # commit + rollback: len = T + j + 1
+        nxt = argmax_lowest(lf[j])
+        out += ins[1:j + 1] + [nxt]
+        res.kernels.append(KernelRecord(T, list(ins), j, q, nxt, np.array(nact, dtype=np.int32).reshape(-1, model.cfg.n_layers)))
+        T += j + 1
+    res.all_tokens = list(out)
+    res.tokens = out[:n_tokens]
+    return res
+
+
+def greedy_decode(model: OracleModel, prompt: Sequence[int], n_tokens: int, sparse: bool = False,
+                  thresholds=None) -> List[int]:
+    """Plain autoregressive greedy decode (dense = M_F, or CS-only = M_S) after a dense prefill."""
+    logits = model.prefill(prompt)
+    out = [argmax_lowest(logits[-1])]
+    for i in range(n_tokens - 1):
+        row = model.decode(out[-1], len(prompt) + i, sparse, thresholds)
+        out.append(argmax_lowest(row.logits))
+    return out
+
+
+# ---------------------------------------------------------------- efficiency formulas (report fields)
+def apu(n_sparse: float, c_sparse: float, c_full: float, n_aal: float) -> float:
+    """Eq. 1: APU = (n_sparse * C_sparse + C_full) / n_AAL."""
+    return (n_sparse * c_sparse + c_full) / n_aal
+
+
+def effective_density(n_period: float, global_density: float, n_aal: float) -> float:
+    """Eq. 3: ((n_period - 1) * I_globalsparsity + 1) / n_AAL."""
+    return ((n_period - 1) * global_density + 1) / n_aal
+
+
+def sd_expected_aal(alpha: float, gamma: int) -> float:
+    """§2.3: AAL = (1 - alpha^(gamma+1)) / (1 - alpha)."""
+    return (1 - alpha ** (gamma + 1)) / (1 - alpha)
+
+
+def param_counts(cfg) -> Dict[str, int]:
+    """Exact parameter counts by shape arithmetic (untied head); norms counted with attention/head."""
+    d, L, hd = cfg.d_model, cfg.n_layers, cfg.head_dim
+    attn = L * (d * (cfg.n_heads + 2 * cfg.n_kv_heads) * hd + cfg.n_heads * hd * d + d)
+    mlp = L * (3 * d * cfg.ffn_dim + d)
+    emb = cfg.vocab * d
+    head = cfg.vocab * d + d
+    return dict(attention=attn, mlp=mlp, embedding=emb, head=head, total=attn + mlp + emb + head)
+
+
+def global_density(cfg, keep: float, mode: str) -> float:
+    """I_globalsparsity = C_sparse / C_full (Eq. 2).  FSparse sparsifies up+down only
+    (PAPER.md:121 'Up and Down linear layers only'); CSparse the whole MLP.  C_full counts every
+    parameter (the paper's "MLP ... roughly 70% of the LLM total weights")."""
+    c = param_counts(cfg)
+    full = c["total"]
+    mats = 2 if mode == "fsparse" else 3
+    return (full - (1 - keep) * mats * cfg.d_model * cfg.ffn_dim * cfg.n_layers) / full
