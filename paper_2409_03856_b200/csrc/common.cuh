@@ -1,0 +1,185 @@
+// common.cuh — device helpers for the sm_100a Sirius kernels (PTX wrappers, reductions,
+// bf16 packing, grid barrier).  Product code: no oracle code is included or shared.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#define SIRIUS_DEV __device__ __forceinline__
+
+namespace sirius {
+
+constexpr int kWarp = 32;
+
+SIRIUS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ------------------------------------------------------------------ mbarrier
+SIRIUS_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+SIRIUS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+SIRIUS_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+SIRIUS_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+SIRIUS_DEV void mbar_arrive(uint64_t* bar, uint32_t count = 1) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+SIRIUS_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+SIRIUS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// ------------------------------------------------------------------ bulk async copies (TMA engine, 1-D)
+// L2 eviction policy for weight streams: every weight byte is read once per step.
+SIRIUS_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+SIRIUS_DEV uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// global -> shared, `bytes` multiple of 16, both addresses 16-byte aligned; completes tx on `bar`.
+SIRIUS_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// ------------------------------------------------------------------ PDL (programmatic dependent launch)
+SIRIUS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SIRIUS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ------------------------------------------------------------------ loads
+SIRIUS_DEV uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+SIRIUS_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------------ bf16
+SIRIUS_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+SIRIUS_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+SIRIUS_DEV uint16_t f2bf_bits(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
+SIRIUS_DEV float round_bf16(float f) { return __bfloat162float(__float2bfloat16_rn(f)); }
+SIRIUS_DEV uint32_t pack_bf16(float lo, float hi) { return (uint32_t)f2bf_bits(lo) | ((uint32_t)f2bf_bits(hi) << 16); }
+
+// dot of 8 bf16 (packed in a uint4) with 8 floats
+SIRIUS_DEV float dot8(const uint4 w, const float* x) {
+  float s = 0.f;
+  s = fmaf(bf16_lo(w.x), x[0], s);
+  s = fmaf(bf16_hi(w.x), x[1], s);
+  s = fmaf(bf16_lo(w.y), x[2], s);
+  s = fmaf(bf16_hi(w.y), x[3], s);
+  s = fmaf(bf16_lo(w.z), x[4], s);
+  s = fmaf(bf16_hi(w.z), x[5], s);
+  s = fmaf(bf16_lo(w.w), x[6], s);
+  s = fmaf(bf16_hi(w.w), x[7], s);
+  return s;
+}
+// dot of 8 bf16 weights with 8 bf16 activations
+SIRIUS_DEV float dot8bf(const uint4 w, const uint4 h, float s) {
+  s = fmaf(bf16_lo(w.x), bf16_lo(h.x), s);
+  s = fmaf(bf16_hi(w.x), bf16_hi(h.x), s);
+  s = fmaf(bf16_lo(w.y), bf16_lo(h.y), s);
+  s = fmaf(bf16_hi(w.y), bf16_hi(h.y), s);
+  s = fmaf(bf16_lo(w.z), bf16_lo(h.z), s);
+  s = fmaf(bf16_hi(w.z), bf16_hi(h.z), s);
+  s = fmaf(bf16_lo(w.w), bf16_lo(h.w), s);
+  s = fmaf(bf16_hi(w.w), bf16_hi(h.w), s);
+  return s;
+}
+
+// ------------------------------------------------------------------ warp / block reductions (fixed order)
+SIRIUS_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+SIRIUS_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// order-preserving float -> uint32 (monotone), for packed argmax keys
+SIRIUS_DEV uint32_t float_ordered(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+SIRIUS_DEV float ordered_float(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+// argmax key: larger value wins, then LOWER index wins (reading D13)
+SIRIUS_DEV unsigned long long argmax_key(float v, uint32_t idx) {
+  return ((unsigned long long)float_ordered(v) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+}
+SIRIUS_DEV uint32_t argmax_key_index(unsigned long long k) { return 0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull); }
+SIRIUS_DEV unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------ grid-wide barrier
+// All CTAs of the launch must be co-resident (cooperative launch).  Monotone 64-bit counter:
+// generation g completes when the counter reaches (g+1)*nblocks; never reset, never wraps.
+SIRIUS_DEV void grid_barrier(unsigned long long* counter, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long old = atomicAdd(counter, 1ull);
+    unsigned long long target = (old / nblocks + 1) * nblocks;
+    while (ld_acquire_u64(counter) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// "last CTA to arrive" election for split reductions; returns true in exactly one CTA per group
+// of `n` arrivals.  The last arrival resets the counter to 0 for the next launch.
+SIRIUS_DEV bool arrive_last(unsigned* counter, unsigned n) {
+  __shared__ unsigned s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned old = atomicAdd(counter, 1u);
+    bool last = old == n - 1;
+    if (last) {
+      atomicExch(counter, 0u);
+      __threadfence();
+    }
+    s_last = last ? 1u : 0u;
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+}  // namespace sirius

@@ -1,0 +1,76 @@
+// decode_kernels.cuh — kernel argument structs shared by decode_kernels.cu and runtime.cu.
+#pragma once
+#include <cstdint>
+
+namespace sirius {
+
+// ---- input prologue modes of the streaming GEMV / fused FFN kernels
+enum InMode : int {
+  IN_BF16 = 0,   // activation already bf16 in global: in_bf16 [B, K]
+  IN_RESID = 1,  // x = base + delta (delta may be NULL); h = bf16(rmsnorm(x) * norm_w)
+  IN_EMBED = 2,  // x = embed[tokens[b]];             h = bf16(rmsnorm(x) * norm_w)
+};
+
+struct Prologue {
+  int mode;
+  const uint16_t* in_bf16;  // IN_BF16
+  const float* base;        // IN_RESID [B, K]
+  const float* delta;       // IN_RESID [B, K] or NULL
+  const int32_t* tokens;    // IN_EMBED [B]
+  const uint16_t* embed;    // IN_EMBED [V, K]
+  int vocab;
+  const uint16_t* norm_w;   // [K]
+  float eps;
+  float* res_out;           // if non-NULL, CTA 0 stores x [B, K] here (never aliases base)
+};
+
+// ---- streaming GEMV: out[b, r] = sum_k W[r, k] * h[b, k]
+enum GemvEpi : int { EPI_STORE = 0, EPI_ARGMAX = 1 };
+
+struct GemvArgs {
+  Prologue pro;
+  const uint16_t* W;  // [rows, K]
+  int rows, K;
+  int epi;
+  float* out;                   // EPI_STORE: [B, ldo]; EPI_ARGMAX: optional logits [B, ldo]
+  int ldo;                      // row stride of out
+  unsigned long long* amax;     // EPI_ARGMAX: packed (value, lowest index) keys [B]
+  uint32_t index_offset;        // EPI_ARGMAX: global vocab offset of row 0 (TP shard)
+  int finalize;                 // EPI_ARGMAX: last CTA converts amax -> token_out and resets amax
+  unsigned* done_counter;       // EPI_ARGMAX + finalize
+  int32_t* token_out;           // EPI_ARGMAX + finalize: [B]
+};
+
+// ---- fused CATS FFN (gate GEMV + SiLU + threshold + ballot compaction + up/down gathers)
+struct FfnArgs {
+  Prologue pro;
+  const uint16_t *w_gate, *w_up, *w_down;  // [F, d] neuron-major
+  int F, d;
+  const float* threshold;  // device fp32 (this layer's t_l)
+  int dense;               // 1: every neuron active (M_F)
+  float* part;             // workspace [grid, B, d] fp32 partial sums
+  int* part_cnt;           // workspace [grid, B]
+  unsigned long long* barrier;  // grid barrier counter
+  float* out;              // [B, d] = sum over active neurons of m_i * W_down[i]
+  int32_t* n_active_out;   // [B * n_active_stride] (+layer) or NULL
+  int n_active_stride;
+  float* gate_out;         // [B * gate_stride] (+layer*F) or NULL: a = SiLU(g)
+  long long gate_stride;
+};
+
+// ---- decode attention (RoPE + KV append + split-K flash decode + last-CTA combine)
+struct AttnArgs {
+  const float* qkv;        // [B, (Hr + 2 KVr) * hd] raw projections (pre-RoPE), fp32
+  const int32_t* pos;      // [B]
+  const float* rope_cos;   // [max_seq, hd/2]
+  const float* rope_sin;
+  uint16_t* k_cache;       // this layer: [B, KVr, max_seq, hd]
+  uint16_t* v_cache;
+  int Hr, KVr, max_seq, splits;
+  float* part;             // workspace [B, KVr, splits, G, hd + 2]
+  unsigned* counters;      // [B, KVr]
+  uint16_t* out;           // [B, Hr * hd] bf16
+  int* err;                // sticky device error word
+};
+
+}  // namespace sirius

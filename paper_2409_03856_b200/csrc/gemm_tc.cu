@@ -1,0 +1,297 @@
+// gemm_tc.cu — tcgen05 tensor-core GEMM for the gamma-row full-model verification forward
+// ("memory-bound while rows <= 64", PAPER.md:70 / Table 10; the verify pass is
+// the one place on the path that really is a dense contraction).
+//
+//   C[m, n] = sum_k X[m, k] * W[n, k]          X: activations [Mp, K] bf16, W: weights [N, K] bf16
+//
+// Swap-AB: the weights are the MMA "A" operand (M = 128 weight rows per tile), the Mp <= 256 token
+// rows are the MMA "B" operand (N = Mp), so one tcgen05.mma.kind::f16 128 x Mp x 16 instruction
+// covers every token of the kernel; accumulators (fp32) live in TMEM.  Operands arrive via 2-D TMA
+// (cp.async.bulk.tensor, SWIZZLE_128B) into a multi-stage mbarrier ring.  Work is split stream-K
+// style over the 148 SMs: CTA c owns the contiguous k-block range [W c / G, W (c+1) / G) of the
+// (tile, k-block) space, so every SM streams the same number of weight bytes; tiles cut by a CTA
+// boundary are reduced deterministically (fixed CTA order) by the last-arriving CTA.
+//
+// Roles (128 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer, warp 2 = TMEM
+// allocator; all four warps run the epilogue (TMEM lane = weight row = threadIdx.x).
+// Epilogues: fp32 store, or SwiGLU m = bf16(SiLU(g) * u) from two accumulators (gate, up).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+namespace sirius {
+
+SIRIUS_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+      "[%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+SIRIUS_DEV void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1"):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major), SBO>>4 [32,46) = 1024 B between
+// 8-row core groups, version [46,48) = 1, layout [61,64) = 2 (SWIZZLE_128B).
+SIRIUS_DEV uint64_t sw128_desc(const void* smem) {
+  const uint32_t a = smem_u32(smem);
+  return (uint64_t)((a & 0x3FFFFu) >> 4) | ((uint64_t)(1024u >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+SIRIUS_DEV void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+SIRIUS_DEV void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+SIRIUS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SIRIUS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 16 columns of fp32 from TMEM (this warp's lane quarter) -> 16 registers per thread.
+SIRIUS_DEV void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// last CTA owning work item x (CTA c owns [floor(W c / G), floor(W (c+1) / G)))
+SIRIUS_DEV int owner_of(long long x, long long W, int G) { return (int)(((x + 1) * G + W - 1) / W) - 1; }
+
+template <bool DUAL>
+SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
+  if (j >= g.M || n >= g.N) return;
+  if (DUAL) {
+    const float a = v0 / (1.0f + expf(-v0));  // SiLU(gate)
+    reinterpret_cast<uint16_t*>(g.out)[(size_t)j * g.ldc + n] = f2bf_bits(a * v1);
+  } else {
+    reinterpret_cast<float*>(g.out)[(size_t)j * g.ldc + n] = v0;
+  }
+}
+
+template <bool DUAL>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                   const __grid_constant__ CUtensorMap tmB, GemmArgs g, int MP, int stages) {
+  constexpr int NACC = DUAL ? 2 : 1;
+  constexpr uint32_t A_BYTES = 128 * 64 * 2;  // one 128 x 64 bf16 weight tile
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int G = gridDim.x, c = blockIdx.x;
+  const long long W = (long long)g.n_tiles * g.kb;
+  const long long w0 = W * c / G, w1 = W * (c + 1) / G;
+  if (w0 == w1) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t b_bytes = (uint32_t)MP * 128;
+  const uint32_t stage_bytes = ((NACC * A_BYTES + b_bytes) + 1023) & ~1023u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* accum = empty + stages;
+  uint32_t* tmem_ptr_s = reinterpret_cast<uint32_t*>(accum + 1);
+  uint32_t ncols = 32;
+  while (ncols < (uint32_t)(NACC * MP)) ncols <<= 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    fence_mbar_init();
+    prefetch_tmap(&tmA0);
+    if (DUAL) prefetch_tmap(&tmA1);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_ptr_s)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr_s;
+  // instruction descriptor, kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
+  // both K-major, N>>3 at [17,23), M>>4 at [24,29)
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((128u >> 4) << 24);
+  const uint32_t tx_bytes = NACC * A_BYTES + b_bytes;
+
+  long long it = 0;  // global k-iteration counter: stage = it % stages, parity = (it / stages) & 1
+  int sidx = 0;
+  for (long long w = w0; w < w1; ++sidx) {
+    const int t = (int)(w / g.kb);
+    const int kbeg = (int)(w % g.kb);
+    const long long wend = min(w1, (long long)(t + 1) * g.kb);
+    const int nk = (int)(wend - w);
+    if (warp == 0 && lane == 0) {  // ---- TMA producer
+      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      for (int i = 0; i < nk; ++i) {
+        const long long q = it + i;
+        const int s = (int)(q % stages);
+        mbar_wait(&empty[s], ((uint32_t)(q / stages) & 1u) ^ 1u);
+        uint8_t* st = smem + (size_t)s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], tx_bytes);
+        const int kc = (kbeg + i) * 64;
+        tma_load_2d(st, &tmA0, kc, t * 128, &full[s], pol_w);
+        if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[s], pol_w);
+        for (int r = 0; r < MP / 16; ++r)
+          tma_load_2d(st + NACC * A_BYTES + r * 2048, &tmB, kc, r * 16, &full[s], pol_x);
+      }
+    } else if (warp == 1 && lane == 0) {  // ---- MMA issuer
+      for (int i = 0; i < nk; ++i) {
+        const long long q = it + i;
+        const int s = (int)(q % stages);
+        mbar_wait(&full[s], (uint32_t)(q / stages) & 1u);
+        tc_fence_after();
+        uint8_t* st = smem + (size_t)s * stage_bytes;
+        const uint64_t a0 = sw128_desc(st), b0 = sw128_desc(st + NACC * A_BYTES);
+        const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES) : 0ull;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
+          const uint32_t accf = (i > 0 || k > 0) ? 1u : 0u;
+          mma_bf16(tmem, a0 + 2 * k, b0 + 2 * k, idesc, accf);
+          if (DUAL) mma_bf16(tmem + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
+        }
+        mma_commit(&empty[s]);  // smem slot free once these MMAs have read it
+      }
+      mma_commit(accum);  // accumulator complete
+    }
+    it += nk;
+    __syncwarp();
+    // ---- epilogue (all 128 threads; thread = TMEM lane = weight row of the tile)
+    mbar_wait(accum, (uint32_t)sidx & 1u);
+    tc_fence_after();
+    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    const int n = t * 128 + tid;
+    const bool complete = (kbeg == 0 && wend == (long long)(t + 1) * g.kb);
+    if (complete) {
+      for (int j0 = 0; j0 < MP; j0 += 16) {
+        float v0[16], v1[16];
+        tmem_ld16(tbase + j0, v0);
+        if (DUAL) tmem_ld16(tbase + MP + j0, v1);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, v0[j], DUAL ? v1[j] : 0.f);
+      }
+    } else {
+      const int slot = (w == w0) ? 0 : 1;
+      float* mine = g.part + ((size_t)(c * 2 + slot) * NACC) * 256 * 128;
+      for (int j0 = 0; j0 < MP; j0 += 16) {
+        float v[16];
+        for (int a = 0; a < NACC; ++a) {
+          tmem_ld16(tbase + a * MP + j0, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) mine[((size_t)a * 256 + j0 + j) * 128 + tid] = v[j];
+        }
+      }
+      const int cf = owner_of((long long)t * g.kb, W, G);
+      const int cl = owner_of(min(W, (long long)(t + 1) * g.kb) - 1, W, G);
+      if (arrive_last(g.counters + t, (unsigned)(cl - cf + 1))) {
+        for (int j0 = 0; j0 < MP; j0 += 16) {
+          float s0[16], s1[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) s0[j] = s1[j] = 0.f;
+          for (int cc = cf; cc <= cl; ++cc) {  // fixed CTA order -> deterministic
+            const long long cw0 = W * cc / G;
+            const int sl = ((int)(cw0 / g.kb) == t) ? 0 : 1;
+            const float* p = g.part + ((size_t)(cc * 2 + sl) * NACC) * 256 * 128;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              s0[j] += __ldcg(p + (size_t)(j0 + j) * 128 + tid);
+              if (DUAL) s1[j] += __ldcg(p + ((size_t)256 + j0 + j) * 128 + tid);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, s0[j], s1[j]);
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM drained before the next segment's MMAs overwrite it
+    tc_fence_after();
+    w = wend;
+  }
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+}
+
+// ===================================================================== host side
+namespace launch {
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, K] matrix; box = 64 (K) x box_rows, SWIZZLE_128B.
+bool make_tmap(void* map, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {K * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+size_t gemm_workspace_bytes(int num_sms) { return (size_t)num_sms * 2 * 2 * 256 * 128 * sizeof(float); }
+
+cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const GemmArgs& g, int MP, int num_sms,
+                 size_t smem_budget, cudaStream_t st) {
+  if (MP < 16 || MP > 256 || MP % 16) return cudaErrorInvalidValue;
+  const bool dual = tmA1 != nullptr;
+  const int NACC = dual ? 2 : 1;
+  const size_t stage_bytes = ((size_t)NACC * 16384 + (size_t)MP * 128 + 1023) & ~(size_t)1023;
+  const size_t extra = 1024 + 256;
+  int stages = (int)((smem_budget - extra) / stage_bytes);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)stages * stage_bytes + extra;
+  const long long W = (long long)g.n_tiles * g.kb;
+  const int grid = (int)(W < num_sms ? W : num_sms);
+  const CUtensorMap* a0 = reinterpret_cast<const CUtensorMap*>(tmA0);
+  const CUtensorMap* a1 = reinterpret_cast<const CUtensorMap*>(dual ? tmA1 : tmA0);
+  const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmB);
+  if (dual) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    gemm_tc_kernel<true><<<grid, 128, smem, st>>>(*a0, *a1, *b, g, MP, stages);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    gemm_tc_kernel<false><<<grid, 128, smem, st>>>(*a0, *a1, *b, g, MP, stages);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace launch
+}  // namespace sirius

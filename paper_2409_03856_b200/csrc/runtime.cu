@@ -1,0 +1,820 @@
+// runtime.cu — libsirius runtime: context, static KV slabs, workspaces, tensor maps, TP all-reduces
+// (NCCL over NVLink, or the single-GPU in-order emulation), and the C-ABI entry points declared in
+// include/sirius.h.  The Sirius loop itself (Algorithm 1) is driven by the caller through these
+// entry points; every arithmetic step runs in the kernels of decode_kernels.cu, gemm_tc.cu and
+// verify_kernels.cu.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sirius.h"
+#include "common.cuh"
+#include "decode_kernels.cuh"
+#include "gemm_tc.cuh"
+#include "verify_kernels.cuh"
+
+namespace sirius {
+namespace launch {
+int gemv_nslot(int B, int K, size_t smem_budget);
+cudaError_t gemv(const GemvArgs& a, int B, int grid, int nslot, cudaStream_t st);
+cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st);
+int ffn_nslot(int B, int d, size_t smem_budget);
+int ffn_grid(int F, int num_sms);
+cudaError_t ffn(const FfnArgs& a, int B, int grid, int nslot, cudaStream_t st);
+cudaError_t attn_decode(const AttnArgs& a, int B, int hd, int group, cudaStream_t st);
+}  // namespace launch
+}  // namespace sirius
+
+using namespace sirius;
+
+// ----------------------------------------------------------------------------- NCCL (dlopen'd)
+namespace {
+typedef int ncclResult_t_;
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t_ (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  ncclResult_t_ (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t_) = nullptr;
+  ncclResult_t_ (*getUniqueId)(void*) = nullptr;
+  ncclResult_t_ (*commInitRank)(void**, int, char[128], int) = nullptr;
+  ncclResult_t_ (*commDestroy)(void*) = nullptr;
+};
+// nccl.h enum values (stable ABI): ncclUint8 = 1... ncclUint64 = 5, ncclFloat32 = 7; ncclSum = 0, ncclMax = 2
+constexpr int kNcclUint8 = 1, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclSum = 0, kNcclMax = 2;
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.loaded) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.loaded = api.allReduce && api.allGather && api.getUniqueId && api.commInitRank;
+    }
+  }
+  return api;
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+}  // namespace
+
+// ----------------------------------------------------------------------------- context
+struct TmapBuf {
+  alignas(64) unsigned char b[128];
+};
+
+struct RankState {
+  int rank = 0;
+  // weights (borrowed) + owned transposed W_down copies for the verify GEMM (K-major in ffn)
+  const uint16_t *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  std::vector<const uint16_t*> attn_norm, w_qkv, w_o, ffn_norm, w_gate, w_up, w_down;
+  std::vector<uint16_t*> w_down_t;
+  // KV cache + verify staging
+  uint16_t *k_cache = nullptr, *v_cache = nullptr, *stage_k = nullptr, *stage_v = nullptr;
+  // activations (MAXM rows)
+  float *resA = nullptr, *resB = nullptr, *dA = nullptr, *dF = nullptr, *qkv = nullptr, *logits = nullptr;
+  uint16_t *xn = nullptr, *qb = nullptr, *ob = nullptr, *mb = nullptr;
+  // workspaces
+  float *ffn_part = nullptr, *attn_part = nullptr, *gemm_part = nullptr;
+  int* ffn_cnt = nullptr;
+  unsigned long long* ffn_barrier = nullptr;
+  unsigned *attn_cnt = nullptr, *gemm_cnt = nullptr, *head_cnt = nullptr;
+  // tensor maps
+  std::vector<TmapBuf> tm_qkv, tm_o, tm_gate, tm_up, tm_down;
+  TmapBuf tm_head, tm_xn, tm_ob, tm_mb;
+};
+
+struct sirius_ctx {
+  sirius_config cfg;
+  int nranks = 1;  // ranks run by this context (tp_size when emulating, else 1)
+  bool emulated = false;
+  void* comm = nullptr;
+  cudaStream_t stream = nullptr;
+  int Hr = 0, KVr = 0, Fr = 0, Vr = 0, Nqkv = 0, G = 0, MAXM = 0;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  int attn_splits = 1;
+  int accept_splits = 8;
+  std::vector<RankState> ranks;
+  float *thresholds = nullptr, *rope_cos = nullptr, *rope_sin = nullptr;
+  int* err_dev = nullptr;
+  int* err_host = nullptr;  // pinned mirror
+  unsigned long long* amax = nullptr;
+  RowStat *stats = nullptr, *stats_gather = nullptr;
+  float** dA_ptrs = nullptr;  // device arrays of per-rank buffer pointers (emulated all-reduce)
+  float** dF_ptrs = nullptr;
+  int32_t* pre_start = nullptr;  // [batch] chunk start positions (prefill)
+  int32_t* pre_start_host = nullptr;
+  int32_t* scratch_tok = nullptr;
+  int last_gamma = 0;
+  bool have_correct = false;
+  bool prefilled = false;
+  sirius_status sticky = SIRIUS_OK;
+  std::vector<void*> allocations;
+  std::string last_error = "ok";
+};
+
+namespace {
+
+sirius_status fail(sirius_ctx* c, sirius_status s, const std::string& msg) {
+  if (c) {
+    c->last_error = msg;
+    if (s == SIRIUS_ERR_CUDA || s == SIRIUS_ERR_NCCL) c->sticky = s;
+  }
+  return s;
+}
+
+#define CU(x)                                                                                        \
+  do {                                                                                               \
+    cudaError_t _e = (x);                                                                            \
+    if (_e != cudaSuccess) return fail(c, SIRIUS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+template <class T>
+sirius_status alloc(sirius_ctx* c, T** p, size_t count, bool zero = true) {
+  void* q = nullptr;
+  size_t bytes = count * sizeof(T);
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) return fail(c, SIRIUS_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  if (zero) cudaMemset(q, 0, bytes);
+  c->allocations.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return SIRIUS_OK;
+}
+
+#define OK(x)                              \
+  do {                                     \
+    sirius_status _s = (x);                \
+    if (_s != SIRIUS_OK) return _s;        \
+  } while (0)
+
+sirius_status check_sticky(sirius_ctx* c) {
+  if (c->sticky != SIRIUS_OK) return c->sticky;
+  if (*c->err_host != 0) {
+    int e = *c->err_host;
+    return fail(c, SIRIUS_ERR_CAPACITY,
+                std::string("device-side capacity error (bits ") + std::to_string(e) +
+                    "): 1 = decode pos outside [0, max_seq), 2 = verify/prefill row outside capacity, "
+                    "4 = kv_rewrite n_rows/start outside capacity");
+  }
+  return SIRIUS_OK;
+}
+
+// enqueue a copy of the device error word into the pinned host mirror (read by the next call)
+void mirror_err(sirius_ctx* c) { cudaMemcpyAsync(c->err_host, c->err_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream); }
+
+sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev, size_t rows) {
+  const size_t n = rows * c->cfg.d_model;
+  if (c->nranks > 1) {
+    CU(launch::sum_ranks(ptrs_dev, c->nranks, rows, c->cfg.d_model, c->cfg.d_model, c->stream));
+  } else if (c->cfg.tp_size > 1) {
+    NcclApi& api = nccl();
+    float* p = c->ranks[0].*buf;
+    int r = api.allReduce(p, p, n, kNcclFloat32, kNcclSum, c->comm, c->stream);
+    if (r != 0) return fail(c, SIRIUS_ERR_NCCL, std::string("ncclAllReduce: ") + api.getErrorString(r));
+  }
+  return SIRIUS_OK;
+}
+
+// ---- one GEMV (decode) launch
+sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
+  const int grid = a.rows < c->num_sms ? a.rows : c->num_sms;
+  const int nslot = launch::gemv_nslot(B, a.K, c->smem_optin);
+  if (nslot < 2) return fail(c, SIRIUS_ERR_UNSUPPORTED, "gemv: row too large for shared memory");
+  CU(launch::gemv(a, B, grid, nslot, c->stream));
+  return SIRIUS_OK;
+}
+
+sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x, int N,
+                       int K, int M, void* out, int ldc) {
+  GemmArgs g;
+  g.N = N;
+  g.K = K;
+  g.M = M;
+  g.n_tiles = (N + 127) / 128;
+  g.kb = (K + 63) / 64;
+  g.out = out;
+  g.ldc = ldc;
+  g.part = R.gemm_part;
+  g.counters = R.gemm_cnt;
+  const int MP = round_up(M, 16);
+  CU(launch::gemm(wa.b, wb ? wb->b : nullptr, x.b, g, MP, c->num_sms, c->smem_optin, c->stream));
+  return SIRIUS_OK;
+}
+
+// ---- the dense / verify / prefill forward over M token rows (chunk).  Rows are ordered
+// (sequence, i); rows_per_seq rows per sequence, sequences b_base .. b_base + nseq - 1.
+// to_cache: prefill (K/V -> cache at start[b] + i, attention reads the cache only).
+sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* start, int b_base, int nseq,
+                           int rows_per_seq, bool to_cache, int l_dummy = 0) {
+  (void)l_dummy;
+  const sirius_config& cf = c->cfg;
+  const int M = nseq * rows_per_seq, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
+  for (int l = 0; l < L; ++l) {
+    for (auto& R : c->ranks) {
+      NormRowsArgs na = {};
+      if (l == 0) {
+        na.tokens = tokens;
+        na.embed = R.embed;
+      } else {
+        na.base = R.resB;
+        na.delta = R.dF;
+      }
+      na.vocab = cf.vocab;
+      na.d = d;
+      na.norm_w = R.attn_norm[l];
+      na.eps = cf.rms_eps;
+      na.res_out = R.resA;
+      na.out = R.xn;
+      CU(launch::norm_rows(na, M, c->stream));
+      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn, c->Nqkv, d, M, R.qkv, c->Nqkv));
+      const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
+      const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
+      RopeStoreArgs ra = {};
+      ra.qkv = R.qkv;
+      ra.start = start;
+      ra.b_base = b_base;
+      ra.rows_per_seq = rows_per_seq;
+      ra.rope_cos = c->rope_cos;
+      ra.rope_sin = c->rope_sin;
+      ra.Hr = c->Hr;
+      ra.KVr = c->KVr;
+      ra.hd = hd;
+      ra.max_seq = cf.max_seq;
+      ra.max_gamma = cf.max_gamma;
+      ra.to_cache = to_cache ? 1 : 0;
+      ra.q_out = R.qb;
+      ra.k_dst = to_cache ? R.k_cache + l * kv_layer : R.stage_k + l * st_layer;
+      ra.v_dst = to_cache ? R.v_cache + l * kv_layer : R.stage_v + l * st_layer;
+      ra.err = c->err_dev;
+      CU(launch::rope_store(ra, M, c->stream));
+      AttnRowsArgs aa = {};
+      aa.q = R.qb;
+      aa.start = start;
+      aa.b_base = b_base;
+      aa.rows_per_seq = rows_per_seq;
+      aa.G = c->G;
+      aa.Hr = c->Hr;
+      aa.KVr = c->KVr;
+      aa.max_seq = cf.max_seq;
+      aa.k_cache = R.k_cache + l * kv_layer;
+      aa.v_cache = R.v_cache + l * kv_layer;
+      aa.k_fresh = R.stage_k + l * st_layer;
+      aa.v_fresh = R.stage_v + l * st_layer;
+      aa.fresh_stride = cf.max_gamma;
+      aa.fresh_in_cache = to_cache ? 1 : 0;
+      aa.part = R.attn_part;
+      aa.counters = R.attn_cnt;
+      aa.out = R.ob;
+      const int row_blocks = (rows_per_seq * c->G + 63) / 64;
+      int splits = (2 * c->num_sms + nseq * c->KVr * row_blocks - 1) / (nseq * c->KVr * row_blocks);
+      splits = splits < 1 ? 1 : (splits > 32 ? 32 : splits);
+      CU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
+      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob, d, c->Hr * hd, M, R.dA, d));
+    }
+    OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
+    for (auto& R : c->ranks) {
+      NormRowsArgs na = {};
+      na.base = R.resA;
+      na.delta = R.dA;
+      na.vocab = cf.vocab;
+      na.d = d;
+      na.norm_w = R.ffn_norm[l];
+      na.eps = cf.rms_eps;
+      na.res_out = R.resB;
+      na.out = R.xn;
+      CU(launch::norm_rows(na, M, c->stream));
+      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn, c->Fr, d, M, R.mb, c->Fr));
+      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb, d, c->Fr, M, R.dF, d));
+    }
+    OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
+  }
+  return SIRIUS_OK;
+}
+
+}  // namespace
+
+// ============================================================================= C ABI
+extern "C" {
+
+const char* sirius_version(void) { return "libsirius sm_100a (tcgen05 verify GEMM, bulk-copy GEMV, CATS FFN)"; }
+
+const char* sirius_last_error(const sirius_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+
+sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, const float* cats_threshold,
+                          void* nccl_comm, void* stream, sirius_ctx** out) {
+  if (!cfgp || !w || !cats_threshold || !out) return SIRIUS_ERR_INVALID_ARG;
+  *out = nullptr;
+  const sirius_config cf = *cfgp;
+  if (cf.vocab <= 0 || cf.d_model <= 0 || cf.n_layers <= 0 || cf.n_heads <= 0 || cf.n_kv_heads <= 0 ||
+      cf.head_dim <= 0 || cf.ffn_dim <= 0 || cf.batch <= 0 || cf.max_seq <= 0 || cf.max_gamma <= 0 ||
+      cf.tp_size <= 0 || cf.n_heads % cf.n_kv_heads || cf.rms_eps <= 0.f || cf.rope_theta <= 0.f)
+    return SIRIUS_ERR_INVALID_ARG;
+  if (cf.tp_rank < 0 || cf.tp_rank >= cf.tp_size) return SIRIUS_ERR_INVALID_ARG;
+  if (cf.n_heads % cf.tp_size || cf.n_kv_heads % cf.tp_size || cf.ffn_dim % cf.tp_size || cf.vocab % cf.tp_size)
+    return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.head_dim != 64 && cf.head_dim != 128) return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.d_model % 256 || ((cf.n_heads / cf.tp_size) * cf.head_dim) % 64 || (cf.ffn_dim / cf.tp_size) % 8)
+    return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.max_gamma > 64 || (long)cf.batch * cf.max_gamma > 256) return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4) return SIRIUS_ERR_UNSUPPORTED;
+  for (int l = 0; l < cf.n_layers; ++l)
+    if (!(cats_threshold[l] >= 0.f)) return SIRIUS_ERR_INVALID_ARG;
+  const bool emulate = cf.tp_size > 1 && nccl_comm == nullptr;
+  if (cf.tp_size > 1 && !emulate && !nccl().loaded) return SIRIUS_ERR_NCCL;
+
+  sirius_ctx* c = new sirius_ctx();
+  c->cfg = cf;
+  c->stream = (cudaStream_t)stream;
+  c->comm = nccl_comm;
+  c->emulated = emulate;
+  c->nranks = emulate ? cf.tp_size : 1;
+  c->Hr = cf.n_heads / cf.tp_size;
+  c->KVr = cf.n_kv_heads / cf.tp_size;
+  c->Fr = cf.ffn_dim / cf.tp_size;
+  c->Vr = cf.vocab / cf.tp_size;
+  c->G = cf.n_heads / cf.n_kv_heads;
+  c->Nqkv = (c->Hr + 2 * c->KVr) * cf.head_dim;
+  c->MAXM = 256;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  c->smem_optin = (size_t)optin - 1024;  // keep room for static shared memory
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) {
+    sirius_status s = fail(c, SIRIUS_ERR_UNSUPPORTED, "libsirius is built for sm_100a (B200) only");
+    delete c;
+    return s;
+  }
+  {
+    int total = cf.batch * c->KVr;
+    int s = (2 * c->num_sms + total - 1) / total;
+    c->attn_splits = s < 1 ? 1 : (s > 64 ? 64 : s);
+  }
+  auto cleanup_fail = [&](sirius_status s) {
+    sirius_destroy(c);
+    return s;
+  };
+  const int L = cf.n_layers, d = cf.d_model, hd = cf.head_dim, B = cf.batch;
+  // shared buffers
+  if (alloc(c, &c->thresholds, L) || alloc(c, &c->rope_cos, (size_t)cf.max_seq * hd / 2) ||
+      alloc(c, &c->rope_sin, (size_t)cf.max_seq * hd / 2) || alloc(c, &c->err_dev, 4) || alloc(c, &c->amax, 64) ||
+      alloc(c, &c->stats, (size_t)c->nranks * c->MAXM * c->accept_splits) ||
+      alloc(c, &c->stats_gather, (size_t)cf.tp_size * c->MAXM * c->accept_splits) ||
+      alloc(c, &c->dA_ptrs, 64) || alloc(c, &c->dF_ptrs, 64) || alloc(c, &c->pre_start, B) ||
+      alloc(c, &c->scratch_tok, 64))
+    return cleanup_fail(SIRIUS_ERR_CUDA);
+  if (cudaHostAlloc(&c->err_host, 64, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&c->pre_start_host, sizeof(int32_t) * B, cudaHostAllocDefault) != cudaSuccess)
+    return cleanup_fail(SIRIUS_ERR_CUDA);
+  *c->err_host = 0;
+  cudaMemcpy(c->thresholds, cats_threshold, sizeof(float) * L, cudaMemcpyHostToDevice);
+  {  // RoPE table: fp64 then rounded to fp32 (reading D16); rotate-half pairs (i, i + hd/2)
+    std::vector<float> cs((size_t)cf.max_seq * hd / 2), sn((size_t)cf.max_seq * hd / 2);
+    for (int p = 0; p < cf.max_seq; ++p)
+      for (int i = 0; i < hd / 2; ++i) {
+        const double inv = std::pow((double)cf.rope_theta, -2.0 * i / hd);
+        const double ang = (double)p * inv;
+        cs[(size_t)p * hd / 2 + i] = (float)std::cos(ang);
+        sn[(size_t)p * hd / 2 + i] = (float)std::sin(ang);
+      }
+    cudaMemcpy(c->rope_cos, cs.data(), sizeof(float) * cs.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(c->rope_sin, sn.data(), sizeof(float) * sn.size(), cudaMemcpyHostToDevice);
+  }
+  c->ranks.resize(c->nranks);
+  std::vector<float*> dA_h, dF_h;
+  const int ffn_grid = launch::ffn_grid(c->Fr, c->num_sms);
+  if (ffn_grid < 0) return cleanup_fail(SIRIUS_ERR_UNSUPPORTED);
+  for (int r = 0; r < c->nranks; ++r) {
+    RankState& R = c->ranks[r];
+    const sirius_weights& W = w[emulate ? r : 0];
+    R.rank = emulate ? r : cf.tp_rank;
+    if (!W.embed || !W.final_norm || !W.lm_head || !W.attn_norm || !W.w_qkv || !W.w_o || !W.ffn_norm || !W.w_gate ||
+        !W.w_up || !W.w_down)
+      return cleanup_fail(SIRIUS_ERR_INVALID_ARG);
+    R.embed = (const uint16_t*)W.embed;
+    R.final_norm = (const uint16_t*)W.final_norm;
+    R.lm_head = (const uint16_t*)W.lm_head;
+    for (int l = 0; l < L; ++l) {
+      const void* ptrs[7] = {W.attn_norm[l], W.w_qkv[l], W.w_o[l], W.ffn_norm[l], W.w_gate[l], W.w_up[l], W.w_down[l]};
+      for (const void* p : ptrs)
+        if (!p || ((uintptr_t)p & 15)) return cleanup_fail(SIRIUS_ERR_INVALID_ARG);
+      R.attn_norm.push_back((const uint16_t*)W.attn_norm[l]);
+      R.w_qkv.push_back((const uint16_t*)W.w_qkv[l]);
+      R.w_o.push_back((const uint16_t*)W.w_o[l]);
+      R.ffn_norm.push_back((const uint16_t*)W.ffn_norm[l]);
+      R.w_gate.push_back((const uint16_t*)W.w_gate[l]);
+      R.w_up.push_back((const uint16_t*)W.w_up[l]);
+      R.w_down.push_back((const uint16_t*)W.w_down[l]);
+    }
+    const size_t kv = (size_t)L * B * c->KVr * cf.max_seq * hd;
+    const size_t stg = (size_t)L * B * c->KVr * cf.max_gamma * hd;
+    const int M = c->MAXM;
+    const int row_blocks_max = (cf.max_gamma * c->G + 63) / 64 + (M * c->G + 63) / 64;
+    if (alloc(c, &R.k_cache, kv) || alloc(c, &R.v_cache, kv) || alloc(c, &R.stage_k, stg) ||
+        alloc(c, &R.stage_v, stg) || alloc(c, &R.resA, (size_t)M * d) || alloc(c, &R.resB, (size_t)M * d) ||
+        alloc(c, &R.dA, (size_t)M * d) || alloc(c, &R.dF, (size_t)M * d) || alloc(c, &R.qkv, (size_t)M * c->Nqkv) ||
+        alloc(c, &R.logits, (size_t)M * c->Vr) || alloc(c, &R.xn, (size_t)M * d) ||
+        alloc(c, &R.qb, (size_t)M * c->Hr * hd) || alloc(c, &R.ob, (size_t)M * c->Hr * hd) ||
+        alloc(c, &R.mb, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * 4 * d) ||
+        alloc(c, &R.ffn_cnt, (size_t)c->num_sms * 4) || alloc(c, &R.ffn_barrier, 8) ||
+        alloc(c, &R.attn_part, (size_t)B * c->KVr * 64 * 64 * (hd + 2) + (size_t)c->KVr * row_blocks_max * 32 * 64 * (hd + 2)) ||
+        alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) ||
+        alloc(c, &R.gemm_part, launch::gemm_workspace_bytes(c->num_sms) / sizeof(float)) ||
+        alloc(c, &R.gemm_cnt, (size_t)(c->Vr / 128 + 1024)) || alloc(c, &R.head_cnt, 16))
+      return cleanup_fail(SIRIUS_ERR_CUDA);
+    dA_h.push_back(R.dA);
+    dF_h.push_back(R.dF);
+    // transposed W_down ([d, F/tp], K-major in the neuron dim) for the verify down-projection GEMM
+    R.w_down_t.resize(L);
+    for (int l = 0; l < L; ++l) {
+      if (alloc(c, &R.w_down_t[l], (size_t)d * c->Fr, false)) return cleanup_fail(SIRIUS_ERR_CUDA);
+      if (launch::transpose_bf16(R.w_down[l], R.w_down_t[l], c->Fr, d, c->stream) != cudaSuccess)
+        return cleanup_fail(SIRIUS_ERR_CUDA);
+    }
+    // tensor maps: weights (box 128 rows) and activations (box 16 rows)
+    R.tm_qkv.resize(L);
+    R.tm_o.resize(L);
+    R.tm_gate.resize(L);
+    R.tm_up.resize(L);
+    R.tm_down.resize(L);
+    bool ok = true;
+    for (int l = 0; l < L; ++l) {
+      ok &= launch::make_tmap(R.tm_qkv[l].b, R.w_qkv[l], c->Nqkv, d, 128);
+      ok &= launch::make_tmap(R.tm_o[l].b, R.w_o[l], d, c->Hr * hd, 128);
+      ok &= launch::make_tmap(R.tm_gate[l].b, R.w_gate[l], c->Fr, d, 128);
+      ok &= launch::make_tmap(R.tm_up[l].b, R.w_up[l], c->Fr, d, 128);
+      ok &= launch::make_tmap(R.tm_down[l].b, R.w_down_t[l], d, c->Fr, 128);
+    }
+    ok &= launch::make_tmap(R.tm_head.b, R.lm_head, c->Vr, d, 128);
+    ok &= launch::make_tmap(R.tm_xn.b, R.xn, M, d, 16);
+    ok &= launch::make_tmap(R.tm_ob.b, R.ob, M, c->Hr * hd, 16);
+    ok &= launch::make_tmap(R.tm_mb.b, R.mb, M, c->Fr, 16);
+    if (!ok) {
+      c->last_error = "cuTensorMapEncodeTiled failed";
+      return cleanup_fail(SIRIUS_ERR_CUDA);
+    }
+  }
+  cudaMemcpy(c->dA_ptrs, dA_h.data(), sizeof(float*) * dA_h.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->dF_ptrs, dF_h.data(), sizeof(float*) * dF_h.size(), cudaMemcpyHostToDevice);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return cleanup_fail(SIRIUS_ERR_CUDA);
+  *out = c;
+  return SIRIUS_OK;
+}
+
+sirius_status sirius_destroy(sirius_ctx* c) {
+  if (!c) return SIRIUS_ERR_INVALID_ARG;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocations) cudaFree(p);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->pre_start_host) cudaFreeHost(c->pre_start_host);
+  delete c;
+  return SIRIUS_OK;
+}
+
+sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t* prompt_len, int32_t* first_token) {
+  if (!c || !tokens || !prompt_len || !first_token) return SIRIUS_ERR_INVALID_ARG;
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  long off = 0;
+  for (int b = 0; b < cf.batch; ++b) {
+    if (prompt_len[b] < 1) return fail(c, SIRIUS_ERR_INVALID_ARG, "prompt_len must be >= 1");
+    if (prompt_len[b] > cf.max_seq - cf.max_gamma) return fail(c, SIRIUS_ERR_CAPACITY, "prompt longer than max_seq - max_gamma");
+  }
+  const int d = cf.d_model;
+  for (int b = 0; b < cf.batch; ++b) {
+    const int P = prompt_len[b];
+    for (int s = 0; s < P; s += c->MAXM) {
+      const int rows = P - s < c->MAXM ? P - s : c->MAXM;
+      c->pre_start_host[b] = s;
+      CU(cudaMemcpyAsync(c->pre_start + b, c->pre_start_host + b, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+      OK(forward_rows(c, tokens + off + s, c->pre_start, b, 1, rows, true));
+      CU(cudaStreamSynchronize(c->stream));  // pre_start_host reuse
+      if (s + rows == P) {  // dense greedy next token from the last prompt row (reading D17)
+        for (auto& R : c->ranks) {
+          GemvArgs a = {};
+          a.pro.mode = IN_RESID;
+          a.pro.base = R.resB + (size_t)(rows - 1) * d;
+          a.pro.delta = R.dF + (size_t)(rows - 1) * d;
+          a.pro.norm_w = R.final_norm;
+          a.pro.eps = cf.rms_eps;
+          a.W = R.lm_head;
+          a.rows = c->Vr;
+          a.K = d;
+          a.epi = EPI_ARGMAX;
+          a.ldo = c->Vr;
+          a.amax = c->amax;
+          a.index_offset = (uint32_t)R.rank * c->Vr;
+          a.finalize = (cf.tp_size == 1);
+          a.done_counter = R.head_cnt;
+          a.token_out = first_token + b;
+          OK(run_gemv(c, a, 1));
+        }
+        if (cf.tp_size > 1) {
+          if (!c->emulated) {
+            NcclApi& api = nccl();
+            int r = api.allReduce(c->amax, c->amax, 1, kNcclUint64, kNcclMax, c->comm, c->stream);
+            if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllReduce(max)");
+          }
+          CU(launch::argmax_finalize(c->amax, 1, first_token + b, c->stream));
+        }
+      }
+    }
+    off += P;
+  }
+  mirror_err(c);
+  CU(cudaGetLastError());
+  c->prefilled = true;
+  c->have_correct = false;
+  return SIRIUS_OK;
+}
+
+sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
+                                 int32_t* token_out, float* logits_out, int32_t* n_active_out, float* gate_act_out) {
+  if (!c || !token_in || !pos || !token_out) return SIRIUS_ERR_INVALID_ARG;
+  if (flags & ~(uint32_t)SIRIUS_DENSE) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  const int B = cf.batch, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
+  const bool dense = flags & SIRIUS_DENSE;
+  if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
+  const int ffn_grid = launch::ffn_grid(c->Fr, c->num_sms);
+  const int ffn_nslot = launch::ffn_nslot(B, d, c->smem_optin);
+  if (ffn_nslot < 2) return fail(c, SIRIUS_ERR_UNSUPPORTED, "ffn: row too large for shared memory");
+  for (int l = 0; l < L; ++l) {
+    for (auto& R : c->ranks) {
+      GemvArgs a = {};
+      if (l == 0) {
+        a.pro.mode = IN_EMBED;
+        a.pro.tokens = token_in;
+        a.pro.embed = R.embed;
+        a.pro.vocab = cf.vocab;
+      } else {
+        a.pro.mode = IN_RESID;
+        a.pro.base = R.resB;
+        a.pro.delta = R.dF;
+      }
+      a.pro.norm_w = R.attn_norm[l];
+      a.pro.eps = cf.rms_eps;
+      a.pro.res_out = R.resA;
+      a.W = R.w_qkv[l];
+      a.rows = c->Nqkv;
+      a.K = d;
+      a.epi = EPI_STORE;
+      a.out = R.qkv;
+      a.ldo = c->Nqkv;
+      OK(run_gemv(c, a, B));
+      AttnArgs at = {};
+      const size_t kv_layer = (size_t)B * c->KVr * cf.max_seq * hd;
+      at.qkv = R.qkv;
+      at.pos = pos;
+      at.rope_cos = c->rope_cos;
+      at.rope_sin = c->rope_sin;
+      at.k_cache = R.k_cache + l * kv_layer;
+      at.v_cache = R.v_cache + l * kv_layer;
+      at.Hr = c->Hr;
+      at.KVr = c->KVr;
+      at.max_seq = cf.max_seq;
+      at.splits = c->attn_splits;
+      at.part = R.attn_part;
+      at.counters = R.attn_cnt;
+      at.out = R.ob;
+      at.err = c->err_dev;
+      CU(launch::attn_decode(at, B, hd, c->G, c->stream));
+      GemvArgs o = {};
+      o.pro.mode = IN_BF16;
+      o.pro.in_bf16 = R.ob;
+      o.W = R.w_o[l];
+      o.rows = d;
+      o.K = c->Hr * hd;
+      o.epi = EPI_STORE;
+      o.out = R.dA;
+      o.ldo = d;
+      OK(run_gemv(c, o, B));
+    }
+    OK(allreduce(c, &RankState::dA, c->dA_ptrs, B));
+    for (auto& R : c->ranks) {
+      FfnArgs f = {};
+      f.pro.mode = IN_RESID;
+      f.pro.base = R.resA;
+      f.pro.delta = R.dA;
+      f.pro.norm_w = R.ffn_norm[l];
+      f.pro.eps = cf.rms_eps;
+      f.pro.res_out = R.resB;
+      f.w_gate = R.w_gate[l];
+      f.w_up = R.w_up[l];
+      f.w_down = R.w_down[l];
+      f.F = c->Fr;
+      f.d = d;
+      f.threshold = c->thresholds + l;
+      f.dense = dense ? 1 : 0;
+      f.part = R.ffn_part;
+      f.part_cnt = R.ffn_cnt;
+      f.barrier = R.ffn_barrier;
+      f.out = R.dF;
+      f.n_active_out = n_active_out ? n_active_out + l : nullptr;
+      f.n_active_stride = L;
+      if (gate_act_out) {  // [B, L, F] (emulated group: rank shards concatenated) or [B, L, F/tp]
+        const int F = c->emulated ? cf.ffn_dim : c->Fr;
+        f.gate_out = gate_act_out + (size_t)l * F + (c->emulated ? (size_t)R.rank * c->Fr : 0);
+        f.gate_stride = (long long)L * F;
+      }
+      CU(launch::ffn(f, B, ffn_grid, ffn_nslot, c->stream));
+    }
+    OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
+  }
+  for (auto& R : c->ranks) {
+    GemvArgs a = {};
+    a.pro.mode = IN_RESID;
+    a.pro.base = R.resB;
+    a.pro.delta = R.dF;
+    a.pro.norm_w = R.final_norm;
+    a.pro.eps = cf.rms_eps;
+    a.W = R.lm_head;
+    a.rows = c->Vr;
+    a.K = d;
+    a.epi = EPI_ARGMAX;
+    a.out = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : nullptr;
+    a.ldo = c->emulated ? cf.vocab : c->Vr;
+    a.amax = c->amax;
+    a.index_offset = (uint32_t)R.rank * c->Vr;
+    a.finalize = (cf.tp_size == 1);
+    a.done_counter = R.head_cnt;
+    a.token_out = token_out;
+    OK(run_gemv(c, a, B));
+  }
+  if (cf.tp_size > 1) {
+    if (!c->emulated) {
+      NcclApi& api = nccl();
+      int r = api.allReduce(c->amax, c->amax, B, kNcclUint64, kNcclMax, c->comm, c->stream);
+      if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllReduce(max)");
+    }
+    CU(launch::argmax_finalize(c->amax, B, token_out, c->stream));
+  }
+  CU(cudaGetLastError());
+  return SIRIUS_OK;
+}
+
+sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const int32_t* start_pos, int32_t gamma,
+                             float accept_threshold, int32_t accept_mode, int32_t* n_accept_out,
+                             int32_t* next_token_out, float* q_out, float* logits_out) {
+  if (!c || !kernel_tokens || !start_pos || !n_accept_out || !next_token_out) return SIRIUS_ERR_INVALID_ARG;
+  if (accept_mode != SIRIUS_ACCEPT_THRESHOLD && accept_mode != SIRIUS_ACCEPT_EXACT_ARGMAX)
+    return fail(c, SIRIUS_ERR_INVALID_ARG, "accept_mode");
+  if (!(accept_threshold >= 0.f && accept_threshold <= 1.f)) return fail(c, SIRIUS_ERR_INVALID_ARG, "r outside [0,1]");
+  if (gamma < 1) return fail(c, SIRIUS_ERR_INVALID_ARG, "gamma < 1");
+  if (gamma > c->cfg.max_gamma) return fail(c, SIRIUS_ERR_CAPACITY, "gamma > max_gamma");
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  const int B = cf.batch, d = cf.d_model, M = B * gamma;
+  OK(forward_rows(c, kernel_tokens, start_pos, 0, B, gamma, false));
+  for (auto& R : c->ranks) {
+    NormRowsArgs na = {};
+    na.base = R.resB;
+    na.delta = R.dF;
+    na.vocab = cf.vocab;
+    na.d = d;
+    na.norm_w = R.final_norm;
+    na.eps = cf.rms_eps;
+    na.out = R.xn;
+    CU(launch::norm_rows(na, M, c->stream));
+    float* lo = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : R.logits;
+    const int ldl = logits_out ? (c->emulated ? cf.vocab : c->Vr) : c->Vr;
+    OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn, c->Vr, d, M, lo, ldl));
+    AcceptStatsArgs as = {};
+    as.logits = lo;
+    as.ldl = ldl;
+    as.Vr = c->Vr;
+    as.voff = R.rank * c->Vr;
+    as.M = M;
+    as.gamma = gamma;
+    as.rank = c->emulated ? R.rank : 0;
+    as.tokens = kernel_tokens;
+    as.stats = c->stats;
+    CU(launch::accept_stats(as, c->accept_splits, c->stream));
+  }
+  const RowStat* stats = c->stats;
+  int nranks = c->nranks;
+  if (cf.tp_size > 1 && !c->emulated) {
+    NcclApi& api = nccl();
+    int r = api.allGather(c->stats, c->stats_gather, (size_t)M * c->accept_splits * sizeof(RowStat), kNcclUint8,
+                          c->comm, c->stream);
+    if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllGather(stats)");
+    stats = c->stats_gather;
+    nranks = cf.tp_size;
+  }
+  AcceptFinalArgs fa = {};
+  fa.stats = stats;
+  fa.nranks = nranks;
+  fa.S = c->accept_splits;
+  fa.M = M;
+  fa.gamma = gamma;
+  fa.mode = accept_mode;
+  fa.r = accept_threshold;
+  fa.tokens = kernel_tokens;
+  fa.n_accept = n_accept_out;
+  fa.next_token = next_token_out;
+  fa.q_out = q_out;
+  CU(launch::accept_finalize(fa, B, c->stream));
+  mirror_err(c);
+  CU(cudaGetLastError());
+  c->last_gamma = gamma;
+  c->have_correct = true;
+  return SIRIUS_OK;
+}
+
+sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t* n_rows) {
+  if (!c || !start_pos || !n_rows) return SIRIUS_ERR_INVALID_ARG;
+  if (!c->have_correct) return fail(c, SIRIUS_ERR_STATE, "kv_rewrite without a preceding correct_kernel");
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  for (auto& R : c->ranks) {
+    KvRewriteArgs a = {};
+    a.stage_k = R.stage_k;
+    a.stage_v = R.stage_v;
+    a.k_cache = R.k_cache;
+    a.v_cache = R.v_cache;
+    a.start = start_pos;
+    a.n_rows = n_rows;
+    a.B = cf.batch;
+    a.KVr = c->KVr;
+    a.hd = cf.head_dim;
+    a.max_seq = cf.max_seq;
+    a.max_gamma = cf.max_gamma;
+    a.gamma = c->last_gamma;
+    a.err = c->err_dev;
+    CU(launch::kv_rewrite(a, cf.n_layers, c->stream));
+  }
+  mirror_err(c);
+  CU(cudaGetLastError());
+  c->have_correct = false;
+  return SIRIUS_OK;
+}
+
+// ---------------------------------------------------------------- NCCL bootstrap helpers (X4)
+int sirius_nccl_available(void) { return nccl().loaded ? 1 : 0; }
+int sirius_nccl_unique_id(void* out128) {
+  NcclApi& api = nccl();
+  if (!api.loaded) return -1;
+  return api.getUniqueId(out128);
+}
+int sirius_nccl_comm_init(int nranks, const void* id128, int rank, void** comm_out) {
+  NcclApi& api = nccl();
+  if (!api.loaded) return -1;
+  char id[128];
+  memcpy(id, id128, 128);
+  return api.commInitRank(comm_out, nranks, id, rank);
+}
+int sirius_nccl_comm_destroy(void* comm) {
+  NcclApi& api = nccl();
+  if (!api.loaded || !api.commDestroy) return -1;
+  return api.commDestroy(comm);
+}
+
+// ---------------------------------------------------------------- test-only entry: the tcgen05 GEMM
+// out[m, n] = sum_k X[m, k] W[n, k] (fp32), or (W2 != NULL) bf16(SiLU(X W^T) * (X W2^T)).
+// X: DEV bf16 [x_rows >= M, K]; W, W2: DEV bf16 [N, K].  Synchronous.  Returns cudaError_t.
+int sirius_debug_gemm(const void* X, int x_rows, const void* Wt, const void* W2, void* out, int M, int N, int K) {
+  static float* part = nullptr;
+  static unsigned* cnt = nullptr;
+  int dev = 0, sms = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (!part) {
+    if (cudaMalloc(&part, launch::gemm_workspace_bytes(sms))) return -1;
+    if (cudaMalloc(&cnt, 65536 * sizeof(unsigned))) return -1;
+    cudaMemset(cnt, 0, 65536 * sizeof(unsigned));
+  }
+  TmapBuf ta, tb, tx;
+  if (!launch::make_tmap(ta.b, Wt, N, K, 128) || !launch::make_tmap(tx.b, X, x_rows, K, 16)) return -2;
+  if (W2 && !launch::make_tmap(tb.b, W2, N, K, 128)) return -2;
+  GemmArgs g;
+  g.N = N;
+  g.K = K;
+  g.M = M;
+  g.n_tiles = (N + 127) / 128;
+  g.kb = (K + 63) / 64;
+  g.out = out;
+  g.ldc = N;
+  g.part = part;
+  g.counters = cnt;
+  cudaError_t e = launch::gemm(ta.b, W2 ? tb.b : nullptr, tx.b, g, round_up(M, 16), sms, (size_t)optin - 1024, 0);
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaDeviceSynchronize();
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// verify_kernels.cuh — argument structs of verify_kernels.cu.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sirius {
+
+struct NormRowsArgs {
+  const float* base;       // [M, d] residual or NULL (embed mode)
+  const float* delta;      // [M, d] or NULL
+  const int32_t* tokens;   // embed mode: [M] token ids (else NULL)
+  const uint16_t* embed;   // [V, d]
+  int vocab, d;
+  const uint16_t* norm_w;  // [d]
+  float eps;
+  float* res_out;          // [M, d] or NULL
+  uint16_t* out;           // [M, d] bf16
+};
+
+struct RopeStoreArgs {
+  const float* qkv;        // [M, (Hr + 2 KVr) * hd]
+  const int32_t* start;    // [B] first position of each sequence's rows
+  int b_base, rows_per_seq;
+  const float* rope_cos;   // [max_seq, hd/2]
+  const float* rope_sin;
+  int Hr, KVr, hd, max_seq, max_gamma;
+  int to_cache;            // 1: K/V -> cache slots pos (prefill); 0: -> staging row i (verify)
+  uint16_t* q_out;         // [M, Hr * hd]
+  uint16_t* k_dst;         // this layer's cache [B, KVr, max_seq, hd] or staging [B, KVr, max_gamma, hd]
+  uint16_t* v_dst;
+  int* err;
+};
+
+struct AttnRowsArgs {
+  const uint16_t* q;        // [nseq * rows, Hr * hd] bf16 (post-RoPE)
+  const int32_t* start;     // [B]  T of each sequence
+  int b_base, rows_per_seq, G, Hr, KVr, max_seq;
+  const uint16_t* k_cache;  // this layer [B, KVr, max_seq, hd]
+  const uint16_t* v_cache;
+  const uint16_t* k_fresh;  // staging [B, KVr, fresh_stride, hd] (ignored if fresh_in_cache)
+  const uint16_t* v_fresh;
+  int fresh_stride, fresh_in_cache;
+  float* part;              // workspace
+  unsigned* counters;       // [nseq * KVr * row_blocks]
+  uint16_t* out;            // [nseq * rows, Hr * hd] bf16
+};
+
+struct RowStat {
+  float mx, sum, ld, pad;
+  unsigned long long key;
+};
+
+struct AcceptStatsArgs {
+  const float* logits;     // [M, ldl] (this rank's vocab shard in columns [0, Vr))
+  int ldl, Vr, voff, M, gamma, rank;
+  const int32_t* tokens;   // [B, gamma] kernel tokens
+  RowStat* stats;          // [nranks, M, S]
+};
+
+struct AcceptFinalArgs {
+  const RowStat* stats;
+  int nranks, S, M, gamma, mode;
+  float r;
+  const int32_t* tokens;
+  int32_t* n_accept;
+  int32_t* next_token;
+  float* q_out;
+};
+
+struct KvRewriteArgs {
+  const uint16_t* stage_k;  // [L, B, KVr, max_gamma, hd]
+  const uint16_t* stage_v;
+  uint16_t* k_cache;        // [L, B, KVr, max_seq, hd]
+  uint16_t* v_cache;
+  const int32_t* start;
+  const int32_t* n_rows;
+  int B, KVr, hd, max_seq, max_gamma, gamma;
+  int* err;
+};
+
+namespace launch {
+cudaError_t norm_rows(const NormRowsArgs& a, int M, cudaStream_t st);
+cudaError_t rope_store(const RopeStoreArgs& a, int M, cudaStream_t st);
+cudaError_t attn_rows(const AttnRowsArgs& a, int nseq, int hd, int splits, int row_blocks, cudaStream_t st);
+cudaError_t accept_stats(const AcceptStatsArgs& a, int splits, cudaStream_t st);
+cudaError_t accept_finalize(const AcceptFinalArgs& a, int B, cudaStream_t st);
+cudaError_t kv_rewrite(const KvRewriteArgs& a, int L, cudaStream_t st);
+cudaError_t transpose_bf16(const uint16_t* in, uint16_t* out, int R, int C, cudaStream_t st);
+cudaError_t sum_ranks(float* const* bufs_dev, int nranks, size_t rows, size_t width, size_t ld, cudaStream_t st);
+}  // namespace launch
+}  // namespace sirius

@@ -1,0 +1,179 @@
+"""Thin ctypes binding of libsirius (include/sirius.h): argument marshalling only.
+
+Every entry point has the C name: ``sirius_init``, ``sirius_prefill``, ``sparse_decode_step``,
+``correct_kernel``, ``kv_rewrite``, ``sirius_destroy``.  Tensors are torch CUDA tensors (torch is
+used for device memory and streams only); the library is loaded from this directory and nothing
+falls back to the CPU: if the CUDA library or a GPU is missing, ``load()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsirius.so")
+
+SIRIUS_OK = 0
+STATUS = {0: "OK", -1: "INVALID_ARG", -2: "CAPACITY", -3: "STATE", -4: "CUDA", -5: "NCCL", -6: "UNSUPPORTED"}
+SIRIUS_DENSE = 1
+ACCEPT_THRESHOLD = 0
+ACCEPT_EXACT_ARGMAX = 1
+
+# every symbol include/sirius.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
+               "sirius_destroy", "sirius_last_error", "sirius_version")
+
+
+class SiriusError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"sirius status {status} ({STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class SiriusConfig(ctypes.Structure):
+    _fields_ = [("vocab", ctypes.c_int32), ("d_model", ctypes.c_int32), ("n_layers", ctypes.c_int32),
+                ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("ffn_dim", ctypes.c_int32), ("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float),
+                ("batch", ctypes.c_int32), ("max_seq", ctypes.c_int32), ("max_gamma", ctypes.c_int32),
+                ("tp_size", ctypes.c_int32), ("tp_rank", ctypes.c_int32)]
+
+
+_PP = ctypes.POINTER(ctypes.c_void_p)
+
+
+class SiriusWeights(ctypes.Structure):
+    _fields_ = [("embed", ctypes.c_void_p), ("final_norm", ctypes.c_void_p), ("lm_head", ctypes.c_void_p),
+                ("attn_norm", _PP), ("w_qkv", _PP), ("w_o", _PP), ("ffn_norm", _PP), ("w_gate", _PP),
+                ("w_up", _PP), ("w_down", _PP)]
+
+
+_lib = None
+
+
+def load():
+    """Load libsirius.so (built in-tree by __graft_entry__.build()).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I, U, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_float
+        lib.sirius_init.argtypes = [ctypes.POINTER(SiriusConfig), ctypes.POINTER(SiriusWeights), P, P, P,
+                                    ctypes.POINTER(P)]
+        lib.sirius_init.restype = I
+        lib.sirius_prefill.argtypes = [P, P, P, P]
+        lib.sirius_prefill.restype = I
+        lib.sparse_decode_step.argtypes = [P, P, P, U, P, P, P, P]
+        lib.sparse_decode_step.restype = I
+        lib.correct_kernel.argtypes = [P, P, P, I, F, I, P, P, P, P]
+        lib.correct_kernel.restype = I
+        lib.kv_rewrite.argtypes = [P, P, P]
+        lib.kv_rewrite.restype = I
+        lib.sirius_destroy.argtypes = [P]
+        lib.sirius_destroy.restype = I
+        lib.sirius_last_error.argtypes = [P]
+        lib.sirius_last_error.restype = ctypes.c_char_p
+        lib.sirius_version.argtypes = []
+        lib.sirius_version.restype = ctypes.c_char_p
+        lib.sirius_debug_gemm.argtypes = [P, I, P, P, P, I, I, I]
+        lib.sirius_debug_gemm.restype = I
+        lib.sirius_nccl_available.restype = I
+        lib.sirius_nccl_unique_id.argtypes = [P]
+        lib.sirius_nccl_unique_id.restype = I
+        lib.sirius_nccl_comm_init.argtypes = [I, P, I, ctypes.POINTER(P)]
+        lib.sirius_nccl_comm_init.restype = I
+        lib.sirius_nccl_comm_destroy.argtypes = [P]
+        lib.sirius_nccl_comm_destroy.restype = I
+        _lib = lib
+    return _lib
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class Sirius:
+    """One libsirius context (one GPU / TP rank, or a whole TP group emulated on one GPU)."""
+
+    def __init__(self, cfg, weights, thresholds: Sequence[float], batch: int, max_seq: int, max_gamma: int,
+                 tp_size: int = 1, tp_rank: int = 0, nccl_comm: Optional[int] = None, stream=None):
+        import torch
+        lib = load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("libsirius needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.cfg = cfg
+        self.batch, self.max_seq, self.max_gamma = batch, max_seq, max_gamma
+        self.tp_size, self.tp_rank = tp_size, tp_rank
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        c = SiriusConfig(cfg.vocab, cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                         cfg.ffn_dim, cfg.rope_theta, cfg.rms_eps, batch, max_seq, max_gamma, tp_size, tp_rank)
+        shards = weights if isinstance(weights, (list, tuple)) else [weights]
+        self._keep = []  # keep ctypes arrays alive for the context's lifetime
+        arr = (SiriusWeights * len(shards))()
+        L = cfg.n_layers
+        for i, w in enumerate(shards):
+            per = {}
+            for n in ("attn_norm", "w_qkv", "w_o", "ffn_norm", "w_gate", "w_up", "w_down"):
+                a = (ctypes.c_void_p * L)(*[w[f"layers.{l}.{n}"].data_ptr() for l in range(L)])
+                self._keep.append(a)
+                per[n] = ctypes.cast(a, _PP)
+            arr[i] = SiriusWeights(w["embed"].data_ptr(), w["final_norm"].data_ptr(), w["lm_head"].data_ptr(),
+                                   per["attn_norm"], per["w_qkv"], per["w_o"], per["ffn_norm"], per["w_gate"],
+                                   per["w_up"], per["w_down"])
+        self._weights = shards
+        thr = (ctypes.c_float * L)(*[float(t) for t in thresholds])
+        h = ctypes.c_void_p()
+        st = lib.sirius_init(ctypes.byref(c), arr, thr, nccl_comm, ctypes.c_void_p(self.stream.cuda_stream),
+                             ctypes.byref(h))
+        if st != SIRIUS_OK:
+            raise SiriusError(st, "sirius_init failed")
+        self.h = h
+        self.lib = lib
+
+    def _check(self, st: int):
+        if st != SIRIUS_OK:
+            raise SiriusError(st, self.lib.sirius_last_error(self.h).decode())
+
+    def last_error(self) -> str:
+        return self.lib.sirius_last_error(self.h).decode()
+
+    # ---- C ABI, same names ------------------------------------------------------------
+    def sirius_prefill(self, tokens, prompt_len: Sequence[int], first_token):
+        lens = (ctypes.c_int32 * len(prompt_len))(*prompt_len)
+        self._check(self.lib.sirius_prefill(self.h, _ptr(tokens), lens, _ptr(first_token)))
+
+    def sparse_decode_step(self, token_in, pos, flags: int, token_out, logits_out=None, n_active_out=None,
+                           gate_act_out=None):
+        self._check(self.lib.sparse_decode_step(self.h, _ptr(token_in), _ptr(pos), flags, _ptr(token_out),
+                                                _ptr(logits_out), _ptr(n_active_out), _ptr(gate_act_out)))
+
+    def correct_kernel(self, kernel_tokens, start_pos, gamma: int, accept_threshold: float, accept_mode: int,
+                       n_accept_out, next_token_out, q_out=None, logits_out=None):
+        self._check(self.lib.correct_kernel(self.h, _ptr(kernel_tokens), _ptr(start_pos), gamma,
+                                            accept_threshold, accept_mode, _ptr(n_accept_out),
+                                            _ptr(next_token_out), _ptr(q_out), _ptr(logits_out)))
+
+    def kv_rewrite(self, start_pos, n_rows):
+        self._check(self.lib.kv_rewrite(self.h, _ptr(start_pos), _ptr(n_rows)))
+
+    def sirius_destroy(self):
+        if getattr(self, "h", None):
+            self.lib.sirius_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.sirius_destroy()
+        except Exception:
+            pass
+
+
+def debug_gemm(X, W, out, M: int, W2=None) -> None:
+    """Test-only: out = X[:M] @ W.T (fp32) or bf16(SiLU(X W^T) * (X W2^T)) via the tcgen05 kernel."""
+    lib = load()
+    N, K = W.shape
+    r = lib.sirius_debug_gemm(X.data_ptr(), X.shape[0], W.data_ptr(), _ptr(W2), out.data_ptr(), M, N, K)
+    if r != 0:
+        raise RuntimeError(f"sirius_debug_gemm failed: {r}")

@@ -1,0 +1,59 @@
+"""Kernel-isolated numerics of the tcgen05 verify GEMM against a plain fp64 PyTorch CPU reference
+of the same op (out = X W^T, and the fused SwiGLU dual GEMM)."""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (M tokens, N weight rows, K) — several tiles, ragged tails, split-K/stream-K cuts
+    (1, 128, 256), (4, 512, 256), (16, 6144, 4096), (20, 688, 256), (16, 4096, 14336), (64, 1280, 1024),
+    (128, 256, 688), (256, 1024, 512), (48, 128256 // 8, 4096),
+]
+
+
+def _ref(X, W, M):
+    return X[:M].double().cpu() @ W.double().cpu().T
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_matches_fp64_reference(M, N, K):
+    from paper_2409_03856_b200 import sirius as S
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
+    rows = max(16, (M + 15) // 16 * 16)
+    X = (torch.randn(rows, K, generator=g) * 0.5).to(torch.bfloat16).cuda()
+    W = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16).cuda()
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    S.debug_gemm(X, W, out, M)
+    ref = _ref(X, W, M)
+    err = (out.double().cpu() - ref).abs()
+    # fp32 accumulation of K bf16 products: |err| <= K * 2^-24 * sum|x w| (generous bound used: 1e-5 * sqrt(K) scale)
+    bound = 2e-6 * K ** 0.5 * 4 + 1e-5 * ref.abs()
+    assert torch.isfinite(out).all()
+    assert (err <= bound).all(), float(err.max())
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 14336 // 8, 4096), (5, 688, 256), (64, 512, 1024)])
+def test_dual_swiglu_gemm(M, N, K):
+    from paper_2409_03856_b200 import sirius as S
+    g = torch.Generator(device="cpu").manual_seed(1 + M + N)
+    X = (torch.randn(256, K, generator=g)).to(torch.bfloat16).cuda()
+    W1 = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16).cuda()
+    W2 = (torch.randn(N, K, generator=g) / K ** 0.5).to(torch.bfloat16).cuda()
+    out = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+    S.debug_gemm(X, W1, out, M, W2=W1 if False else W2)
+    gte = _ref(X, W1, M)
+    up = _ref(X, W2, M)
+    ref = gte / (1 + torch.exp(-gte)) * up
+    err = (out.double().cpu() - ref).abs()
+    assert (err <= 1e-2 * ref.abs() + 1e-3).all(), float(err.max())
+
+
+def test_gemm_deterministic():
+    from paper_2409_03856_b200 import sirius as S
+    X = torch.randn(16, 4096).to(torch.bfloat16).cuda()
+    W = (torch.randn(4096, 4096) / 64).to(torch.bfloat16).cuda()
+    a = torch.empty((16, 4096), device="cuda")
+    b = torch.empty((16, 4096), device="cuda")
+    S.debug_gemm(X, W, a, 16)
+    S.debug_gemm(X, W, b, 16)
+    assert torch.equal(a, b)

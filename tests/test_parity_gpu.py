@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element, on the
+same seeded inputs (SURVEY.md §8(c) parity rules; north_star tolerances):
+  * logits  |l_gpu - l_ref| <= 2e-2 + 1e-2 |l_ref|
+  * argmax / drafted token pinned iff the oracle's top-2 margin > 2 eps_row (else an ambiguity event)
+  * active set: every mismatch explained, | |a_ref| - t | <= |a_gpu - a_ref|; a within 1e-3 + 1e-3|a|
+  * accept decision pinned iff |ln q_ref - ln r| > 2 eps_row + 1e-5
+  * token sequences identical when no ambiguity event occurred
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import sirius_oracle as so
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ABS, REL = 2e-2, 1e-2
+
+
+@pytest.fixture(scope="module")
+def tiny_models():
+    from synth import gpu as sg
+    cfg = synth.TINY
+    wh = synth.host_weights(cfg)
+    wd = sg.device_weights(cfg)
+    return cfg, wh, wd
+
+
+def make_ctx(cfg, wd, thr, batch=1, max_seq=256, max_gamma=16, tp=1):
+    from paper_2409_03856_b200 import sirius as S
+    return S.Sirius(cfg, wd, thr, batch=batch, max_seq=max_seq, max_gamma=max_gamma, tp_size=tp)
+
+
+def check_logits(gpu, ref):
+    err = np.abs(gpu - ref)
+    assert np.all(err <= ABS + REL * np.abs(ref)), (err.max(), np.argmax(err))
+    return float(err.max())
+
+
+def pinned_argmax(ref, eps):
+    s = np.sort(ref)
+    return (s[-1] - s[-2]) > 2 * eps
+
+
+def test_weights_on_device_equal_host(tiny_models):
+    cfg, wh, wd = tiny_models
+    for k in wh:
+        np.testing.assert_array_equal(wd[k].view(torch.int16).cpu().numpy().view(np.uint16).reshape(wh[k].shape), wh[k])
+
+
+def test_prefill_and_decode_lockstep(tiny_models):
+    """Teacher-forced: the GPU and the oracle decode the same tokens; compare logits, gate
+    activations, active sets and argmax every step, sparse and dense."""
+    from paper_2409_03856_b200 import sirius as S
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, [0.5, 0.35])  # distinct per-layer thresholds
+    prompt = synth.eval_prompt(cfg, 0, 64)
+    ctx = make_ctx(cfg, wd, thr)
+    om = so.OracleModel(cfg, wh, max_seq=256, max_gamma=16)
+    ref_pre = om.prefill(prompt)
+    first = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(torch.tensor(prompt, device="cuda"), [len(prompt)], first)
+    torch.cuda.synchronize()
+    l_last = ref_pre[-1]
+    assert not pinned_argmax(l_last, 0.05) or int(first.item()) == so.argmax_lowest(l_last)
+    tok = so.argmax_lowest(l_last)
+    L, F = cfg.n_layers, cfg.ffn_dim
+    n_mis = 0
+    for step in range(12):
+        sparse = step % 3 != 2
+        pos = len(prompt) + step
+        r = om.decode(tok, pos, sparse, thr, want_gate=True, want_mask=True)
+        ti = torch.tensor([tok], dtype=torch.int32, device="cuda")
+        pi = torch.tensor([pos], dtype=torch.int32, device="cuda")
+        to = torch.zeros(1, dtype=torch.int32, device="cuda")
+        lo = torch.zeros((1, cfg.vocab), dtype=torch.float32, device="cuda")
+        na = torch.zeros((1, L), dtype=torch.int32, device="cuda")
+        ga = torch.zeros((1, L, F), dtype=torch.float32, device="cuda")
+        ctx.sparse_decode_step(ti, pi, 0 if sparse else S.SIRIUS_DENSE, to, lo, na, ga)
+        torch.cuda.synchronize()
+        lg = lo.cpu().numpy()[0]
+        eps = check_logits(lg, r.logits)
+        a_gpu = ga.cpu().numpy()[0]
+        assert np.all(np.abs(a_gpu - r.gate) <= 1e-3 + 1e-3 * np.abs(r.gate))
+        if sparse:
+            act_gpu = np.abs(a_gpu) >= thr[:, None]
+            mism = act_gpu != r.mask.astype(bool)
+            n_mis += int(mism.sum())
+            # a mismatch is only allowed where the float error explains it
+            assert np.all(np.abs(np.abs(r.gate[mism]) - np.repeat(thr[:, None], F, 1)[mism])
+                          <= np.abs(a_gpu[mism] - r.gate[mism]) + 1e-7)
+            assert np.array_equal(na.cpu().numpy()[0], act_gpu.sum(1))
+        else:
+            assert np.all(na.cpu().numpy()[0] == F)
+        if pinned_argmax(r.logits, eps):
+            assert int(to.item()) == so.argmax_lowest(r.logits)
+        assert int(to.item()) == int(np.argmax(lg))
+        tok = so.argmax_lowest(r.logits)
+    assert n_mis <= 4
+
+
+def test_verify_accept_rewrite_lockstep(tiny_models):
+    """correct_kernel logits / q / j against the oracle's verify + accept scan; then kv_rewrite and a
+    further decode step match the oracle (which rewrote the same rows)."""
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 1, 48)
+    gamma = 6
+    ctx = make_ctx(cfg, wd, thr)
+    om = so.OracleModel(cfg, wh, max_seq=256, max_gamma=16)
+    om.prefill(prompt)
+    first = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(torch.tensor(prompt, device="cuda"), [len(prompt)], first)
+    T = len(prompt)
+    ins = [int(first.item())]
+    for i in range(gamma - 1):  # oracle drafts; GPU decodes the same tokens (teacher forcing)
+        r = om.decode(ins[i], T + i, True, thr)
+        ctx.sparse_decode_step(torch.tensor([ins[i]], dtype=torch.int32, device="cuda"),
+                               torch.tensor([T + i], dtype=torch.int32, device="cuda"), 0,
+                               torch.zeros(1, dtype=torch.int32, device="cuda"))
+        ins.append(so.argmax_lowest(r.logits))
+    lf = om.verify(ins, T)
+    for rr in (0.0, 0.05, 0.3, 0.9):
+        j_ref, q_ref = so.accept_scan(lf, ins, rr)
+        kt = torch.tensor([ins], dtype=torch.int32, device="cuda")
+        st = torch.tensor([T], dtype=torch.int32, device="cuda")
+        na, nx = torch.zeros(1, dtype=torch.int32, device="cuda"), torch.zeros(1, dtype=torch.int32, device="cuda")
+        q = torch.zeros((1, gamma), dtype=torch.float32, device="cuda")
+        lo = torch.zeros((1, gamma, cfg.vocab), dtype=torch.float32, device="cuda")
+        ctx.correct_kernel(kt, st, gamma, rr, 0, na, nx, q, lo)
+        torch.cuda.synchronize()
+        lg = lo.cpu().numpy()[0]
+        eps = max(check_logits(lg[i], lf[i]) for i in range(gamma))
+        qg = q.cpu().numpy()[0]
+        np.testing.assert_allclose(qg, q_ref, rtol=0.05, atol=1e-4)
+        # decision pinned unless ln q lies within the float band around ln r
+        pinned = all(abs(np.log(max(q_ref[i], 1e-30)) - np.log(rr)) > 2 * eps + 1e-5
+                     for i in range(gamma - 1)) if rr > 0 else True
+        if pinned:
+            assert int(na.item()) == j_ref
+            assert int(nx.item()) == so.argmax_lowest(lf[j_ref])
+    # commit j+1 rows (oracle and GPU), then one more decode must agree
+    j = int(na.item())
+    om.kv_rewrite(T, j + 1)
+    ctx.kv_rewrite(st, torch.tensor([j + 1], dtype=torch.int32, device="cuda"))
+    nxt = so.argmax_lowest(lf[j])
+    r = om.decode(nxt, T + j + 1, True, thr)
+    lo1 = torch.zeros((1, cfg.vocab), dtype=torch.float32, device="cuda")
+    ctx.sparse_decode_step(torch.tensor([nxt], dtype=torch.int32, device="cuda"),
+                           torch.tensor([T + j + 1], dtype=torch.int32, device="cuda"), 0,
+                           torch.zeros(1, dtype=torch.int32, device="cuda"), lo1)
+    torch.cuda.synchronize()
+    check_logits(lo1.cpu().numpy()[0], r.logits)
+
+
+@pytest.mark.parametrize("gamma,r,mode", [(4, 0.1, 0), (4, 0.3, 0), (6, 0.0, 1), (5, 0.6, 0)])
+def test_generate_token_exact(tiny_models, gamma, r, mode):
+    """Free-running Sirius generation: identical tokens and accept decisions to the oracle."""
+    from paper_2409_03856_b200 import driver
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 2, 64)
+    ref = so.generate(so.OracleModel(cfg, wh, max_seq=256, max_gamma=16), prompt, 32, gamma, r, thr, accept_mode=mode)
+    ctx = make_ctx(cfg, wd, thr)
+    out = driver.Driver(ctx).sirius([prompt], 32, gamma, r, accept_mode=mode)
+    assert out.tokens[0] == ref.tokens
+    assert out.advances(0)[:len(ref.advances)] == ref.advances[:len(out.kernels)]
+
+
+def test_dense_and_sparse_greedy_token_exact(tiny_models):
+    from paper_2409_03856_b200 import driver
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 3, 64)
+    ctx = make_ctx(cfg, wd, thr)
+    d = driver.Driver(ctx)
+    assert d.greedy([prompt], 24, dense=True).tokens[0] == so.greedy_decode(
+        so.OracleModel(cfg, wh, max_seq=256), prompt, 24)
+    assert d.greedy([prompt], 24, dense=False).tokens[0] == so.greedy_decode(
+        so.OracleModel(cfg, wh, max_seq=256), prompt, 24, True, thr)
+
+
+def test_exact_argmax_gpu_equals_gpu_dense_greedy(tiny_models):
+    """north_star invariant on the GPU itself: EXACT_ARGMAX Sirius == dense greedy, token for token."""
+    from paper_2409_03856_b200 import driver
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.3)
+    prompt = synth.eval_prompt(cfg, 5, 32)
+    d = driver.Driver(make_ctx(cfg, wd, thr))
+    dense = d.greedy([prompt], 40, dense=True).tokens[0]
+    sir = d.sirius([prompt], 40, 4, 0.0, accept_mode=1)
+    assert sir.tokens[0] == dense
+
+
+def test_threshold_zero_gpu_sparse_equals_dense(tiny_models):
+    from paper_2409_03856_b200 import driver
+    cfg, wh, wd = tiny_models
+    zero = np.zeros(cfg.n_layers, dtype=np.float32)
+    prompt = synth.eval_prompt(cfg, 6, 32)
+    d = driver.Driver(make_ctx(cfg, wd, zero))
+    assert d.greedy([prompt], 20, dense=False).tokens[0] == d.greedy([prompt], 20, dense=True).tokens[0]
+
+
+def test_r_zero_accepts_all_on_gpu(tiny_models):
+    from paper_2409_03856_b200 import driver
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.3)
+    d = driver.Driver(make_ctx(cfg, wd, thr))
+    out = d.sirius([synth.eval_prompt(cfg, 7, 32)], 24, 5, 0.0)
+    assert all(a == 5 for a in out.advances(0))

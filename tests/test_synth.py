@@ -71,7 +71,7 @@ def test_frozen_checksum():
 @pytest.mark.gpu
 def test_gpu_generator_bit_equal_to_cpu_generator():
     import torch
-    from paper_2409_03856_b200 import synth_gpu
+    from synth import gpu as synth_gpu
     cfg = synth.LLAMA3_8B
     specs = {s.name: s for s in synth.tensor_specs(cfg)}
     for name, (r0, nr, c0, nc) in [("layers.3.w_gate", (1000, 37, 0, 4096)), ("lm_head", (128000, 256, 0, 4096)),
