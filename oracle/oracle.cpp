@@ -16,11 +16,12 @@
 //     kernel, whose K/V later overwrite the cache rows — kv_rewrite).
 // The Sirius loop itself (Algorithm 1) is oracle/sirius_oracle.py.
 //
-// Numeric contract (reading D15): weights are bf16; activations are
-// rounded to bf16 (round-to-nearest-even, directly from the fp64 value) at exactly these points:
-// the RMSNorm outputs, q/k/v after RoPE, the attention output, m = a*u.  Everything else
-// (residual stream, g, a, scores, softmax, logits) is fp64.  With round_acts = 0 no activation is
-// rounded (the mode used to pin this file against HuggingFace LlamaForCausalLM in fp64).
+// Numeric contract (reading D15, north_star "bf16 weights with fp32 accumulation"):
+// weights are bf16; the KV cache stores K (after RoPE) and V rounded to bf16 (round-to-nearest-
+// even, directly from the fp64 value) — the static bf16 KV cache of PAPER.md:496.  Every other
+// activation (residual stream, RMSNorm outputs, q, attention output, g, a, u, m, scores, softmax,
+// logits) is kept at full precision (fp64 here).  With round_kv = 0 nothing is rounded (the mode
+// used to pin this file against HuggingFace LlamaForCausalLM in fp64).
 //
 // Each function below is one step of the definition; no blocking, fusion or reordering beyond
 // the definition.  std::thread only splits independent output rows.
@@ -34,7 +35,7 @@ namespace {
 
 struct Oracle {
   // shape
-  int vocab, d, L, H, KV, hd, ffn, max_seq, max_gamma, threads, round_acts;
+  int vocab, d, L, H, KV, hd, ffn, max_seq, max_gamma, threads, round_kv;
   double theta, eps;
   // weights (host, bf16 bit patterns, borrowed)
   const uint16_t *embed, *final_norm, *lm_head;
@@ -61,7 +62,7 @@ inline double round_bf16(double x) {
   return std::ldexp(std::nearbyint(std::ldexp(m, 8)), e - 8);  // nearbyint: default mode = RNE
 }
 
-inline double act(const Oracle* o, double x) { return o->round_acts ? round_bf16(x) : x; }
+inline double kv_store(const Oracle* o, double x) { return o->round_kv ? round_bf16(x) : x; }
 
 template <class F>
 void parallel_rows(int n, int threads, F fn) {
@@ -87,12 +88,12 @@ void matvec(const Oracle* o, const uint16_t* W, int n, int k, const double* x, d
   });
 }
 
-// RMSNorm: h = x / sqrt(mean(x^2) + eps) * w, then rounded to bf16 (it is a linear-layer input).
+// RMSNorm: h = x / sqrt(mean(x^2) + eps) * w.
 void rmsnorm(const Oracle* o, const double* x, const uint16_t* w, double* h) {
   double ss = 0.0;
   for (int k = 0; k < o->d; ++k) ss += x[k] * x[k];
   double r = 1.0 / std::sqrt(ss / o->d + o->eps);
-  for (int k = 0; k < o->d; ++k) h[k] = act(o, x[k] * r * bf16_value(w[k]));
+  for (int k = 0; k < o->d; ++k) h[k] = x[k] * r * bf16_value(w[k]);
 }
 
 // RoPE, rotate-half convention: pairs (i, i + hd/2); angle = pos * theta^(-2i/hd).
@@ -123,7 +124,7 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row) {
   double* v = k + KV * hd;
   for (int hh = 0; hh < H; ++hh) rope(o, q + hh * hd, pos);
   for (int kh = 0; kh < KV; ++kh) rope(o, k + kh * hd, pos);
-  for (int i = 0; i < rows; ++i) qkv[i] = act(o, qkv[i]);  // q, k, v rounded after RoPE
+  for (int i = H * hd; i < rows; ++i) qkv[i] = kv_store(o, qkv[i]);  // K (after RoPE), V as stored in the bf16 cache
 
   // store this row's K/V
   for (int kh = 0; kh < KV; ++kh)
@@ -166,7 +167,7 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row) {
     for (int i = 0; i < hd; ++i) {
       double acc = 0.0;
       for (int p = 0; p < n_vis; ++p) acc += s[p] * val(p)[i];
-      attn[hh * hd + i] = act(o, acc);  // attention output rounded: it is W_o's input
+      attn[hh * hd + i] = acc;
     }
   }
   matvec(o, o->wo[l], d, H * hd, attn.data(), y.data());
@@ -174,9 +175,9 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row) {
 }
 
 // One decoder layer's MLP with CATS thresholding.
-//   h2 = bf16(RMSNorm(x));  g = h2 . W_gate (dense, always);  a = SiLU(g) = g / (1 + e^-g)
+//   h2 = RMSNorm(x);  g = h2 . W_gate (dense, always);  a = SiLU(g) = g / (1 + e^-g)
 //   active_i  <=>  dense  or  |a_i| >= t_l
-//   u_i = h2 . W_up[i]  (active i only);  m_i = bf16(a_i * u_i);  x += sum_{active i, ascending} m_i W_down[i]
+//   u_i = h2 . W_up[i]  (active i only);  m_i = a_i * u_i;  x += sum_{active i, ascending} m_i W_down[i]
 void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_out, uint8_t* mask_out,
                int* n_active) {
   const int d = o->d, F = o->ffn;
@@ -196,7 +197,7 @@ void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_o
     const uint16_t* w = Wu + (size_t)i * d;
     double u = 0.0;
     for (int k = 0; k < d; ++k) u += bf16_value(w[k]) * h2[k];
-    m[i] = act(o, a[i] * u);
+    m[i] = a[i] * u;
   });
   const uint16_t* Wd = o->wdown[l];
   parallel_rows(d, o->threads, [&](int j) {
@@ -216,11 +217,11 @@ void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_o
 extern "C" {
 
 void* oracle_create(int vocab, int d, int L, int H, int KV, int hd, int ffn, double theta, double eps, int max_seq,
-                    int max_gamma, int threads, int round_acts) {
+                    int max_gamma, int threads, int round_kv) {
   Oracle* o = new Oracle();
   o->vocab = vocab; o->d = d; o->L = L; o->H = H; o->KV = KV; o->hd = hd; o->ffn = ffn;
   o->theta = theta; o->eps = eps; o->max_seq = max_seq; o->max_gamma = max_gamma;
-  o->threads = threads; o->round_acts = round_acts;
+  o->threads = threads; o->round_kv = round_kv;
   o->attn_norm.resize(L); o->wqkv.resize(L); o->wo.resize(L); o->ffn_norm.resize(L);
   o->wgate.resize(L); o->wup.resize(L); o->wdown.resize(L);
   o->kc.assign((size_t)L * max_seq * KV * hd, 0.0);

@@ -83,7 +83,7 @@ class OracleModel:
     """One sequence's oracle state: borrowed weights + its own KV cache and staging."""
 
     def __init__(self, cfg, weights: Dict[str, np.ndarray], max_seq: int, max_gamma: int = 64,
-                 threads: Optional[int] = None, round_acts: bool = True):
+                 threads: Optional[int] = None, round_kv: bool = True):
         self.cfg = cfg
         self.w = weights  # keep alive
         self.max_seq, self.max_gamma = max_seq, max_gamma
@@ -91,7 +91,7 @@ class OracleModel:
         lib = _lib()
         self.h = lib.oracle_create(cfg.vocab, cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
                                    cfg.ffn_dim, cfg.rope_theta, cfg.rms_eps, max_seq, max_gamma, self.threads,
-                                   1 if round_acts else 0)
+                                   1 if round_kv else 0)
         for k in weights:
             assert weights[k].dtype == np.uint16 and weights[k].flags["C_CONTIGUOUS"], k
         lib.oracle_set_global(self.h, _ptr(weights["embed"]), _ptr(weights["final_norm"]), _ptr(weights["lm_head"]))

@@ -784,6 +784,19 @@ int sirius_nccl_comm_destroy(void* comm) {
   return api.commDestroy(comm);
 }
 
+// ---------------------------------------------------------------- test-only: copy an internal buffer
+// which: 0 resA, 1 resB, 2 dA, 3 dF, 4 qkv, 5 ob (bf16), 6 xn (bf16), 7 k_cache, 8 v_cache, 9 stage_k,
+// 10 stage_v, 11 mb (bf16), 12 qb (bf16).  Synchronous D2D copy of `bytes` bytes into dst.
+int sirius_debug_buffer(sirius_ctx* c, int rank, int which, void* dst, size_t bytes) {
+  if (!c || rank < 0 || rank >= c->nranks) return -1;
+  RankState& R = c->ranks[rank];
+  const void* src[13] = {R.resA, R.resB, R.dA, R.dF, R.qkv, R.ob, R.xn, R.k_cache, R.v_cache,
+                         R.stage_k, R.stage_v, R.mb, R.qb};
+  if (which < 0 || which > 12) return -1;
+  cudaStreamSynchronize(c->stream);
+  return (int)cudaMemcpy(dst, src[which], bytes, cudaMemcpyDeviceToDevice);
+}
+
 // ---------------------------------------------------------------- test-only entry: the tcgen05 GEMM
 // out[m, n] = sum_k X[m, k] W[n, k] (fp32), or (W2 != NULL) bf16(SiLU(X W^T) * (X W2^T)).
 // X: DEV bf16 [x_rows >= M, K]; W, W2: DEV bf16 [N, K].  Synchronous.  Returns cudaError_t.

@@ -22,7 +22,7 @@ def _f64(bits: np.ndarray) -> np.ndarray:
 def test_dense_decoder_matches_hf_llama_fp64(tiny):
     """The dense decoder (embed, RMSNorm, RoPE rotate-half, GQA kv=h//(H/KV), SiLU-gated MLP, head)
     equals transformers.LlamaForCausalLM in fp64 with the same weights (oracle with no activation
-    rounding).  Residual ~3e-6 comes from HF's fp32 RoPE table."""
+    rounding of the KV cache).  Residual ~3e-6 comes from HF's fp32 RoPE table."""
     torch = pytest.importorskip("torch")
     tr = pytest.importorskip("transformers")
     cfg, w = tiny
@@ -54,7 +54,7 @@ def test_dense_decoder_matches_hf_llama_fp64(tiny):
     prompt = synth.eval_prompt(cfg, 0, 48)
     with torch.no_grad():
         ref = m(torch.tensor(prompt[None].astype(np.int64))).logits[0].numpy()
-    om = so.OracleModel(cfg, w, max_seq=64, round_acts=False)
+    om = so.OracleModel(cfg, w, max_seq=64, round_kv=False)
     mine = om.prefill(prompt)
     assert np.abs(ref).max() > 5.0  # logits are not degenerate
     assert np.abs(mine - ref).max() < 2e-5, np.abs(mine - ref).max()
@@ -142,11 +142,11 @@ def test_sparse_mlp_equals_dense_mlp_with_inactive_neurons_zeroed(tiny):
 
 
 def test_mlp_formula_against_numpy(tiny):
-    """The MLP (no activation rounding) equals x + W_down^T (SiLU(W_gate h) * W_up h * mask) written
+    """The MLP equals x + W_down^T (SiLU(W_gate h) * W_up h * mask) written
     with numpy matrix products, h = x / sqrt(mean x^2 + eps) * w_norm.  Catches a transposed operand,
     a wrong activation or a wrong norm."""
     cfg, w = tiny
-    m = so.OracleModel(cfg, w, max_seq=8, round_acts=False)
+    m = so.OracleModel(cfg, w, max_seq=8, round_kv=False)
     rng = np.random.default_rng(5)
     x = rng.standard_normal(cfg.d_model)
     thr = float(synth.cats_threshold(0.4))
