@@ -13,8 +13,9 @@
 //                           partial down-projections.
 //  * attn_decode_kernel   : RoPE of q/k, K/V append at pos, split-K flash-decode over the cache,
 //                           last-arriving CTA combines the splits.
-// Numeric contract (D15): bf16 at RMSNorm outputs, q/k/v after RoPE, attention output,
-// m = a*u; fp32 everywhere else (residual, g, a, scores, softmax, logits).
+// Numeric contract (D15): bf16 weights and bf16 KV-cache storage (k after RoPE, v);
+// every activation fp32 (residual, RMSNorm outputs, q, attention output, g, a, u, m, scores,
+// softmax, logits), fp32 accumulation.
 #include "common.cuh"
 #include "decode_kernels.cuh"
 
@@ -23,15 +24,15 @@ namespace sirius {
 // consumer-only named barrier (the producer warp never joins)
 SIRIUS_DEV void cbar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
 
-// Prologue: build the bf16 activation rows h[b, 0:K) in shared memory.  Executed by the NT
+// Prologue: build the fp32 activation rows h[b, 0:K) in shared memory.  Executed by the NT
 // consumer threads only.  Deterministic fixed-order reductions.
 template <int B>
-SIRIUS_DEV void run_prologue(const Prologue& p, int K, uint16_t* h_s, float* red_s, int tid, int NT, bool store_res) {
+SIRIUS_DEV void run_prologue(const Prologue& p, int K, float* h_s, float* red_s, int tid, int NT, bool store_res) {
   const int nwarp = NT / 32, warp = tid / 32, lane = tid % 32;
-  if (p.mode == IN_BF16) {
-    const uint4* src = reinterpret_cast<const uint4*>(p.in_bf16);
-    uint4* dst = reinterpret_cast<uint4*>(h_s);
-    for (int i = tid; i < B * K / 8; i += NT) dst[i] = src[i];
+  if (p.mode == IN_F32) {
+    const float4* src = reinterpret_cast<const float4*>(p.in_f32);
+    float4* dst = reinterpret_cast<float4*>(h_s);
+    for (int i = tid; i < B * K / 4; i += NT) dst[i] = src[i];
     cbar(NT);
     return;
   }
@@ -64,7 +65,7 @@ SIRIUS_DEV void run_prologue(const Prologue& p, int K, uint16_t* h_s, float* red
     const float r = 1.0f / sqrtf(tot / (float)K + p.eps);
     for (int k = tid; k < K; k += NT) {
       float w = __uint_as_float((uint32_t)p.norm_w[k] << 16);
-      h_s[(size_t)b * K + k] = f2bf_bits((xval(k) * r) * w);
+      h_s[(size_t)b * K + k] = (xval(k) * r) * w;
     }
     cbar(NT);  // red_s reuse + h_s complete
   }
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) gemv_stream_kernel(GemvArgs 
   const int K = a.K, rowbytes = K * 2;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   uint8_t* ring = smem;
-  uint16_t* h_s = reinterpret_cast<uint16_t*>(smem + (size_t)nslot * rowbytes);
+  float* h_s = reinterpret_cast<float*>(smem + (size_t)nslot * rowbytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(h_s + (size_t)B * K);
   uint64_t* empty = full + nslot;
   float* red_s = reinterpret_cast<float*>(empty + nslot);
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) gemv_stream_kernel(GemvArgs 
     for (int c = lane; c < nch; c += 32) {
       const uint4 wv = w[c];
 #pragma unroll
-      for (int b = 0; b < B; ++b) acc[b] = dot8bf(wv, reinterpret_cast<const uint4*>(h_s + (size_t)b * K)[c], acc[b]);
+      for (int b = 0; b < B; ++b) acc[b] += dot8(wv, h_s + (size_t)b * K + c * 8);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) ffn_fused_kernel(FfnArgs a, 
   const int nch = (n1 - n0 + 31) / 32;
 
   uint8_t* ring = smem;
-  uint16_t* h_s = reinterpret_cast<uint16_t*>(smem + (size_t)nslot * rowbytes);  // [B][d]
+  float* h_s = reinterpret_cast<float*>(smem + (size_t)nslot * rowbytes);        // [B][d]
   float* a_s = reinterpret_cast<float*>(h_s + (size_t)B * d);                    // [B][kFfnMaxN]
   float* m_s = a_s + B * kFfnMaxN;                                                // [B][32]
   float* red_s = m_s + B * 32;                                                    // [32]
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) ffn_fused_kernel(FfnArgs a, 
         for (int c = lane; c < nchunk16; c += 32) {
           const uint4 wv = w[c];
 #pragma unroll
-          for (int b = 0; b < B; ++b) acc[b] = dot8bf(wv, reinterpret_cast<const uint4*>(h_s + (size_t)b * d)[c], acc[b]);
+          for (int b = 0; b < B; ++b) acc[b] += dot8(wv, h_s + (size_t)b * d + c * 8);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot], NW);
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) ffn_fused_kernel(FfnArgs a, 
       const int c = s - 1, cb = n0 + c * 32;
       cbar(NT);  // list_s[c], act_s[c] visible; every warp is done with the previous D loop (m_s)
       const int cnt = cnt_s[c];
-      // ---- up rows (active only): u = h2 . W_up[n];  m = bf16(a * u)
+      // ---- up rows (active only): u = h2 . W_up[n];  m = a * u
       for (int k = warp; k < cnt; k += NW) {
         const int o = op + k, slot = o % nslot;
         mbar_wait(&full[slot], (uint32_t)(o / nslot) & 1u);
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) ffn_fused_kernel(FfnArgs a, 
         for (int ch = lane; ch < nchunk16; ch += 32) {
           const uint4 wv = w[ch];
 #pragma unroll
-          for (int b = 0; b < B; ++b) acc[b] = dot8bf(wv, reinterpret_cast<const uint4*>(h_s + (size_t)b * d)[ch], acc[b]);
+          for (int b = 0; b < B; ++b) acc[b] += dot8(wv, h_s + (size_t)b * d + ch * 8);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot], NW);
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) ffn_fused_kernel(FfnArgs a, 
           const float u = warp_sum(acc[b]);
           if (lane == 0) {
             const bool act = (act_s[c * B + b] >> nl) & 1u;
-            m_s[b * 32 + k] = act ? round_bf16(a_s[b * kFfnMaxN + c * 32 + nl] * u) : 0.f;
+            m_s[b * 32 + k] = act ? a_s[b * kFfnMaxN + c * 32 + nl] * u : 0.f;
           }
         }
       }
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
   const int chunk = (nkeys + S - 1) / S;
   const int k0 = min(nkeys, split * chunk), k1 = min(nkeys, k0 + chunk);
 
-  // RoPE (rotate-half) on q and k at position pos, then bf16 rounding (D15)
+  // RoPE (rotate-half) on q and k at position pos; k (and v) rounded to bf16 as stored in the cache
   const float* qkv = a.qkv + (size_t)b * qkv_stride;
   const float* cs = a.rope_cos + (size_t)pos * (HD / 2);
   const float* sn = a.rope_sin + (size_t)pos * (HD / 2);
@@ -457,8 +458,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
     const int g = idx / (HD / 2), i = idx % (HD / 2);
     const float* q = qkv + (kvh * G + g) * HD;
     const float x0 = q[i], x1 = q[i + HD / 2], c = cs[i], s = sn[i];
-    q_s[g][i] = round_bf16(x0 * c - x1 * s);
-    q_s[g][i + HD / 2] = round_bf16(x1 * c + x0 * s);
+    q_s[g][i] = x0 * c - x1 * s;
+    q_s[g][i + HD / 2] = x1 * c + x0 * s;
   }
   if (tid < HD / 2) {
     const float* k = qkv + (Hr + kvh) * HD;
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
         A += __ldcg(ps + 2 + i) * f;
       }
     const float o = L > 0.f ? A / L : 0.f;
-    a.out[(size_t)b * Hr * HD + (kvh * G + g) * HD + i] = f2bf_bits(o);
+    a.out[(size_t)b * Hr * HD + (kvh * G + g) * HD + i] = o;
   }
 }
 
@@ -579,7 +580,7 @@ namespace launch {
 
 constexpr int kNW = 8;
 
-static size_t gemv_fixed_smem(int B, int K) { return (size_t)B * K * 2 + 32 * 4 + kNW * B * 8 + 16 + 64; }
+static size_t gemv_fixed_smem(int B, int K) { return (size_t)B * K * 4 + 32 * 4 + kNW * B * 8 + 16 + 64; }
 
 int gemv_nslot(int B, int K, size_t smem_budget) {
   size_t fixed = gemv_fixed_smem(B, K);
@@ -614,7 +615,7 @@ cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out,
 }
 
 static size_t ffn_fixed_smem(int B, int d) {
-  return (size_t)B * d * 2 + (size_t)B * kFfnMaxN * 4 + B * 32 * 4 + 32 * 4 + kFfnMaxN * 4 + kFfnMaxChunks * B * 4 +
+  return (size_t)B * d * 4 + (size_t)B * kFfnMaxN * 4 + B * 32 * 4 + 32 * 4 + kFfnMaxN * 4 + kFfnMaxChunks * B * 4 +
          kFfnMaxChunks * 4 + B * 4 + 16 + kFfnMaxChunks * 8 + 64;
 }
 

@@ -6,14 +6,14 @@ namespace sirius {
 
 // ---- input prologue modes of the streaming GEMV / fused FFN kernels
 enum InMode : int {
-  IN_BF16 = 0,   // activation already bf16 in global: in_bf16 [B, K]
+  IN_F32 = 0,    // activation already in global (fp32): in_f32 [B, K]
   IN_RESID = 1,  // x = base + delta (delta may be NULL); h = bf16(rmsnorm(x) * norm_w)
   IN_EMBED = 2,  // x = embed[tokens[b]];             h = bf16(rmsnorm(x) * norm_w)
 };
 
 struct Prologue {
   int mode;
-  const uint16_t* in_bf16;  // IN_BF16
+  const float* in_f32;      // IN_F32
   const float* base;        // IN_RESID [B, K]
   const float* delta;       // IN_RESID [B, K] or NULL
   const int32_t* tokens;    // IN_EMBED [B]
@@ -69,7 +69,7 @@ struct AttnArgs {
   int Hr, KVr, max_seq, splits;
   float* part;             // workspace [B, KVr, splits, G, hd + 2]
   unsigned* counters;      // [B, KVr]
-  uint16_t* out;           // [B, Hr * hd] bf16
+  float* out;              // [B, Hr * hd] fp32
   int* err;                // sticky device error word
 };
 

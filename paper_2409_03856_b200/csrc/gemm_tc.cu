@@ -14,7 +14,9 @@
 //
 // Roles (128 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer, warp 2 = TMEM
 // allocator; all four warps run the epilogue (TMEM lane = weight row = threadIdx.x).
-// Epilogues: fp32 store, or SwiGLU m = bf16(SiLU(g) * u) from two accumulators (gate, up).
+// Epilogues: fp32 store, or SwiGLU m = SiLU(g) * u from two accumulators (gate, up), written as a bf16
+// hi/lo pair.  Activations enter as bf16 hi/lo pairs of fp32 values (x = hi + lo to 2^-17): two MMAs
+// per k-step, free while the pass is HBM-bound.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -75,8 +77,10 @@ template <bool DUAL>
 SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
   if (j >= g.M || n >= g.N) return;
   if (DUAL) {
-    const float a = v0 / (1.0f + expf(-v0));  // SiLU(gate)
-    reinterpret_cast<uint16_t*>(g.out)[(size_t)j * g.ldc + n] = f2bf_bits(a * v1);
+    const float m = v0 / (1.0f + expf(-v0)) * v1;  // SiLU(gate) * up
+    const uint16_t hi = f2bf_bits(m);
+    reinterpret_cast<uint16_t*>(g.out)[(size_t)j * g.ldc + n] = hi;
+    reinterpret_cast<uint16_t*>(g.out2)[(size_t)j * g.ldc + n] = f2bf_bits(m - __uint_as_float((uint32_t)hi << 16));
   } else {
     reinterpret_cast<float*>(g.out)[(size_t)j * g.ldc + n] = v0;
   }
@@ -85,7 +89,8 @@ SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
 template <bool DUAL>
 __global__ void __launch_bounds__(128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
-                   const __grid_constant__ CUtensorMap tmB, GemmArgs g, int MP, int stages) {
+                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo, GemmArgs g,
+                   int MP, int stages, int has_lo) {
   constexpr int NACC = DUAL ? 2 : 1;
   constexpr uint32_t A_BYTES = 128 * 64 * 2;  // one 128 x 64 bf16 weight tile
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -97,7 +102,8 @@ __global__ void __launch_bounds__(128, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t b_bytes = (uint32_t)MP * 128;
-  const uint32_t stage_bytes = ((NACC * A_BYTES + b_bytes) + 1023) & ~1023u;
+  const int NB = has_lo ? 2 : 1;
+  const uint32_t stage_bytes = ((NACC * A_BYTES + NB * b_bytes) + 1023) & ~1023u;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
   uint64_t* accum = empty + stages;
@@ -115,6 +121,7 @@ __global__ void __launch_bounds__(128, 1)
     prefetch_tmap(&tmA0);
     if (DUAL) prefetch_tmap(&tmA1);
     prefetch_tmap(&tmB);
+    if (has_lo) prefetch_tmap(&tmBlo);
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_ptr_s)),
@@ -129,7 +136,7 @@ __global__ void __launch_bounds__(128, 1)
   // instruction descriptor, kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
   // both K-major, N>>3 at [17,23), M>>4 at [24,29)
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((128u >> 4) << 24);
-  const uint32_t tx_bytes = NACC * A_BYTES + b_bytes;
+  const uint32_t tx_bytes = NACC * A_BYTES + NB * b_bytes;
 
   long long it = 0;  // global k-iteration counter: stage = it % stages, parity = (it / stages) & 1
   int sidx = 0;
@@ -149,8 +156,10 @@ __global__ void __launch_bounds__(128, 1)
         const int kc = (kbeg + i) * 64;
         tma_load_2d(st, &tmA0, kc, t * 128, &full[s], pol_w);
         if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[s], pol_w);
-        for (int r = 0; r < MP / 16; ++r)
+        for (int r = 0; r < MP / 16; ++r) {
           tma_load_2d(st + NACC * A_BYTES + r * 2048, &tmB, kc, r * 16, &full[s], pol_x);
+          if (has_lo) tma_load_2d(st + NACC * A_BYTES + b_bytes + r * 2048, &tmBlo, kc, r * 16, &full[s], pol_x);
+        }
       }
     } else if (warp == 1 && lane == 0) {  // ---- MMA issuer
       for (int i = 0; i < nk; ++i) {
@@ -161,11 +170,16 @@ __global__ void __launch_bounds__(128, 1)
         uint8_t* st = smem + (size_t)s * stage_bytes;
         const uint64_t a0 = sw128_desc(st), b0 = sw128_desc(st + NACC * A_BYTES);
         const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES) : 0ull;
+        const uint64_t b1 = sw128_desc(st + NACC * A_BYTES + b_bytes);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
           const uint32_t accf = (i > 0 || k > 0) ? 1u : 0u;
           mma_bf16(tmem, a0 + 2 * k, b0 + 2 * k, idesc, accf);
           if (DUAL) mma_bf16(tmem + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
+          if (has_lo) {
+            mma_bf16(tmem, a0 + 2 * k, b1 + 2 * k, idesc, 1u);
+            if (DUAL) mma_bf16(tmem + MP, a1 + 2 * k, b1 + 2 * k, idesc, 1u);
+          }
         }
         mma_commit(&empty[s]);  // smem slot free once these MMAs have read it
       }
@@ -265,12 +279,13 @@ bool make_tmap(void* map, const void* base, uint64_t rows, uint64_t K, uint32_t 
 
 size_t gemm_workspace_bytes(int num_sms) { return (size_t)num_sms * 2 * 2 * 256 * 128 * sizeof(float); }
 
-cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const GemmArgs& g, int MP, int num_sms,
-                 size_t smem_budget, cudaStream_t st) {
+cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void* tmBlo, const GemmArgs& g, int MP,
+                 int num_sms, size_t smem_budget, cudaStream_t st) {
   if (MP < 16 || MP > 256 || MP % 16) return cudaErrorInvalidValue;
   const bool dual = tmA1 != nullptr;
   const int NACC = dual ? 2 : 1;
-  const size_t stage_bytes = ((size_t)NACC * 16384 + (size_t)MP * 128 + 1023) & ~(size_t)1023;
+  const int NB = tmBlo ? 2 : 1;
+  const size_t stage_bytes = ((size_t)NACC * 16384 + (size_t)NB * MP * 128 + 1023) & ~(size_t)1023;
   const size_t extra = 1024 + 256;
   int stages = (int)((smem_budget - extra) / stage_bytes);
   if (stages > 8) stages = 8;
@@ -281,14 +296,16 @@ cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const Gemm
   const CUtensorMap* a0 = reinterpret_cast<const CUtensorMap*>(tmA0);
   const CUtensorMap* a1 = reinterpret_cast<const CUtensorMap*>(dual ? tmA1 : tmA0);
   const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmB);
+  const CUtensorMap* blo = reinterpret_cast<const CUtensorMap*>(tmBlo ? tmBlo : tmB);
+  const int has_lo = tmBlo ? 1 : 0;
   if (dual) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    gemm_tc_kernel<true><<<grid, 128, smem, st>>>(*a0, *a1, *b, g, MP, stages);
+    gemm_tc_kernel<true><<<grid, 128, smem, st>>>(*a0, *a1, *b, *blo, g, MP, stages, has_lo);
   } else {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    gemm_tc_kernel<false><<<grid, 128, smem, st>>>(*a0, *a1, *b, g, MP, stages);
+    gemm_tc_kernel<false><<<grid, 128, smem, st>>>(*a0, *a1, *b, *blo, g, MP, stages, has_lo);
   }
   return cudaGetLastError();
 }

@@ -81,7 +81,9 @@ struct RankState {
   uint16_t *k_cache = nullptr, *v_cache = nullptr, *stage_k = nullptr, *stage_v = nullptr;
   // activations (MAXM rows)
   float *resA = nullptr, *resB = nullptr, *dA = nullptr, *dF = nullptr, *qkv = nullptr, *logits = nullptr;
-  uint16_t *xn = nullptr, *qb = nullptr, *ob = nullptr, *mb = nullptr;
+  float *qb = nullptr, *ob = nullptr;                      // post-RoPE q (verify), attention out (decode)
+  uint16_t *xn_hi = nullptr, *xn_lo = nullptr;            // tensor-core operands: bf16 hi/lo pairs of fp32
+  uint16_t *ob_hi = nullptr, *ob_lo = nullptr, *mb_hi = nullptr, *mb_lo = nullptr;
   // workspaces
   float *ffn_part = nullptr, *attn_part = nullptr, *gemm_part = nullptr;
   int* ffn_cnt = nullptr;
@@ -89,7 +91,7 @@ struct RankState {
   unsigned *attn_cnt = nullptr, *gemm_cnt = nullptr, *head_cnt = nullptr;
   // tensor maps
   std::vector<TmapBuf> tm_qkv, tm_o, tm_gate, tm_up, tm_down;
-  TmapBuf tm_head, tm_xn, tm_ob, tm_mb;
+  TmapBuf tm_head, tm_xn_hi, tm_xn_lo, tm_ob_hi, tm_ob_lo, tm_mb_hi, tm_mb_lo;
 };
 
 struct sirius_ctx {
@@ -194,8 +196,8 @@ sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
   return SIRIUS_OK;
 }
 
-sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x, int N,
-                       int K, int M, void* out, int ldc) {
+sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x_hi,
+                       const TmapBuf& x_lo, int N, int K, int M, void* out, int ldc, void* out2 = nullptr) {
   GemmArgs g;
   g.N = N;
   g.K = K;
@@ -203,11 +205,12 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
   g.n_tiles = (N + 127) / 128;
   g.kb = (K + 63) / 64;
   g.out = out;
+  g.out2 = out2;
   g.ldc = ldc;
   g.part = R.gemm_part;
   g.counters = R.gemm_cnt;
   const int MP = round_up(M, 16);
-  CU(launch::gemm(wa.b, wb ? wb->b : nullptr, x.b, g, MP, c->num_sms, c->smem_optin, c->stream));
+  CU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms, c->smem_optin, c->stream));
   return SIRIUS_OK;
 }
 
@@ -234,9 +237,10 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.norm_w = R.attn_norm[l];
       na.eps = cf.rms_eps;
       na.res_out = R.resA;
-      na.out = R.xn;
+      na.out_hi = R.xn_hi;
+      na.out_lo = R.xn_lo;
       CU(launch::norm_rows(na, M, c->stream));
-      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn, c->Nqkv, d, M, R.qkv, c->Nqkv));
+      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Nqkv, d, M, R.qkv, c->Nqkv));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
       RopeStoreArgs ra = {};
@@ -274,12 +278,13 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       aa.fresh_in_cache = to_cache ? 1 : 0;
       aa.part = R.attn_part;
       aa.counters = R.attn_cnt;
-      aa.out = R.ob;
+      aa.out_hi = R.ob_hi;
+      aa.out_lo = R.ob_lo;
       const int row_blocks = (rows_per_seq * c->G + 63) / 64;
       int splits = (2 * c->num_sms + nseq * c->KVr * row_blocks - 1) / (nseq * c->KVr * row_blocks);
       splits = splits < 1 ? 1 : (splits > 32 ? 32 : splits);
       CU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
-      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob, d, c->Hr * hd, M, R.dA, d));
+      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d));
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
     for (auto& R : c->ranks) {
@@ -291,10 +296,11 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.norm_w = R.ffn_norm[l];
       na.eps = cf.rms_eps;
       na.res_out = R.resB;
-      na.out = R.xn;
+      na.out_hi = R.xn_hi;
+      na.out_lo = R.xn_lo;
       CU(launch::norm_rows(na, M, c->stream));
-      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn, c->Fr, d, M, R.mb, c->Fr));
-      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb, d, c->Fr, M, R.dF, d));
+      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn_hi, R.tm_xn_lo, c->Fr, d, M, R.mb_hi, c->Fr, R.mb_lo));
+      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb_hi, R.tm_mb_lo, d, c->Fr, M, R.dF, d));
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
   }
@@ -426,9 +432,11 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     if (alloc(c, &R.k_cache, kv) || alloc(c, &R.v_cache, kv) || alloc(c, &R.stage_k, stg) ||
         alloc(c, &R.stage_v, stg) || alloc(c, &R.resA, (size_t)M * d) || alloc(c, &R.resB, (size_t)M * d) ||
         alloc(c, &R.dA, (size_t)M * d) || alloc(c, &R.dF, (size_t)M * d) || alloc(c, &R.qkv, (size_t)M * c->Nqkv) ||
-        alloc(c, &R.logits, (size_t)M * c->Vr) || alloc(c, &R.xn, (size_t)M * d) ||
-        alloc(c, &R.qb, (size_t)M * c->Hr * hd) || alloc(c, &R.ob, (size_t)M * c->Hr * hd) ||
-        alloc(c, &R.mb, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * 4 * d) ||
+        alloc(c, &R.logits, (size_t)M * c->Vr) || alloc(c, &R.xn_hi, (size_t)M * d) ||
+        alloc(c, &R.xn_lo, (size_t)M * d) || alloc(c, &R.qb, (size_t)M * c->Hr * hd) ||
+        alloc(c, &R.ob, (size_t)M * c->Hr * hd) || alloc(c, &R.ob_hi, (size_t)M * c->Hr * hd) ||
+        alloc(c, &R.ob_lo, (size_t)M * c->Hr * hd) || alloc(c, &R.mb_hi, (size_t)M * c->Fr) ||
+        alloc(c, &R.mb_lo, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * 4 * d) ||
         alloc(c, &R.ffn_cnt, (size_t)c->num_sms * 4) || alloc(c, &R.ffn_barrier, 8) ||
         alloc(c, &R.attn_part, (size_t)B * c->KVr * 64 * 64 * (hd + 2) + (size_t)c->KVr * row_blocks_max * 32 * 64 * (hd + 2)) ||
         alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) ||
@@ -459,9 +467,12 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       ok &= launch::make_tmap(R.tm_down[l].b, R.w_down_t[l], d, c->Fr, 128);
     }
     ok &= launch::make_tmap(R.tm_head.b, R.lm_head, c->Vr, d, 128);
-    ok &= launch::make_tmap(R.tm_xn.b, R.xn, M, d, 16);
-    ok &= launch::make_tmap(R.tm_ob.b, R.ob, M, c->Hr * hd, 16);
-    ok &= launch::make_tmap(R.tm_mb.b, R.mb, M, c->Fr, 16);
+    ok &= launch::make_tmap(R.tm_xn_hi.b, R.xn_hi, M, d, 16);
+    ok &= launch::make_tmap(R.tm_xn_lo.b, R.xn_lo, M, d, 16);
+    ok &= launch::make_tmap(R.tm_ob_hi.b, R.ob_hi, M, c->Hr * hd, 16);
+    ok &= launch::make_tmap(R.tm_ob_lo.b, R.ob_lo, M, c->Hr * hd, 16);
+    ok &= launch::make_tmap(R.tm_mb_hi.b, R.mb_hi, M, c->Fr, 16);
+    ok &= launch::make_tmap(R.tm_mb_lo.b, R.mb_lo, M, c->Fr, 16);
     if (!ok) {
       c->last_error = "cuTensorMapEncodeTiled failed";
       return cleanup_fail(SIRIUS_ERR_CUDA);
@@ -595,8 +606,8 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
       at.err = c->err_dev;
       CU(launch::attn_decode(at, B, hd, c->G, c->stream));
       GemvArgs o = {};
-      o.pro.mode = IN_BF16;
-      o.pro.in_bf16 = R.ob;
+      o.pro.mode = IN_F32;
+      o.pro.in_f32 = R.ob;
       o.W = R.w_o[l];
       o.rows = d;
       o.K = c->Hr * hd;
@@ -689,11 +700,12 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
     na.d = d;
     na.norm_w = R.final_norm;
     na.eps = cf.rms_eps;
-    na.out = R.xn;
+    na.out_hi = R.xn_hi;
+    na.out_lo = R.xn_lo;
     CU(launch::norm_rows(na, M, c->stream));
     float* lo = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : R.logits;
     const int ldl = logits_out ? (c->emulated ? cf.vocab : c->Vr) : c->Vr;
-    OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn, c->Vr, d, M, lo, ldl));
+    OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Vr, d, M, lo, ldl));
     AcceptStatsArgs as = {};
     as.logits = lo;
     as.ldl = ldl;
@@ -785,22 +797,24 @@ int sirius_nccl_comm_destroy(void* comm) {
 }
 
 // ---------------------------------------------------------------- test-only: copy an internal buffer
-// which: 0 resA, 1 resB, 2 dA, 3 dF, 4 qkv, 5 ob (bf16), 6 xn (bf16), 7 k_cache, 8 v_cache, 9 stage_k,
-// 10 stage_v, 11 mb (bf16), 12 qb (bf16).  Synchronous D2D copy of `bytes` bytes into dst.
+// which: 0 resA, 1 resB, 2 dA, 3 dF, 4 qkv, 5 ob (fp32), 6 xn_hi (bf16), 7 k_cache, 8 v_cache, 9 stage_k,
+// 10 stage_v, 11 mb_hi (bf16), 12 qb (fp32).  Synchronous D2D copy of `bytes` bytes into dst.
 int sirius_debug_buffer(sirius_ctx* c, int rank, int which, void* dst, size_t bytes) {
   if (!c || rank < 0 || rank >= c->nranks) return -1;
   RankState& R = c->ranks[rank];
-  const void* src[13] = {R.resA, R.resB, R.dA, R.dF, R.qkv, R.ob, R.xn, R.k_cache, R.v_cache,
-                         R.stage_k, R.stage_v, R.mb, R.qb};
+  const void* src[13] = {R.resA, R.resB, R.dA, R.dF, R.qkv, R.ob, R.xn_hi, R.k_cache, R.v_cache,
+                         R.stage_k, R.stage_v, R.mb_hi, R.qb};
   if (which < 0 || which > 12) return -1;
   cudaStreamSynchronize(c->stream);
   return (int)cudaMemcpy(dst, src[which], bytes, cudaMemcpyDeviceToDevice);
 }
 
 // ---------------------------------------------------------------- test-only entry: the tcgen05 GEMM
-// out[m, n] = sum_k X[m, k] W[n, k] (fp32), or (W2 != NULL) bf16(SiLU(X W^T) * (X W2^T)).
-// X: DEV bf16 [x_rows >= M, K]; W, W2: DEV bf16 [N, K].  Synchronous.  Returns cudaError_t.
-int sirius_debug_gemm(const void* X, int x_rows, const void* Wt, const void* W2, void* out, int M, int N, int K) {
+// out[m, n] = sum_k (X + Xlo)[m, k] W[n, k] (fp32), or (W2 != NULL) m = SiLU(X W^T) * (X W2^T) as bf16
+// hi (out) / lo (out2).  X, Xlo (nullable): DEV bf16 [x_rows >= M, K]; W, W2: DEV bf16 [N, K].
+// Synchronous.  Returns cudaError_t.
+int sirius_debug_gemm(const void* X, const void* Xlo, int x_rows, const void* Wt, const void* W2, void* out,
+                      void* out2, int M, int N, int K) {
   static float* part = nullptr;
   static unsigned* cnt = nullptr;
   int dev = 0, sms = 0, optin = 0;
@@ -812,8 +826,9 @@ int sirius_debug_gemm(const void* X, int x_rows, const void* Wt, const void* W2,
     if (cudaMalloc(&cnt, 65536 * sizeof(unsigned))) return -1;
     cudaMemset(cnt, 0, 65536 * sizeof(unsigned));
   }
-  TmapBuf ta, tb, tx;
+  TmapBuf ta, tb, tx, txl;
   if (!launch::make_tmap(ta.b, Wt, N, K, 128) || !launch::make_tmap(tx.b, X, x_rows, K, 16)) return -2;
+  if (Xlo && !launch::make_tmap(txl.b, Xlo, x_rows, K, 16)) return -2;
   if (W2 && !launch::make_tmap(tb.b, W2, N, K, 128)) return -2;
   GemmArgs g;
   g.N = N;
@@ -822,10 +837,12 @@ int sirius_debug_gemm(const void* X, int x_rows, const void* Wt, const void* W2,
   g.n_tiles = (N + 127) / 128;
   g.kb = (K + 63) / 64;
   g.out = out;
+  g.out2 = out2;
   g.ldc = N;
   g.part = part;
   g.counters = cnt;
-  cudaError_t e = launch::gemm(ta.b, W2 ? tb.b : nullptr, tx.b, g, round_up(M, 16), sms, (size_t)optin - 1024, 0);
+  cudaError_t e = launch::gemm(ta.b, W2 ? tb.b : nullptr, tx.b, Xlo ? txl.b : nullptr, g, round_up(M, 16), sms,
+                               (size_t)optin - 1024, 0);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaDeviceSynchronize();
 }

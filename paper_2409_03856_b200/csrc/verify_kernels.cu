@@ -48,7 +48,10 @@ __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
   const float r = 1.0f / sqrtf(tot / (float)d + a.eps);
   for (int k = tid; k < d; k += 256) {
     const float w = __uint_as_float((uint32_t)a.norm_w[k] << 16);
-    a.out[(size_t)m * d + k] = f2bf_bits((xval(k) * r) * w);
+    const float h = (xval(k) * r) * w;
+    const uint16_t hi = f2bf_bits(h);
+    a.out_hi[(size_t)m * d + k] = hi;
+    a.out_lo[(size_t)m * d + k] = f2bf_bits(h - __uint_as_float((uint32_t)hi << 16));
   }
 }
 
@@ -68,11 +71,12 @@ __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
   for (int idx = tid; idx < (a.Hr + a.KVr) * half; idx += 128) {
     const int h = idx / half, e = idx % half;
     const float x0 = row[h * hd + e], x1 = row[h * hd + e + half], c = cs[e], s = sn[e];
-    const uint16_t r0 = f2bf_bits(x0 * c - x1 * s), r1 = f2bf_bits(x1 * c + x0 * s);
+    const float y0 = x0 * c - x1 * s, y1 = x1 * c + x0 * s;
     if (h < a.Hr) {
-      a.q_out[(size_t)m * a.Hr * hd + h * hd + e] = r0;
-      a.q_out[(size_t)m * a.Hr * hd + h * hd + e + half] = r1;
+      a.q_out[(size_t)m * a.Hr * hd + h * hd + e] = y0;
+      a.q_out[(size_t)m * a.Hr * hd + h * hd + e + half] = y1;
     } else {
+      const uint16_t r0 = f2bf_bits(y0), r1 = f2bf_bits(y1);
       const int kvh = h - a.Hr;
       uint16_t* dst = a.to_cache ? a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_seq + pos) * hd
                                  : a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + i) * hd;
@@ -120,10 +124,10 @@ __global__ void __launch_bounds__(128) attn_rows_kernel(AttnRowsArgs a, float sc
   float mrun = -INFINITY, lrun = 0.f;
   {
     const int m = bz * rows + (valid ? i : 0);
-    const uint16_t* qp = a.q + (size_t)m * a.Hr * HD + (kvh * G + g) * HD + half * H2;
+    const float* qp = a.q + (size_t)m * a.Hr * HD + (kvh * G + g) * HD + half * H2;
 #pragma unroll
     for (int e = 0; e < H2; ++e) {
-      q[e] = __uint_as_float((uint32_t)qp[e] << 16);
+      q[e] = qp[e];
       acc[e] = 0.f;
     }
   }
@@ -188,9 +192,14 @@ __global__ void __launch_bounds__(128) attn_rows_kernel(AttnRowsArgs a, float sc
 #pragma unroll
     for (int e = 0; e < H2; ++e) o[e] += __ldcg(ps + 2 + half * H2 + e) * f;
   }
-  uint16_t* op = a.out + (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + half * H2;
+  const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + half * H2;
 #pragma unroll
-  for (int e = 0; e < H2; ++e) op[e] = f2bf_bits(L > 0.f ? o[e] / L : 0.f);
+  for (int e = 0; e < H2; ++e) {
+    const float v = L > 0.f ? o[e] / L : 0.f;
+    const uint16_t hi = f2bf_bits(v);
+    a.out_hi[off + e] = hi;
+    a.out_lo[off + e] = f2bf_bits(v - __uint_as_float((uint32_t)hi << 16));
+  }
 }
 
 // ===================================================================== acceptance

@@ -15,7 +15,8 @@ struct NormRowsArgs {
   const uint16_t* norm_w;  // [d]
   float eps;
   float* res_out;          // [M, d] or NULL
-  uint16_t* out;           // [M, d] bf16
+  uint16_t* out_hi;        // [M, d] bf16: hi = bf16(h), lo = bf16(h - hi)  (fp32 h as a bf16 pair for
+  uint16_t* out_lo;        //          the tensor-core B operand; |h - hi - lo| <= 2^-17 |h|)
 };
 
 struct RopeStoreArgs {
@@ -26,14 +27,14 @@ struct RopeStoreArgs {
   const float* rope_sin;
   int Hr, KVr, hd, max_seq, max_gamma;
   int to_cache;            // 1: K/V -> cache slots pos (prefill); 0: -> staging row i (verify)
-  uint16_t* q_out;         // [M, Hr * hd]
+  float* q_out;            // [M, Hr * hd] fp32 (post-RoPE)
   uint16_t* k_dst;         // this layer's cache [B, KVr, max_seq, hd] or staging [B, KVr, max_gamma, hd]
   uint16_t* v_dst;
   int* err;
 };
 
 struct AttnRowsArgs {
-  const uint16_t* q;        // [nseq * rows, Hr * hd] bf16 (post-RoPE)
+  const float* q;           // [nseq * rows, Hr * hd] fp32 (post-RoPE)
   const int32_t* start;     // [B]  T of each sequence
   int b_base, rows_per_seq, G, Hr, KVr, max_seq;
   const uint16_t* k_cache;  // this layer [B, KVr, max_seq, hd]
@@ -43,7 +44,8 @@ struct AttnRowsArgs {
   int fresh_stride, fresh_in_cache;
   float* part;              // workspace
   unsigned* counters;       // [nseq * KVr * row_blocks]
-  uint16_t* out;            // [nseq * rows, Hr * hd] bf16
+  uint16_t* out_hi;         // [nseq * rows, Hr * hd] attention output as a bf16 hi/lo pair
+  uint16_t* out_lo;
 };
 
 struct RowStat {

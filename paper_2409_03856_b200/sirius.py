@@ -76,7 +76,9 @@ def load():
         lib.sirius_last_error.restype = ctypes.c_char_p
         lib.sirius_version.argtypes = []
         lib.sirius_version.restype = ctypes.c_char_p
-        lib.sirius_debug_gemm.argtypes = [P, I, P, P, P, I, I, I]
+        lib.sirius_debug_gemm.argtypes = [P, P, I, P, P, P, P, I, I, I]
+        lib.sirius_debug_buffer.argtypes = [P, I, I, P, ctypes.c_size_t]
+        lib.sirius_debug_buffer.restype = I
         lib.sirius_debug_gemm.restype = I
         lib.sirius_nccl_available.restype = I
         lib.sirius_nccl_unique_id.argtypes = [P]
@@ -170,10 +172,12 @@ class Sirius:
             pass
 
 
-def debug_gemm(X, W, out, M: int, W2=None) -> None:
-    """Test-only: out = X[:M] @ W.T (fp32) or bf16(SiLU(X W^T) * (X W2^T)) via the tcgen05 kernel."""
+def debug_gemm(X, W, out, M: int, W2=None, Xlo=None, out2=None) -> None:
+    """Test-only: out = (X + Xlo)[:M] @ W.T (fp32), or with W2 the SwiGLU m = SiLU(X W^T) * (X W2^T)
+    as a bf16 hi (out) / lo (out2) pair, via the tcgen05 kernel."""
     lib = load()
     N, K = W.shape
-    r = lib.sirius_debug_gemm(X.data_ptr(), X.shape[0], W.data_ptr(), _ptr(W2), out.data_ptr(), M, N, K)
+    r = lib.sirius_debug_gemm(X.data_ptr(), _ptr(Xlo), X.shape[0], W.data_ptr(), _ptr(W2), out.data_ptr(),
+                              _ptr(out2), M, N, K)
     if r != 0:
         raise RuntimeError(f"sirius_debug_gemm failed: {r}")
