@@ -25,6 +25,7 @@
 //
 // Each function below is one step of the definition; no blocking, fusion or reordering beyond
 // the definition.  std::thread only splits independent output rows.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -199,13 +200,18 @@ void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_o
     for (int k = 0; k < d; ++k) u += bf16_value(w[k]) * h2[k];
     m[i] = a[i] * u;
   });
+  // y_j = sum over active i (ascending) of m_i * W_down[i][j]; threads own column blocks and stream
+  // the neuron rows (each y_j still sums over i in ascending order).
   const uint16_t* Wd = o->wdown[l];
-  parallel_rows(d, o->threads, [&](int j) {
-    double acc = 0.0;
+  std::vector<double> y(d, 0.0);
+  const int nblk = (d + 63) / 64;
+  parallel_rows(nblk, o->threads, [&](int blk) {
+    const int j0 = blk * 64, j1 = std::min(d, j0 + 64);
     for (int i = 0; i < F; ++i)
-      if (mask[i]) acc += m[i] * bf16_value(Wd[(size_t)i * d + j]);
-    x[j] += acc;
+      if (mask[i])
+        for (int j = j0; j < j1; ++j) y[j] += m[i] * bf16_value(Wd[(size_t)i * d + j]);
   });
+  for (int j = 0; j < d; ++j) x[j] += y[j];
   if (gate_out)
     for (int i = 0; i < F; ++i) gate_out[i] = a[i];
   if (mask_out) std::memcpy(mask_out, mask.data(), F);

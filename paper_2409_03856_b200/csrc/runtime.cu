@@ -120,6 +120,14 @@ struct sirius_ctx {
   bool have_correct = false;
   bool prefilled = false;
   sirius_status sticky = SIRIUS_OK;
+  unsigned long long launches = 0;  // kernels this context has launched (bench gpu_launches evidence)
+  bool prof_on = false;             // per-kernel CUDA-event timing (bench roofline pass)
+  struct ProfEv {
+    int id;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfEv> prof;
+  size_t prof_used = 0;
   std::vector<void*> allocations;
   std::string last_error = "ok";
 };
@@ -139,6 +147,32 @@ sirius_status fail(sirius_ctx* c, sirius_status s, const std::string& msg) {
     cudaError_t _e = (x);                                                                            \
     if (_e != cudaSuccess) return fail(c, SIRIUS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
   } while (0)
+
+#define LCU(x)     \
+  do {             \
+    ++c->launches; \
+    CU(x);         \
+  } while (0)
+
+// ---- optional per-kernel timing: events recorded on the launch stream around selected launches
+enum ProfId { P_QKV = 0, P_ATTN = 1, P_OPROJ = 2, P_FFN = 3, P_HEAD = 4, P_VERIFY = 5, P_REWRITE = 6, P_NUM = 8 };
+void prof_begin(sirius_ctx* c, int id) {
+  if (!c->prof_on) return;
+  if (c->prof_used == c->prof.size()) {
+    sirius_ctx::ProfEv e;
+    e.id = id;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    c->prof.push_back(e);
+  }
+  c->prof[c->prof_used].id = id;
+  cudaEventRecord(c->prof[c->prof_used].a, c->stream);
+}
+void prof_end(sirius_ctx* c) {
+  if (!c->prof_on) return;
+  cudaEventRecord(c->prof[c->prof_used].b, c->stream);
+  ++c->prof_used;
+}
 
 template <class T>
 sirius_status alloc(sirius_ctx* c, T** p, size_t count, bool zero = true) {
@@ -177,7 +211,7 @@ void mirror_err(sirius_ctx* c) { cudaMemcpyAsync(c->err_host, c->err_dev, sizeof
 sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev, size_t rows) {
   const size_t n = rows * c->cfg.d_model;
   if (c->nranks > 1) {
-    CU(launch::sum_ranks(ptrs_dev, c->nranks, rows, c->cfg.d_model, c->cfg.d_model, c->stream));
+    LCU(launch::sum_ranks(ptrs_dev, c->nranks, rows, c->cfg.d_model, c->cfg.d_model, c->stream));
   } else if (c->cfg.tp_size > 1) {
     NcclApi& api = nccl();
     float* p = c->ranks[0].*buf;
@@ -192,7 +226,7 @@ sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
   const int grid = a.rows < c->num_sms ? a.rows : c->num_sms;
   const int nslot = launch::gemv_nslot(B, a.K, c->smem_optin);
   if (nslot < 2) return fail(c, SIRIUS_ERR_UNSUPPORTED, "gemv: row too large for shared memory");
-  CU(launch::gemv(a, B, grid, nslot, c->stream));
+  LCU(launch::gemv(a, B, grid, nslot, c->stream));
   return SIRIUS_OK;
 }
 
@@ -210,7 +244,7 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
   g.part = R.gemm_part;
   g.counters = R.gemm_cnt;
   const int MP = round_up(M, 16);
-  CU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms, c->smem_optin, c->stream));
+  LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms, c->smem_optin, c->stream));
   return SIRIUS_OK;
 }
 
@@ -239,7 +273,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.res_out = R.resA;
       na.out_hi = R.xn_hi;
       na.out_lo = R.xn_lo;
-      CU(launch::norm_rows(na, M, c->stream));
+      LCU(launch::norm_rows(na, M, c->stream));
       OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Nqkv, d, M, R.qkv, c->Nqkv));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
@@ -260,7 +294,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       ra.k_dst = to_cache ? R.k_cache + l * kv_layer : R.stage_k + l * st_layer;
       ra.v_dst = to_cache ? R.v_cache + l * kv_layer : R.stage_v + l * st_layer;
       ra.err = c->err_dev;
-      CU(launch::rope_store(ra, M, c->stream));
+      LCU(launch::rope_store(ra, M, c->stream));
       AttnRowsArgs aa = {};
       aa.q = R.qb;
       aa.start = start;
@@ -283,7 +317,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       const int row_blocks = (rows_per_seq * c->G + 63) / 64;
       int splits = (2 * c->num_sms + nseq * c->KVr * row_blocks - 1) / (nseq * c->KVr * row_blocks);
       splits = splits < 1 ? 1 : (splits > 32 ? 32 : splits);
-      CU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
+      LCU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
       OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d));
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
@@ -298,7 +332,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.res_out = R.resB;
       na.out_hi = R.xn_hi;
       na.out_lo = R.xn_lo;
-      CU(launch::norm_rows(na, M, c->stream));
+      LCU(launch::norm_rows(na, M, c->stream));
       OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn_hi, R.tm_xn_lo, c->Fr, d, M, R.mb_hi, c->Fr, R.mb_lo));
       OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb_hi, R.tm_mb_lo, d, c->Fr, M, R.dF, d));
     }
@@ -489,6 +523,10 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
 sirius_status sirius_destroy(sirius_ctx* c) {
   if (!c) return SIRIUS_ERR_INVALID_ARG;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& e : c->prof) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
   for (void* p : c->allocations) cudaFree(p);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->pre_start_host) cudaFreeHost(c->pre_start_host);
@@ -540,7 +578,7 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
             int r = api.allReduce(c->amax, c->amax, 1, kNcclUint64, kNcclMax, c->comm, c->stream);
             if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllReduce(max)");
           }
-          CU(launch::argmax_finalize(c->amax, 1, first_token + b, c->stream));
+          LCU(launch::argmax_finalize(c->amax, 1, first_token + b, c->stream));
         }
       }
     }
@@ -587,7 +625,9 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
       a.epi = EPI_STORE;
       a.out = R.qkv;
       a.ldo = c->Nqkv;
+      prof_begin(c, P_QKV);
       OK(run_gemv(c, a, B));
+      prof_end(c);
       AttnArgs at = {};
       const size_t kv_layer = (size_t)B * c->KVr * cf.max_seq * hd;
       at.qkv = R.qkv;
@@ -604,7 +644,9 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
       at.counters = R.attn_cnt;
       at.out = R.ob;
       at.err = c->err_dev;
-      CU(launch::attn_decode(at, B, hd, c->G, c->stream));
+      prof_begin(c, P_ATTN);
+      LCU(launch::attn_decode(at, B, hd, c->G, c->stream));
+      prof_end(c);
       GemvArgs o = {};
       o.pro.mode = IN_F32;
       o.pro.in_f32 = R.ob;
@@ -614,7 +656,9 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
       o.epi = EPI_STORE;
       o.out = R.dA;
       o.ldo = d;
+      prof_begin(c, P_OPROJ);
       OK(run_gemv(c, o, B));
+      prof_end(c);
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, B));
     for (auto& R : c->ranks) {
@@ -643,7 +687,9 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
         f.gate_out = gate_act_out + (size_t)l * F + (c->emulated ? (size_t)R.rank * c->Fr : 0);
         f.gate_stride = (long long)L * F;
       }
-      CU(launch::ffn(f, B, ffn_grid, ffn_nslot, c->stream));
+      prof_begin(c, P_FFN);
+      LCU(launch::ffn(f, B, ffn_grid, ffn_nslot, c->stream));
+      prof_end(c);
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
   }
@@ -665,7 +711,9 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
     a.finalize = (cf.tp_size == 1);
     a.done_counter = R.head_cnt;
     a.token_out = token_out;
+    prof_begin(c, P_HEAD);
     OK(run_gemv(c, a, B));
+    prof_end(c);
   }
   if (cf.tp_size > 1) {
     if (!c->emulated) {
@@ -673,7 +721,7 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
       int r = api.allReduce(c->amax, c->amax, B, kNcclUint64, kNcclMax, c->comm, c->stream);
       if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllReduce(max)");
     }
-    CU(launch::argmax_finalize(c->amax, B, token_out, c->stream));
+    LCU(launch::argmax_finalize(c->amax, B, token_out, c->stream));
   }
   CU(cudaGetLastError());
   return SIRIUS_OK;
@@ -691,6 +739,7 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
   OK(check_sticky(c));
   const sirius_config& cf = c->cfg;
   const int B = cf.batch, d = cf.d_model, M = B * gamma;
+  prof_begin(c, P_VERIFY);
   OK(forward_rows(c, kernel_tokens, start_pos, 0, B, gamma, false));
   for (auto& R : c->ranks) {
     NormRowsArgs na = {};
@@ -702,7 +751,7 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
     na.eps = cf.rms_eps;
     na.out_hi = R.xn_hi;
     na.out_lo = R.xn_lo;
-    CU(launch::norm_rows(na, M, c->stream));
+    LCU(launch::norm_rows(na, M, c->stream));
     float* lo = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : R.logits;
     const int ldl = logits_out ? (c->emulated ? cf.vocab : c->Vr) : c->Vr;
     OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Vr, d, M, lo, ldl));
@@ -716,7 +765,7 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
     as.rank = c->emulated ? R.rank : 0;
     as.tokens = kernel_tokens;
     as.stats = c->stats;
-    CU(launch::accept_stats(as, c->accept_splits, c->stream));
+    LCU(launch::accept_stats(as, c->accept_splits, c->stream));
   }
   const RowStat* stats = c->stats;
   int nranks = c->nranks;
@@ -740,7 +789,8 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
   fa.n_accept = n_accept_out;
   fa.next_token = next_token_out;
   fa.q_out = q_out;
-  CU(launch::accept_finalize(fa, B, c->stream));
+  LCU(launch::accept_finalize(fa, B, c->stream));
+  prof_end(c);
   mirror_err(c);
   CU(cudaGetLastError());
   c->last_gamma = gamma;
@@ -768,7 +818,9 @@ sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t*
     a.max_gamma = cf.max_gamma;
     a.gamma = c->last_gamma;
     a.err = c->err_dev;
-    CU(launch::kv_rewrite(a, cf.n_layers, c->stream));
+    prof_begin(c, P_REWRITE);
+    LCU(launch::kv_rewrite(a, cf.n_layers, c->stream));
+    prof_end(c);
   }
   mirror_err(c);
   CU(cudaGetLastError());
@@ -794,6 +846,33 @@ int sirius_nccl_comm_destroy(void* comm) {
   NcclApi& api = nccl();
   if (!api.loaded || !api.commDestroy) return -1;
   return api.commDestroy(comm);
+}
+
+// ---------------------------------------------------------------- bench / test instrumentation
+unsigned long long sirius_debug_launches(const sirius_ctx* c) { return c ? c->launches : 0ull; }
+// enable/disable per-kernel event timing (resets the accumulated records)
+int sirius_debug_profile(sirius_ctx* c, int on) {
+  if (!c) return -1;
+  c->prof_on = on != 0;
+  c->prof_used = 0;
+  return 0;
+}
+// totals_ms[P_NUM], counts[P_NUM]: summed device time per kernel class since enabling (synchronises).
+// ids: 0 QKV GEMV, 1 decode attention, 2 O-proj GEMV, 3 CATS FFN, 4 LM head, 5 correct_kernel, 6 kv_rewrite
+int sirius_debug_profile_read(sirius_ctx* c, float* totals_ms, int* counts) {
+  if (!c) return -1;
+  cudaStreamSynchronize(c->stream);
+  for (int i = 0; i < P_NUM; ++i) {
+    totals_ms[i] = 0.f;
+    counts[i] = 0;
+  }
+  for (size_t i = 0; i < c->prof_used; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->prof[i].a, c->prof[i].b);
+    totals_ms[c->prof[i].id] += ms;
+    counts[c->prof[i].id] += 1;
+  }
+  return 0;
 }
 
 // ---------------------------------------------------------------- test-only: copy an internal buffer

@@ -50,110 +50,128 @@ class Driver:
         self.drafts = torch.zeros((gm + 1, B), dtype=i32, device=dev)   # [i, b]: token_in of step i
         self.kbuf = torch.zeros((B, gm), dtype=i32, device=dev)         # kernel tokens [B, gamma]
         self.pos = torch.zeros((gm, B), dtype=i32, device=dev)          # positions of step i
-        self.start = torch.zeros(B, dtype=i32, device=dev)
+        self.start = [torch.zeros(B, dtype=i32, device=dev) for _ in range(2)]  # ping-pong: this / previous kernel
         self.n_rows = torch.zeros(B, dtype=i32, device=dev)
         self.n_accept = torch.zeros(B, dtype=i32, device=dev)
         self.next_tok = torch.zeros(B, dtype=i32, device=dev)
         self.q = torch.zeros((B, gm), dtype=torch.float32, device=dev)
-        # pinned staging: [n_rows(B) | start(B) | drafts0(B) | pos(gm*B)] out, [n_accept | next | drafts] in
+        # pinned staging: out = [n_rows(B) | start(B) | pending(B) | pos(gm*B)], in = [n_accept | next | drafts]
         self.h_out = torch.zeros(3 * B + gm * B, dtype=i32).pin_memory()
         self.h_in = torch.zeros(2 * B + (gm + 1) * B, dtype=i32).pin_memory()
         self.d_out = torch.zeros(3 * B + gm * B, dtype=i32, device=dev)
         self.d_in = torch.zeros(2 * B + (gm + 1) * B, dtype=i32, device=dev)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
 
-    # ------------------------------------------------------------------ helpers
-    def prefill(self, prompts: Sequence[Sequence[int]]) -> List[int]:
+    # ------------------------------------------------------------------ session state
+    def begin(self, prompts: Sequence[Sequence[int]]) -> None:
+        """Dense prefill; the first generated token is the dense argmax (reading D17)."""
         torch = self.torch
         flat = torch.tensor(np.concatenate([np.asarray(p, dtype=np.int32) for p in prompts]), device="cuda")
         first = torch.zeros(self.B, dtype=torch.int32, device="cuda")
         self.ctx.sirius_prefill(flat, [len(p) for p in prompts], first)
-        return first.cpu().tolist()
+        first = first.cpu().tolist()
+        self.T = [len(p) for p in prompts]
+        self.out = [[f] for f in first]
+        self.pending = list(first)
+        self.n_rows_h = [0] * self.B
+        self.need_rewrite = False
+        self.kidx = 0
+        self.log: List[KernelLog] = []
 
-    def _upload(self, n_rows, start, pending, T, gamma):
+    def _upload(self, gamma: int) -> None:
         B = self.B
         h = self.h_out.numpy()
-        h[0:B] = n_rows
-        h[B:2 * B] = start
-        h[2 * B:3 * B] = pending
-        pos = (np.asarray(T, dtype=np.int64)[None, :] + np.arange(gamma)[:, None]).astype(np.int32)
+        h[0:B] = self.n_rows_h
+        h[B:2 * B] = self.T
+        h[2 * B:3 * B] = self.pending
+        pos = (np.asarray(self.T, dtype=np.int64)[None, :] + np.arange(gamma)[:, None]).astype(np.int32)
         h[3 * B:3 * B + gamma * B] = pos.reshape(-1)
-        self.d_out[:3 * B + gamma * B].copy_(self.h_out[:3 * B + gamma * B], non_blocking=True)
+        n = 3 * B + gamma * B
+        self.d_out[:n].copy_(self.h_out[:n], non_blocking=True)
+        self.h2d_bytes += 4 * n
 
-    # ------------------------------------------------------------------ baselines
+    def flush(self) -> None:
+        """Commit the last kernel's rows (kv_rewrite) and wait for the stream."""
+        if self.need_rewrite:
+            B = self.B
+            self._upload(1)
+            self.n_rows.copy_(self.d_out[0:B])
+            self.ctx.kv_rewrite(self.start[(self.kidx - 1) % 2], self.n_rows)
+            self.need_rewrite = False
+        self.torch.cuda.current_stream().synchronize()
+
+    def step(self, gamma: int, r: float, accept_mode: int = S.ACCEPT_THRESHOLD, keep_q: bool = False) -> int:
+        """One correction kernel (kernel size gamma): M_S drafts gamma-1 tokens, M_F verifies,
+        accept/reject + interleave; the previous kernel's KV rewrite is enqueued first.  Returns the
+        number of tokens committed for sequence 0."""
+        torch, B = self.torch, self.B
+        assert 1 <= gamma <= self.gmax
+        self._upload(gamma)
+        d = self.d_out
+        cur = self.start[self.kidx % 2]
+        self.n_rows.copy_(d[0:B])
+        cur.copy_(d[B:2 * B])
+        self.drafts[0].copy_(d[2 * B:3 * B])
+        self.pos[:gamma].copy_(d[3 * B:3 * B + gamma * B].view(gamma, B))
+        if self.need_rewrite:  # commit + rollback of the previous kernel (PAPER.md:257, :264)
+            self.ctx.kv_rewrite(self.start[(self.kidx - 1) % 2], self.n_rows)
+        for i in range(gamma - 1):  # M_S drafts gamma-1 tokens (Alg. 1 lines 6-11)
+            self.ctx.sparse_decode_step(self.drafts[i], self.pos[i], 0, self.drafts[i + 1])
+        if B == 1:
+            kt = self.drafts[:gamma].view(1, gamma)
+        else:
+            self.kbuf[:, :gamma].copy_(self.drafts[:gamma].t())
+            kt = self.kbuf[:, :gamma].contiguous()
+        self.ctx.correct_kernel(kt, cur, gamma, r, accept_mode, self.n_accept, self.next_tok,
+                                self.q if keep_q else None)
+        # D2H: accepted count, interleaved token, drafts (the one sync per kernel)
+        n = 2 * B + gamma * B
+        self.d_in[0:B].copy_(self.n_accept)
+        self.d_in[B:2 * B].copy_(self.next_tok)
+        self.d_in[2 * B:n].copy_(self.drafts[:gamma].reshape(-1))
+        self.h_in[:n].copy_(self.d_in[:n], non_blocking=True)
+        self.d2h_bytes += 4 * n
+        torch.cuda.current_stream().synchronize()
+        h = self.h_in.numpy()
+        j = h[0:B].copy()
+        nxt = h[B:2 * B].copy()
+        dr = h[2 * B:n].reshape(gamma, B)
+        self.log.append(KernelLog(list(self.T), dr.T.copy(), j, nxt,
+                                  self.q[:, :gamma].cpu().numpy() if keep_q else None))
+        for b in range(B):
+            jb = int(j[b])
+            self.out[b] += [int(x) for x in dr[1:jb + 1, b]] + [int(nxt[b])]
+            self.n_rows_h[b] = jb + 1
+            self.T[b] += jb + 1
+            self.pending[b] = int(nxt[b])
+        self.need_rewrite = True
+        self.kidx += 1
+        return int(j[0]) + 1
+
+    # ------------------------------------------------------------------ whole generations
+    def sirius(self, prompts, n_tokens: int, gamma: int, r: float, accept_mode: int = S.ACCEPT_THRESHOLD,
+               keep_q: bool = False) -> GenOut:
+        self.begin(prompts)
+        while min(len(o) for o in self.out) < n_tokens:
+            self.step(gamma, r, accept_mode, keep_q)
+        self.flush()
+        return GenOut([o[:n_tokens] for o in self.out], list(self.log))
+
     def greedy(self, prompts, n_tokens: int, dense: bool) -> GenOut:
         """Plain greedy decode (dense M_F or CS-only M_S) after a dense prefill."""
         torch, B = self.torch, self.B
-        first = self.prefill(prompts)
-        P = [len(p) for p in prompts]
-        out = [[f] for f in first]
+        self.begin(prompts)
+        P = self.T
         toks = torch.zeros((n_tokens, B), dtype=torch.int32, device="cuda")
-        toks[0] = torch.tensor(first, dtype=torch.int32)
+        toks[0] = torch.tensor(self.pending, dtype=torch.int32)
         pos = torch.tensor(np.array([[P[b] + i for b in range(B)] for i in range(n_tokens)], dtype=np.int32),
                            device="cuda")
-        flags = S.SIRIUS_DENSE if dense else 0
-        for i in range(n_tokens - 1):
-            self.ctx.sparse_decode_step(toks[i], pos[i], flags, toks[i + 1])
+        self.greedy_steps(toks, pos, n_tokens - 1, dense)
         host = toks.cpu().numpy()
-        for b in range(B):
-            out[b] = host[:, b].tolist()
-        return GenOut(out, steps=n_tokens - 1)
+        return GenOut([host[:, b].tolist() for b in range(B)], steps=n_tokens - 1)
 
-    # ------------------------------------------------------------------ Sirius
-    def sirius(self, prompts, n_tokens: int, gamma: int, r: float, accept_mode: int = S.ACCEPT_THRESHOLD,
-               keep_q: bool = False) -> GenOut:
-        torch, B = self.torch, self.B
-        assert 1 <= gamma <= self.gmax
-        first = self.prefill(prompts)
-        T = [len(p) for p in prompts]
-        out = [[f] for f in first]
-        res = GenOut(out)
-        pending = list(first)
-        n_rows = [0] * B
-        first_kernel = True
-        while min(len(o) for o in out) < n_tokens:
-            # H2D: previous kernel's n_rows, this kernel's start / pending token / positions
-            self._upload(n_rows, T, pending, T, gamma)
-            d = self.d_out
-            self.n_rows.copy_(d[0:B])
-            self.start.copy_(d[B:2 * B])
-            self.drafts[0].copy_(d[2 * B:3 * B])
-            self.pos[:gamma].copy_(d[3 * B:3 * B + gamma * B].view(gamma, B))
-            if not first_kernel:  # commit + rollback of the previous kernel (PAPER.md:257, :264)
-                self.ctx.kv_rewrite(self.prev_start, self.n_rows)
-            for i in range(gamma - 1):  # M_S drafts gamma-1 tokens (Alg. 1 lines 6-11)
-                self.ctx.sparse_decode_step(self.drafts[i], self.pos[i], 0, self.drafts[i + 1])
-                res.steps += 1
-            if B == 1:
-                kt = self.drafts[:gamma].view(1, gamma)
-            else:
-                self.kbuf[:, :gamma].copy_(self.drafts[:gamma].t())
-                kt = self.kbuf[:, :gamma].contiguous()
-            self.ctx.correct_kernel(kt, self.start, gamma, r, accept_mode, self.n_accept, self.next_tok,
-                                    self.q if keep_q else None)
-            # D2H: accepted count, interleaved token, drafts (one sync per kernel)
-            self.d_in[0:B].copy_(self.n_accept)
-            self.d_in[B:2 * B].copy_(self.next_tok)
-            self.d_in[2 * B:2 * B + gamma * B].copy_(self.drafts[:gamma].reshape(-1))
-            self.h_in[:2 * B + gamma * B].copy_(self.d_in[:2 * B + gamma * B], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            h = self.h_in.numpy()
-            j = h[0:B].copy()
-            nxt = h[B:2 * B].copy()
-            dr = h[2 * B:2 * B + gamma * B].reshape(gamma, B)
-            kl = KernelLog(list(T), dr.T.copy(), j, nxt, self.q[:, :gamma].cpu().numpy() if keep_q else None)
-            res.kernels.append(kl)
-            self.prev_start = self.start.clone()
-            for b in range(B):
-                jb = int(j[b])
-                out[b] += [int(x) for x in dr[1:jb + 1, b]] + [int(nxt[b])]
-                n_rows[b] = jb + 1
-                T[b] += jb + 1
-                pending[b] = int(nxt[b])
-            first_kernel = False
-        # final commit of the last kernel
-        self._upload(n_rows, T, pending, T, 1)
-        self.n_rows.copy_(self.d_out[0:B])
-        self.ctx.kv_rewrite(self.prev_start, self.n_rows)
-        torch.cuda.current_stream().synchronize()
-        res.tokens = [o[:n_tokens] for o in out]
-        return res
+    def greedy_steps(self, toks, pos, n: int, dense: bool, first: int = 0) -> None:
+        flags = S.SIRIUS_DENSE if dense else 0
+        for i in range(first, first + n):
+            self.ctx.sparse_decode_step(toks[i], pos[i], flags, toks[i + 1])

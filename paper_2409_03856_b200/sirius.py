@@ -79,6 +79,12 @@ def load():
         lib.sirius_debug_gemm.argtypes = [P, P, I, P, P, P, P, I, I, I]
         lib.sirius_debug_buffer.argtypes = [P, I, I, P, ctypes.c_size_t]
         lib.sirius_debug_buffer.restype = I
+        lib.sirius_debug_launches.argtypes = [P]
+        lib.sirius_debug_launches.restype = ctypes.c_ulonglong
+        lib.sirius_debug_profile.argtypes = [P, I]
+        lib.sirius_debug_profile.restype = I
+        lib.sirius_debug_profile_read.argtypes = [P, P, P]
+        lib.sirius_debug_profile_read.restype = I
         lib.sirius_debug_gemm.restype = I
         lib.sirius_nccl_available.restype = I
         lib.sirius_nccl_unique_id.argtypes = [P]
@@ -159,6 +165,24 @@ class Sirius:
 
     def kv_rewrite(self, start_pos, n_rows):
         self._check(self.lib.kv_rewrite(self.h, _ptr(start_pos), _ptr(n_rows)))
+
+    # ---- instrumentation (bench / tests) ------------------------------------------------
+    PROF_NAMES = ("qkv_gemv", "attn_decode", "oproj_gemv", "cats_ffn", "lm_head", "correct_kernel", "kv_rewrite")
+
+    def launches(self) -> int:
+        """Kernels this context has launched so far (library-side counter)."""
+        return int(self.lib.sirius_debug_launches(self.h))
+
+    def profile(self, on: bool) -> None:
+        self.lib.sirius_debug_profile(self.h, 1 if on else 0)
+
+    def profile_read(self) -> Dict[str, tuple]:
+        """{kernel class: (total device ms, launches)} since profile(True); CUDA events on the
+        library's stream around each launch."""
+        tot = (ctypes.c_float * 8)()
+        cnt = (ctypes.c_int * 8)()
+        self.lib.sirius_debug_profile_read(self.h, tot, cnt)
+        return {n: (float(tot[i]), int(cnt[i])) for i, n in enumerate(self.PROF_NAMES)}
 
     def sirius_destroy(self):
         if getattr(self, "h", None):
