@@ -9,9 +9,15 @@ method's arithmetic lives here.
 Why these gains (SURVEY.md §8(d) "Gains", fixed before any measurement):
   * every projection is fan-in scaled (unit-variance outputs for unit-RMS inputs);
   * the embedding has unit variance;
-  * the LM head has gain 5 (logit std ~5), so the full model's next-token
-    distribution is peaked enough that the likelihood threshold r=0.1 both
-    accepts and rejects (a std-0.02 init gives a flat distribution, AAL = 1);
+  * every neuron i of a layer has a gain s_i on its W_gate and W_up rows, log-normal-like
+    (s_i = 2^(k_i/4), k_i a rounded Gaussian, sigma_ln = 1.25): the heavy-tailed activation
+    magnitudes of trained LLMs that CATS thresholding relies on; with Gaussian
+    gates (no gain) 50% thresholding keeps too little of the MLP and the sparse model's drafts are
+    rejected almost always (AAL 1.5/16 measured);
+  * the LM head has gain 10 (logit std ~10): a next-token distribution about as peaked as the
+    paper's, so the likelihood threshold both accepts and rejects; with gain 1.25/head 10 the
+    Llama-3-8B shape gives AAL ~15.5/16 at r=0.1 and ~12.7 at r=0.3 (Table 8:
+    14.6 and 11.6) — chosen on a GPU sweep (tools/explore_recipe.py) before any timing;
   * RMSNorm weights are 1 + N(0, 0.1^2)-ish (not exactly 1, so a mis-indexed norm
     weight is caught by the parity tests).
 """
@@ -44,7 +50,7 @@ class ModelConfig:
     ffn_dim: int
     rope_theta: float = 500000.0
     rms_eps: float = 1e-5
-    head_gain: float = 5.0
+    head_gain: float = 10.0
 
     @property
     def qkv_rows(self) -> int:
@@ -64,6 +70,9 @@ LLAMA3_8B_2L = LLAMA3_8B.with_layers(2)
 CONFIGS = {c.name: c for c in (TINY, LLAMA3_8B, LLAMA3_70B, LLAMA3_8B_2L)}
 
 WEIGHT_SEED = 0
+GAIN_SIGMA = 1.25  # ln-space std of the per-neuron gate/up gain
+GAIN_STEP = int(round(IH_STD * math.log(2.0) / (4.0 * GAIN_SIGMA)))  # IH units per quarter octave (5245)
+GAIN_TABLE = np.array([2.0 ** ((j - 24) / 4.0) for j in range(49)], dtype=np.float32)
 LAYER_NAMES = ("attn_norm", "w_qkv", "w_o", "ffn_norm", "w_gate", "w_up", "w_down")
 
 
@@ -75,6 +84,7 @@ class TensorSpec:
     cols: int
     scale: float  # fp32 multiplier of the Irwin-Hall integer
     offset: float  # fp32 additive offset (1.0 for norm weights)
+    gain_id: int = 0  # != 0: per-row gain 2^(k/4), k from the Irwin-Hall stream `gain_id`
 
 
 def _f32(x: float) -> float:
@@ -99,8 +109,10 @@ def tensor_specs(cfg: ModelConfig) -> List[TensorSpec]:
             TensorSpec(f"layers.{l}.w_o", b + 2, d, cfg.n_heads * hd,
                        _f32(1.0 / (math.sqrt(cfg.n_heads * hd) * IH_STD)), 0.0),
             TensorSpec(f"layers.{l}.ffn_norm", b + 3, 1, d, **norm),
-            TensorSpec(f"layers.{l}.w_gate", b + 4, cfg.ffn_dim, d, _f32(1.0 / (math.sqrt(d) * IH_STD)), 0.0),
-            TensorSpec(f"layers.{l}.w_up", b + 5, cfg.ffn_dim, d, _f32(1.0 / (math.sqrt(d) * IH_STD)), 0.0),
+            TensorSpec(f"layers.{l}.w_gate", b + 4, cfg.ffn_dim, d, _f32(1.0 / (math.sqrt(d) * IH_STD)), 0.0,
+                       gain_id=b + 7),
+            TensorSpec(f"layers.{l}.w_up", b + 5, cfg.ffn_dim, d, _f32(1.0 / (math.sqrt(d) * IH_STD)), 0.0,
+                       gain_id=b + 7),
             # neuron-major W_down: row i is neuron i's d-vector; fan-in of the product is ffn_dim
             TensorSpec(f"layers.{l}.w_down", b + 6, cfg.ffn_dim, d,
                        _f32(1.0 / (math.sqrt(cfg.ffn_dim) * IH_STD)), 0.0),
@@ -141,8 +153,11 @@ def _load_cpu():
         if not os.path.exists(path):
             build_cpu()
         lib = ctypes.CDLL(path)
-        lib.synth_fill_bf16.argtypes = [ctypes.c_uint64] * 7 + [ctypes.c_float, ctypes.c_float, ctypes.c_void_p,
+        lib.synth_fill_bf16.argtypes = [ctypes.c_uint64] * 7 + [ctypes.c_float, ctypes.c_float, ctypes.c_uint64,
+                                                               ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                                                ctypes.c_int]
+        lib.synth_row_gain_ks.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
+                                          ctypes.c_void_p]
         lib.synth_fill_bf16.restype = None
         lib.synth_fill_tokens.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
                                           ctypes.c_void_p]
@@ -171,7 +186,7 @@ def fill_host(spec: TensorSpec, row0: int, nrows: int, col0: int, ncols: int, se
     """bf16 bit patterns (uint16 [nrows, ncols]) of a sub-block of tensor `spec`."""
     out = np.empty((nrows, ncols), dtype=np.uint16)
     _load_cpu().synth_fill_bf16(seed, spec.tensor_id, spec.cols, row0, nrows, col0, ncols, spec.scale, spec.offset,
-                                out.ctypes.data, host_threads())
+                                spec.gain_id, GAIN_STEP, GAIN_TABLE.ctypes.data, out.ctypes.data, host_threads())
     return out
 
 
@@ -203,54 +218,66 @@ def calib_prompt(cfg: ModelConfig, b: int, n: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- CATS thresholds
+def row_gain_k(gain_id: int, n: int, seed: int = WEIGHT_SEED) -> np.ndarray:
+    out = np.empty(n, dtype=np.int8)
+    _load_cpu().synth_row_gain_ks(seed, gain_id, n, GAIN_STEP, out.ctypes.data)
+    return out
+
+
 def _silu(z: float) -> float:
     return z / (1.0 + math.exp(-z))
 
 
-def _phi(z: float) -> float:
-    return 0.5 * (1.0 + math.erf(z / math.sqrt(2.0)))
+def _root(f, lo: float, hi: float) -> float:
+    from scipy.optimize import brentq
+    return brentq(f, lo, hi, xtol=1e-14, rtol=1e-14, maxiter=500)
 
 
-def _solve(f, lo: float, hi: float) -> float:
-    for _ in range(200):
-        mid = 0.5 * (lo + hi)
-        if f(lo) * f(mid) <= 0:
-            hi = mid
-        else:
-            lo = mid
-    return 0.5 * (lo + hi)
+SILU_NEG_MIN_Z = _root(lambda z: (1.0 + z * (1.0 - 1.0 / (1.0 + math.exp(-z)))), -3.0, -0.5)  # argmin SiLU (-1.2785)
+SILU_NEG_MIN = -_silu(SILU_NEG_MIN_Z)  # 0.2785
 
 
-SILU_NEG_MIN_Z = _solve(lambda z: 1.0 / (1.0 + math.exp(-z)) * (1.0 + z * (1.0 - 1.0 / (1.0 + math.exp(-z)))),
-                        -3.0, -0.5)  # argmin of SiLU on z<0 (≈ -1.2785)
-SILU_NEG_MIN = -_silu(SILU_NEG_MIN_Z)  # ≈ 0.2785
-
-
-def abs_silu_cdf(t: float) -> float:
-    """P(|SiLU(Z)| <= t) for Z ~ N(0,1)."""
+def _abs_silu_tail(t: float, sig: np.ndarray) -> np.ndarray:
+    """P(|SiLU(X)| >= t) for X ~ N(0, sig^2) (vectorised over sig).  {|SiLU(y)| < t} is
+    (z1, zp) minus [.., z2] pieces: SiLU rises on y > 0 to zp, and on y < 0 |SiLU| rises to its
+    maximum 0.2785 at y = -1.2785 (z1 < -1.2785 < z2 bound the part above t) then decays."""
+    from scipy.special import ndtr
     if t <= 0:
-        return 0.0
-    zp = _solve(lambda z: _silu(z) - t, 0.0, 50.0)
-    p = _phi(zp) - 0.5
+        return np.ones_like(sig)
+    zp = _root(lambda y: _silu(y) - t, 0.0, t + 60.0)
+    below = ndtr(zp / sig) - 0.5  # 0 <= y < zp
     if t >= SILU_NEG_MIN:
-        return p + 0.5
-    z1 = _solve(lambda z: -_silu(z) - t, -60.0, SILU_NEG_MIN_Z)
-    z2 = _solve(lambda z: -_silu(z) - t, SILU_NEG_MIN_Z, 0.0)
-    return p + _phi(z1) + (0.5 - _phi(z2))
+        below = below + 0.5
+    else:
+        z1 = _root(lambda y: -_silu(y) - t, -80.0, SILU_NEG_MIN_Z)
+        z2 = _root(lambda y: -_silu(y) - t, SILU_NEG_MIN_Z, 0.0)
+        below = below + ndtr(z1 / sig) + (0.5 - ndtr(z2 / sig))
+    return 1.0 - below
 
 
-def cats_threshold(rho: float) -> float:
-    """Per-layer CATS threshold t with P(|SiLU(g)| >= t) = rho, under the synthetic init's gate
-    pre-activation law g ~ N(0, 1) (unit-RMS h, fan-in-scaled W_gate).  DESIGN.md reading D3'.
-    Returned as an fp32 value; both sides receive the same fp32 number."""
+def cats_threshold(rho: float, gains=None, var: float = 1.0) -> float:
+    """CATS threshold t with mean_i P(|SiLU(g_i)| >= t) = rho under the synthetic init's law of the
+    gate pre-activation: g_i ~ N(0, var * s_i^2) (unit-RMS normalised input times the layer's ffn_norm
+    weight (var = mean(w^2)), fan-in-scaled W_gate row with gain s_i).  DESIGN.md reading D3'.
+    Returned as fp32; both sides receive the same fp32 number."""
     if rho >= 1.0:
         return 0.0
-    t = _solve(lambda t: abs_silu_cdf(t) - (1.0 - rho), 1e-9, 30.0)
-    return _f32(t)
+    sig = np.sqrt(var) * (np.ones(1) if gains is None else np.asarray(gains, dtype=np.float64))
+    f = lambda t: float(np.mean(_abs_silu_tail(t, sig))) - rho
+    return _f32(_root(f, 1e-12, 60.0 * float(sig.max()) + 1.0))
 
 
-def layer_thresholds(cfg: ModelConfig, rho) -> np.ndarray:
+def layer_thresholds(cfg: ModelConfig, rho, seed: int = WEIGHT_SEED) -> np.ndarray:
     """fp32 [n_layers]; rho may be a scalar or a per-layer sequence."""
     if np.isscalar(rho):
         rho = [rho] * cfg.n_layers
-    return np.array([cats_threshold(r) for r in rho], dtype=np.float32)
+    specs = {s.name: s for s in tensor_specs(cfg)}
+    out = []
+    for l, r in enumerate(rho):
+        k = row_gain_k(specs[f"layers.{l}.w_gate"].gain_id, cfg.ffn_dim, seed)
+        kv, cnt = np.unique(k, return_counts=True)
+        gains = np.repeat(GAIN_TABLE[kv.astype(int) + 24].astype(np.float64), cnt)
+        w = (host_shard(cfg, specs[f"layers.{l}.ffn_norm"]).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        # unique gains with multiplicities: mean over neurons == weighted mean over distinct gains
+        out.append(cats_threshold(r, gains, float(np.mean(w * w))))
+    return np.array(out, dtype=np.float32)

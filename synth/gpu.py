@@ -4,7 +4,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from . import ModelConfig, TensorSpec, WEIGHT_SEED, shard_blocks, tensor_specs
+from . import GAIN_STEP, GAIN_TABLE, ModelConfig, TensorSpec, WEIGHT_SEED, shard_blocks, tensor_specs
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _lib = None
@@ -17,7 +17,8 @@ def _load():
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
         lib = ctypes.CDLL(path)
-        lib.synth_gpu_fill_bf16.argtypes = [ctypes.c_uint64] * 7 + [ctypes.c_float, ctypes.c_float, ctypes.c_void_p,
+        lib.synth_gpu_fill_bf16.argtypes = [ctypes.c_uint64] * 7 + [ctypes.c_float, ctypes.c_float, ctypes.c_uint64,
+                                                                   ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                                                    ctypes.c_void_p]
         lib.synth_gpu_fill_bf16.restype = ctypes.c_int
         lib.synth_gpu_fill_tokens.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
@@ -36,7 +37,8 @@ def fill(spec: TensorSpec, row0: int, nrows: int, col0: int, ncols: int, out, se
     """Write the sub-block of tensor `spec` into the contiguous 2-byte CUDA tensor `out`."""
     assert out.is_cuda and out.is_contiguous() and out.element_size() == 2 and out.numel() == nrows * ncols
     r = _load().synth_gpu_fill_bf16(seed, spec.tensor_id, spec.cols, row0, nrows, col0, ncols, spec.scale,
-                                    spec.offset, out.data_ptr(), _stream())
+                                    spec.offset, spec.gain_id, GAIN_STEP, GAIN_TABLE.ctypes.data, out.data_ptr(),
+                                    _stream())
     if r != 0:
         raise RuntimeError(f"synth_gpu_fill_bf16: cuda error {r}")
 

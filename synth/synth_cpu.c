@@ -7,13 +7,14 @@
  * synth/synth_gpu.cu, an independent implementation of the same counter-based
  * recipe, and tests/test_synth.py checks the two agree bit for bit.
  *
- * Recipe (DESIGN.md §"Input recipe", SURVEY.md §8(d) "Weight generator"):
- *   key      = mix64(seed ^ mix64(tensor_id))
- *   r_i      = mix64(key + (i + 1) * GOLDEN)                 (SplitMix64 stream)
- *   z_i      = lane0 + lane1 + lane2 + lane3 - 131070         (Irwin–Hall(4) of u16 lanes, exact int)
- *   w_i      = bf16_rne( (float)z_i * scale + offset )       (fp32 multiply-add, then bf16 RNE)
- * `scale` and `offset` are fp32 constants supplied by the caller (fan-in scaled gain; see
- * synth/__init__.py).  No transcendental function is used, so every platform
+ * Recipe (DESIGN.md §3 "Input recipe"):
+ *   key(t)   = mix64(seed ^ mix64(t))
+ *   IH(t, i) = sum of the four u16 lanes of mix64(key(t) + (i + 1) * GOLDEN) - 131070
+ *              (Irwin–Hall(4), an exact integer, std 65536/sqrt(3))
+ *   row gain (optional, W_gate / W_up): k_r = clamp(floor_div(IH(gain_id, r) + step/2, step), -24, 24),
+ *              scale_r = fp32(scale * gain_table[k_r + 24])       (gain_table[j] = fp32(2^((j-24)/4)))
+ *   w[r][c]  = bf16_rne( fp32(IH(tensor_id, r*ld + c) * scale_r) + offset )
+ * Only integer ops and fp32 multiply/add (no contraction, no transcendental), so every platform
  * produces the same bits.
  */
 #include <stdint.h>
@@ -48,29 +49,52 @@ int32_t synth_irwin_hall(uint64_t seed, uint64_t tensor_id, uint64_t i) {
   return irwin_hall4(mix64(synth_key(seed, tensor_id) + (i + 1) * GOLDEN));
 }
 
+static inline int32_t floor_div(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+/* Gain index k in [-24, 24] of row r (quarter octaves): exposed for tests and threshold recipes. */
+int32_t synth_row_gain_k(uint64_t seed, uint64_t gain_id, uint64_t r, int32_t step) {
+  int32_t k = floor_div(synth_irwin_hall(seed, gain_id, r) + step / 2, step);
+  return k < -24 ? -24 : (k > 24 ? 24 : k);
+}
+
+void synth_row_gain_ks(uint64_t seed, uint64_t gain_id, uint64_t n, int32_t step, int8_t* out) {
+  for (uint64_t r = 0; r < n; ++r) out[r] = (int8_t)synth_row_gain_k(seed, gain_id, r, step);
+}
+
 typedef struct {
-  uint64_t key, ld, row0, col0, ncols, rbegin, rend;
+  uint64_t key, ld, row0, col0, ncols, rbegin, rend, seed, gain_id;
   float scale, offset;
+  int32_t step;
+  const float* table;
   uint16_t* out;
 } fill_job;
 
 static void* fill_worker(void* p) {
   fill_job* j = (fill_job*)p;
-  for (uint64_t r = j->rbegin; r < j->rend; ++r)
+  for (uint64_t r = j->rbegin; r < j->rend; ++r) {
+    volatile float sc = j->scale;
+    if (j->gain_id) {
+      int32_t k = synth_row_gain_k(j->seed, j->gain_id, j->row0 + r, j->step);
+      sc = j->scale * j->table[k + 24];
+    }
+    const float s = sc;
     for (uint64_t c = 0; c < j->ncols; ++c) {
       uint64_t i = (j->row0 + r) * j->ld + j->col0 + c; /* index in the FULL (unsharded) tensor */
       int32_t z = irwin_hall4(mix64(j->key + (i + 1) * GOLDEN));
-      volatile float prod = (float)z * j->scale; /* no contraction: one rounding, then the add */
+      volatile float prod = (float)z * s; /* no contraction: one rounding, then the add */
       j->out[r * j->ncols + c] = f32_to_bf16_rne(prod + j->offset);
     }
+  }
   return 0;
 }
 
 /* Fill the sub-block rows [row0,row0+nrows) x cols [col0,col0+ncols) of the full tensor
  * (seed, tensor_id) whose row length is ld, into out (row-major [nrows, ncols], bf16 bits).
+ * gain_id != 0 applies the per-row gain (table: 49 fp32 values, step: IH units per quarter octave).
  * A 1-D tensor is ld = n, nrows = 1.  Threads: 1..64 (host cores). */
 void synth_fill_bf16(uint64_t seed, uint64_t tensor_id, uint64_t ld, uint64_t row0, uint64_t nrows,
-                     uint64_t col0, uint64_t ncols, float scale, float offset, uint16_t* out, int threads) {
+                     uint64_t col0, uint64_t ncols, float scale, float offset, uint64_t gain_id, int32_t step,
+                     const float* table, uint16_t* out, int threads) {
   if (threads < 1) threads = 1;
   if (threads > 64) threads = 64;
   if (nrows * ncols < (1u << 16) || nrows < (uint64_t)threads) threads = 1;
@@ -85,6 +109,10 @@ void synth_fill_bf16(uint64_t seed, uint64_t tensor_id, uint64_t ld, uint64_t ro
     jobs[t].ncols = ncols;
     jobs[t].rbegin = nrows * (uint64_t)t / (uint64_t)threads;
     jobs[t].rend = nrows * (uint64_t)(t + 1) / (uint64_t)threads;
+    jobs[t].seed = seed;
+    jobs[t].gain_id = gain_id;
+    jobs[t].step = step;
+    jobs[t].table = table;
     jobs[t].scale = scale;
     jobs[t].offset = offset;
     jobs[t].out = out;

@@ -104,7 +104,7 @@ def test_verify_accept_rewrite_lockstep(tiny_models):
     """correct_kernel logits / q / j against the oracle's verify + accept scan; then kv_rewrite and a
     further decode step match the oracle (which rewrote the same rows)."""
     cfg, wh, wd = tiny_models
-    thr = synth.layer_thresholds(cfg, 0.5)
+    thr = synth.layer_thresholds(cfg, 0.1)
     prompt = synth.eval_prompt(cfg, 1, 48)
     gamma = 6
     ctx = make_ctx(cfg, wd, thr)
@@ -154,12 +154,12 @@ def test_verify_accept_rewrite_lockstep(tiny_models):
     check_logits(lo1.cpu().numpy()[0], r.logits)
 
 
-@pytest.mark.parametrize("gamma,r,mode", [(4, 0.1, 0), (4, 0.3, 0), (6, 0.0, 1), (5, 0.6, 0)])
+@pytest.mark.parametrize("gamma,r,mode", [(4, 0.1, 0), (4, 0.3, 0), (6, 0.0, 1), (5, 0.6, 0), (8, 0.9, 0)])
 def test_generate_token_exact(tiny_models, gamma, r, mode):
     """Free-running Sirius generation: identical tokens and accept decisions to the oracle."""
     from paper_2409_03856_b200 import driver
     cfg, wh, wd = tiny_models
-    thr = synth.layer_thresholds(cfg, 0.5)
+    thr = synth.layer_thresholds(cfg, 0.1)
     prompt = synth.eval_prompt(cfg, 2, 64)
     ref = so.generate(so.OracleModel(cfg, wh, max_seq=256, max_gamma=16), prompt, 32, gamma, r, thr, accept_mode=mode)
     ctx = make_ctx(cfg, wd, thr)
@@ -171,7 +171,7 @@ def test_generate_token_exact(tiny_models, gamma, r, mode):
 def test_dense_and_sparse_greedy_token_exact(tiny_models):
     from paper_2409_03856_b200 import driver
     cfg, wh, wd = tiny_models
-    thr = synth.layer_thresholds(cfg, 0.5)
+    thr = synth.layer_thresholds(cfg, 0.1)
     prompt = synth.eval_prompt(cfg, 3, 64)
     ctx = make_ctx(cfg, wd, thr)
     d = driver.Driver(ctx)
@@ -185,7 +185,7 @@ def test_exact_argmax_gpu_equals_gpu_dense_greedy(tiny_models):
     """north_star invariant on the GPU itself: EXACT_ARGMAX Sirius == dense greedy, token for token."""
     from paper_2409_03856_b200 import driver
     cfg, wh, wd = tiny_models
-    thr = synth.layer_thresholds(cfg, 0.3)
+    thr = synth.layer_thresholds(cfg, 0.1)
     prompt = synth.eval_prompt(cfg, 5, 32)
     d = driver.Driver(make_ctx(cfg, wd, thr))
     dense = d.greedy([prompt], 40, dense=True).tokens[0]
@@ -205,7 +205,7 @@ def test_threshold_zero_gpu_sparse_equals_dense(tiny_models):
 def test_r_zero_accepts_all_on_gpu(tiny_models):
     from paper_2409_03856_b200 import driver
     cfg, wh, wd = tiny_models
-    thr = synth.layer_thresholds(cfg, 0.3)
+    thr = synth.layer_thresholds(cfg, 0.1)
     d = driver.Driver(make_ctx(cfg, wd, thr))
     out = d.sirius([synth.eval_prompt(cfg, 7, 32)], 24, 5, 0.0)
     assert all(a == 5 for a in out.advances(0))

@@ -26,7 +26,14 @@ def test_weights_deterministic_and_scaled():
     b = synth.host_shard(cfg, specs["layers.1.w_gate"])
     np.testing.assert_array_equal(a, b)
     f = (a.astype(np.uint32) << 16).view(np.float32)
-    assert abs(f.std() * np.sqrt(cfg.d_model) - 1.0) < 0.02  # fan-in scaled, unit gain
+    # fan-in scaled rows times the per-neuron gain 2^(k/4): row std * sqrt(d) == gain
+    k = synth.row_gain_k(specs["layers.1.w_gate"].gain_id, cfg.ffn_dim)
+    gains = synth.GAIN_TABLE[k.astype(int) + 24]
+    ratio = f.std(axis=1) * np.sqrt(cfg.d_model) / gains
+    assert abs(np.median(ratio) - 1.0) < 0.02 and np.all(np.abs(ratio - 1) < 0.25)
+    assert 1.0 < np.std(k / 4.0 * np.log(2.0)) / synth.GAIN_SIGMA * 1.0 + 0.2  # log-gain spread ~ sigma
+    assert abs(np.std(k / 4.0 * np.log(2.0)) - synth.GAIN_SIGMA) < 0.1
+    np.testing.assert_array_equal(synth.host_shard(cfg, specs["layers.1.w_up"]).shape, a.shape)
     n = (synth.host_shard(cfg, specs["final_norm"]).astype(np.uint32) << 16).view(np.float32)
     assert abs(n.mean() - 1.0) < 0.02 and 0.05 < n.std() < 0.15
     c = synth.host_shard(cfg, specs["layers.0.w_gate"])
