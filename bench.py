@@ -358,6 +358,7 @@ def main():
                     "note": "wall clock of the same K kernels through the C ABI; per kernel the positions/pending "
                             "token go H2D from pinned host memory and the accepted count + drafted tokens come back D2H"},
             "gpu_launches": launches,
+            "cuda_graphs": ctx.graphs(),
             "clocks": ck,
             "setup_s": setup_s,
         }

@@ -1,0 +1,436 @@
+// gemv_ffn.cu — the HBM-bound weight-streaming kernels of the decode step.
+//
+//  * gemv_kernel : y[b, r] = sum_k W[r, k] h[b, k] for the QKV, O-proj and LM-head GEMVs.  One warp per
+//                  row; every lane issues all of its 128-bit weight loads for the row before using
+//                  them (16 KB+ in flight per warp, 2 CTAs x 8 warps per SM), the fp32 activation rows
+//                  sit in shared memory as two float4 "planes" so the per-chunk reads are
+//                  bank-conflict free; warp-shuffle reduction.  Prologue fuses residual add + RMSNorm
+//                  (or the embedding gather).  Epilogues: store, or packed (value, lowest index) argmax.
+//  * ffn_kernel  : the CATS-sparse MLP of one layer in one
+//                  cooperative launch, one CTA (16 warps) per SM, neurons split evenly over the CTAs:
+//                    A  dense gate rows -> g -> a = SiLU(g)                        (warp per row)
+//                    B  CATS threshold |a| >= t_l, warp-ballot compaction per 32-neuron chunk
+//                    C  ACTIVE W_up rows only -> u -> m = a * u                    (warp per row)
+//                    D  ACTIVE W_down rows only -> y += m * W_down[n]   (threads own output columns)
+//                  so HBM bytes scale with the density; grid barrier; deterministic column reduction
+//                  of the per-CTA partial outputs.
+// Design note: an earlier version staged rows through a 1-D bulk-copy (TMA) mbarrier
+// ring; the per-row handoff capped it at ~3.3 TB/s for 8 KB rows (tools/bw_probe.cu), direct
+// 128-bit loads with many rows in flight reach ~7.3 TB/s.
+// Numeric contract (D15): bf16 weights, fp32 activations and accumulation.
+#include "common.cuh"
+#include "decode_kernels.cuh"
+
+namespace sirius {
+namespace {
+
+constexpr int kGemvWarps = 8;   // 2 CTAs per SM
+constexpr int kFfnWarps = 16;   // 1 CTA per SM (cooperative)
+constexpr int kFfnMaxN = 256;   // neurons per CTA
+constexpr int kFfnMaxChunks = kFfnMaxN / 32;
+
+// plane layout of an fp32 activation row of K elements: chunk c = 8 consecutive elements,
+// plane p = 0 holds elements 8c..8c+3, plane 1 holds 8c+4..8c+7 (float4 per chunk per plane)
+SIRIUS_DEV int plane_index(int b, int k, int CH) {
+  const int c = k >> 3, e = k & 7;
+  return ((b * 2 + (e >> 2)) * CH + c) * 4 + (e & 3);
+}
+
+// Prologue: activation rows h[b, :] (plane layout) in shared memory; all NT threads participate.
+template <int B>
+SIRIUS_DEV void prologue(const Prologue& p, int K, float* h_s, float* red_s, bool store_res) {
+  const int tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarp = NT >> 5;
+  const int CH = K / 8;
+  for (int b = 0; b < B; ++b) {
+    if (p.mode == IN_F32) {
+      for (int k = tid; k < K; k += NT) h_s[plane_index(b, k, CH)] = p.in_f32[(size_t)b * K + k];
+      continue;
+    }
+    const float* base = p.mode == IN_RESID ? p.base + (size_t)b * K : nullptr;
+    const float* delta = (p.mode == IN_RESID && p.delta) ? p.delta + (size_t)b * K : nullptr;
+    const uint16_t* erow = nullptr;
+    if (p.mode == IN_EMBED) {
+      int tok = p.tokens[b];
+      tok = tok < 0 ? 0 : (tok >= p.vocab ? p.vocab - 1 : tok);
+      erow = p.embed + (size_t)tok * K;
+    }
+    float ss = 0.f;
+    for (int k = tid; k < K; k += NT) {  // x -> h_s (raw), sum of squares (fixed order)
+      float v;
+      if (erow) {
+        v = __uint_as_float((uint32_t)erow[k] << 16);
+      } else {
+        v = base[k];
+        if (delta) v += delta[k];
+      }
+      h_s[plane_index(b, k, CH)] = v;
+      ss = fmaf(v, v, ss);
+      if (store_res && p.res_out) p.res_out[(size_t)b * K + k] = v;
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) red_s[warp] = ss;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < nwarp; ++w) tot += red_s[w];
+    const float r = 1.0f / sqrtf(tot / (float)K + p.eps);
+    for (int k = tid; k < K; k += NT) {
+      const float w = __uint_as_float((uint32_t)p.norm_w[k] << 16);
+      const int i = plane_index(b, k, CH);
+      h_s[i] = (h_s[i] * r) * w;  // this thread wrote h_s[i] above
+    }
+    __syncthreads();  // red_s reuse
+  }
+  __syncthreads();
+}
+
+SIRIUS_DEV float dot8p(const uint4 w, const float4 x0, const float4 x1, float s) {
+  s = fmaf(bf16_lo(w.x), x0.x, s);
+  s = fmaf(bf16_hi(w.x), x0.y, s);
+  s = fmaf(bf16_lo(w.y), x0.z, s);
+  s = fmaf(bf16_hi(w.y), x0.w, s);
+  s = fmaf(bf16_lo(w.z), x1.x, s);
+  s = fmaf(bf16_hi(w.z), x1.y, s);
+  s = fmaf(bf16_lo(w.w), x1.z, s);
+  s = fmaf(bf16_hi(w.w), x1.w, s);
+  return s;
+}
+
+// Warp-cooperative dot of one bf16 row (global) with the B activation rows (planes in smem).
+// Lane l handles chunks l + 32 j; loads are issued in groups of U before use.  Result: lane sums
+// (not yet reduced across the warp).
+template <int B, int CPL>
+SIRIUS_DEV void row_dot(const uint16_t* __restrict__ wrow, const float4* __restrict__ hp, int CH, int lane,
+                        float* acc) {
+  constexpr int U = CPL < 16 ? CPL : 16;
+#pragma unroll
+  for (int b = 0; b < B; ++b) acc[b] = 0.f;
+#pragma unroll
+  for (int j0 = 0; j0 < CPL; j0 += U) {
+    uint4 wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = lane + 32 * (j0 + u);
+      wv[u] = c < CH ? ld_nc_v4(wrow + (size_t)c * 8) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = lane + 32 * (j0 + u);
+      if (c < CH) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] = dot8p(wv[u], hp[(b * 2) * CH + c], hp[(b * 2 + 1) * CH + c], acc[b]);
+      }
+    }
+  }
+}
+
+// ===================================================================== dense GEMV
+template <int B, int CPL>
+__global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
+  extern __shared__ __align__(16) float h_s[];  // [B][2][CH] float4
+  __shared__ float red_s[32];
+  __shared__ unsigned long long key_s[kGemvWarps * B];
+  __shared__ unsigned flag_s;
+  const int K = a.K, CH = K / 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  prologue<B>(a.pro, K, h_s, red_s, blockIdx.x == 0);
+  const float4* hp = reinterpret_cast<const float4*>(h_s);
+  const int r0 = (int)((long long)a.rows * blockIdx.x / gridDim.x);
+  const int r1 = (int)((long long)a.rows * (blockIdx.x + 1) / gridDim.x);
+  unsigned long long best[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) best[b] = 0ull;
+  for (int row = r0 + warp; row < r1; row += kGemvWarps) {
+    float acc[B];
+    row_dot<B, CPL>(a.W + (size_t)row * K, hp, CH, lane, acc);
+#pragma unroll
+    for (int b = 0; b < B; ++b) acc[b] = warp_sum(acc[b]);
+    if (lane == 0) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (a.out) a.out[(size_t)b * a.ldo + row] = acc[b];
+        if (a.epi == EPI_ARGMAX) {
+          const unsigned long long k = argmax_key(acc[b], a.index_offset + (uint32_t)row);
+          best[b] = k > best[b] ? k : best[b];
+        }
+      }
+    }
+  }
+  if (a.epi != EPI_ARGMAX) return;
+  if (lane == 0)
+    for (int b = 0; b < B; ++b) key_s[warp * B + b] = best[b];
+  __syncthreads();
+  if (tid < B) {
+    unsigned long long k = 0ull;
+    for (int w = 0; w < kGemvWarps; ++w) k = key_s[w * B + tid] > k ? key_s[w * B + tid] : k;
+    atomicMax(a.amax + tid, k);
+  }
+  if (a.finalize) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(a.done_counter, 1u);
+      const bool last = old == gridDim.x - 1;
+      if (last) {
+        atomicExch(a.done_counter, 0u);
+        __threadfence();
+      }
+      flag_s = last ? 1u : 0u;
+    }
+    __syncthreads();
+    if (flag_s && tid < B) {
+      const unsigned long long k = atomicExch(a.amax + tid, 0ull);  // read + reset for the next step
+      a.token_out[tid] = (int32_t)argmax_key_index(k);
+    }
+  }
+}
+
+// ===================================================================== fused CATS FFN
+template <int B, int CPL, int CPT>
+__global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
+  extern __shared__ __align__(16) float h_s[];  // [B][2][CH] float4
+  __shared__ float red_s[32];
+  __shared__ float a_s[B][kFfnMaxN];            // a = SiLU(g) of the CTA's neurons
+  __shared__ float m_s[B][kFfnMaxN];            // m = a * u, in active-list order
+  __shared__ int list_s[kFfnMaxN];              // active neurons (local index), ascending
+  __shared__ unsigned char bits_s[kFfnMaxN];    // per active neuron: which batch rows are active
+  __shared__ unsigned act_s[kFfnMaxChunks][B];
+  __shared__ int cnt_s[kFfnMaxChunks], off_s[kFfnMaxChunks + 1];
+  constexpr int NT = kFfnWarps * 32;
+  const int d = a.d, CH = d / 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int n0 = (int)((long long)a.F * cta / G), n1 = (int)((long long)a.F * (cta + 1) / G), nn = n1 - n0;
+  const int nch = (nn + 31) / 32;
+
+  prologue<B>(a.pro, d, h_s, red_s, cta == 0);
+  const float4* hp = reinterpret_cast<const float4*>(h_s);
+  const float t = a.dense ? 0.f : *a.threshold;
+
+  // ---- A: dense gate rows: g = h2 . W_gate[n];  a = SiLU(g)
+  for (int i = warp; i < nn; i += kFfnWarps) {
+    float acc[B];
+    row_dot<B, CPL>(a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const float g = warp_sum(acc[b]);
+      if (lane == 0) a_s[b][i] = g / (1.0f + expf(-g));
+    }
+  }
+  __syncthreads();
+  // ---- B: CATS threshold |a| >= t and warp-ballot compaction (warp c <-> 32-neuron chunk c)
+  unsigned um = 0u;
+  if (warp < nch) {
+    const int i = warp * 32 + lane;
+    const bool valid = i < nn;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const float av = valid ? a_s[b][i] : 0.f;
+      const bool on = valid && (a.dense || fabsf(av) >= t);
+      const unsigned mb = __ballot_sync(0xffffffffu, on);
+      um |= mb;
+      if (lane == 0) act_s[warp][b] = mb;
+      if (a.gate_out && valid) a.gate_out[(size_t)b * a.gate_stride + n0 + i] = av;
+    }
+    if (lane == 0) cnt_s[warp] = __popc(um);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int s = 0;
+    for (int c = 0; c < nch; ++c) {
+      off_s[c] = s;
+      s += cnt_s[c];
+    }
+    off_s[nch] = s;
+  }
+  __syncthreads();
+  if (warp < nch && ((um >> lane) & 1u)) {
+    const int k = off_s[warp] + __popc(um & ((1u << lane) - 1u));
+    list_s[k] = warp * 32 + lane;
+    unsigned char bits = 0;
+#pragma unroll
+    for (int b = 0; b < B; ++b) bits |= (unsigned char)(((act_s[warp][b] >> lane) & 1u) << b);
+    bits_s[k] = bits;
+  }
+  __syncthreads();
+  const int nact = off_s[nch];
+  // ---- C: active up rows only: u = h2 . W_up[n];  m = a * u  (inactive (b, n) pairs contribute 0)
+  for (int k = warp; k < nact; k += kFfnWarps) {
+    const int i = list_s[k];
+    float acc[B];
+    row_dot<B, CPL>(a.w_up + (size_t)(n0 + i) * d, hp, CH, lane, acc);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const float u = warp_sum(acc[b]);
+      if (lane == 0) m_s[b][k] = ((bits_s[k] >> b) & 1u) ? a_s[b][i] * u : 0.f;
+    }
+  }
+  __syncthreads();
+  // ---- D: active down rows only: y += m * W_down[n]; thread owns column chunks tid + NT j
+  constexpr int RU = CPT == 1 ? 16 : (CPT == 2 ? 8 : 4);  // rows in flight per thread
+  float y[B][CPT * 8];
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int e = 0; e < CPT * 8; ++e) y[b][e] = 0.f;
+  for (int k0 = 0; k0 < nact; k0 += RU) {
+    uint4 wv[RU][CPT];
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      const int k = k0 + r;
+      const uint16_t* wrow = a.w_down + (size_t)(n0 + (k < nact ? list_s[k] : 0)) * d;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int ch = tid + NT * j;
+        wv[r][j] = (k < nact && ch < CH) ? ld_nc_v4(wrow + (size_t)ch * 8) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      const int k = k0 + r;
+      if (k < nact) {  // ascending neuron order, same for every column
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+          const uint4 w = wv[r][j];
+          const float wf[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
+                               bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const float mk = m_s[b][k];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) y[b][j * 8 + e] = fmaf(mk, wf[e], y[b][j * 8 + e]);
+          }
+        }
+      }
+    }
+  }
+  // ---- per-CTA partials -> grid barrier -> deterministic column reduction
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int ch = tid + NT * j;
+    if (ch < CH) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float4* dst = reinterpret_cast<float4*>(a.part + ((size_t)cta * B + b) * d + ch * 8);
+        dst[0] = make_float4(y[b][j * 8 + 0], y[b][j * 8 + 1], y[b][j * 8 + 2], y[b][j * 8 + 3]);
+        dst[1] = make_float4(y[b][j * 8 + 4], y[b][j * 8 + 5], y[b][j * 8 + 6], y[b][j * 8 + 7]);
+      }
+    }
+  }
+  if (tid < B) {
+    int cnt = 0;
+    for (int c = 0; c < nch; ++c) cnt += __popc(act_s[c][tid]);
+    a.part_cnt[cta * B + tid] = cnt;
+  }
+  grid_barrier(a.barrier, G);
+  const int units = B * d / 4;  // float4 columns
+  const int u0 = (int)((long long)units * cta / G), u1 = (int)((long long)units * (cta + 1) / G);
+  for (int u = u0 + warp; u < u1; u += kFfnWarps) {
+    const int b = u / (d / 4), c4 = u % (d / 4);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = lane; p < G; p += 32) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part + ((size_t)p * B + b) * d) + c4);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    s.x = warp_sum(s.x); s.y = warp_sum(s.y); s.z = warp_sum(s.z); s.w = warp_sum(s.w);
+    if (lane == 0) reinterpret_cast<float4*>(a.out + (size_t)b * d)[c4] = s;
+  }
+  if (cta == 0 && a.n_active_out && tid < B) {
+    int tot = 0;
+    for (int p = 0; p < G; ++p) tot += __ldcg(a.part_cnt + p * B + tid);
+    atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, tot);
+  }
+}
+
+}  // namespace
+
+// ===================================================================== host-side launchers
+namespace launch {
+
+template <int B, int CPL>
+static cudaError_t gemv_bc(const GemvArgs& a, int grid, cudaStream_t st) {
+  auto kern = gemv_kernel<B, CPL>;
+  const size_t smem = (size_t)B * a.K * 4;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kGemvWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int B>
+static cudaError_t gemv_b(const GemvArgs& a, int grid, cudaStream_t st) {
+  const int cpl = (a.K / 8 + 31) / 32;
+  if (cpl <= 1) return gemv_bc<B, 1>(a, grid, st);
+  if (cpl <= 2) return gemv_bc<B, 2>(a, grid, st);
+  if (cpl <= 4) return gemv_bc<B, 4>(a, grid, st);
+  if (cpl <= 8) return gemv_bc<B, 8>(a, grid, st);
+  if (cpl <= 16) return gemv_bc<B, 16>(a, grid, st);
+  if (cpl <= 32) return gemv_bc<B, 32>(a, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+int gemv_grid(int rows, int num_sms) {
+  const int g = 2 * num_sms;
+  return rows < g ? rows : g;
+}
+
+cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st) {
+  if (a.K % 8) return cudaErrorInvalidValue;
+  switch (B) {
+    case 1: return gemv_b<1>(a, grid, st);
+    case 2: return gemv_b<2>(a, grid, st);
+    case 4: return gemv_b<4>(a, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int ffn_grid(int F, int num_sms) {
+  int g = (F + 7) / 8;
+  if (g > num_sms) g = num_sms;
+  if ((F + g - 1) / g > kFfnMaxN) return -1;
+  return g;
+}
+
+template <int B, int CPL, int CPT>
+static cudaError_t ffn_bc(const FfnArgs& a, int grid, cudaStream_t st) {
+  auto kern = ffn_kernel<B, CPL, CPT>;
+  const size_t smem = (size_t)B * a.d * 4;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFfnWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int B>
+static cudaError_t ffn_b(const FfnArgs& a, int grid, cudaStream_t st) {
+  const int CH = a.d / 8;
+  const int cpl = (CH + 31) / 32, cpt = (CH + kFfnWarps * 32 - 1) / (kFfnWarps * 32);
+  if (cpl <= 1) return ffn_bc<B, 1, 1>(a, grid, st);
+  if (cpl <= 2) return ffn_bc<B, 2, 1>(a, grid, st);
+  if (cpl <= 4) return ffn_bc<B, 4, 1>(a, grid, st);
+  if (cpl <= 8) return ffn_bc<B, 8, 1>(a, grid, st);
+  if (cpl <= 16) return ffn_bc<B, 16, 1>(a, grid, st);  // d = 4096
+  if (cpl <= 32 && cpt <= 2) return ffn_bc<B, 32, 2>(a, grid, st);  // d = 8192
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st) {
+  if (a.d % 8) return cudaErrorInvalidValue;
+  switch (B) {
+    case 1: return ffn_b<1>(a, grid, st);
+    case 2: return ffn_b<2>(a, grid, st);
+    case 4: return ffn_b<4>(a, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace launch
+}  // namespace sirius

@@ -19,12 +19,12 @@
 
 namespace sirius {
 namespace launch {
-int gemv_nslot(int B, int K, size_t smem_budget);
-cudaError_t gemv(const GemvArgs& a, int B, int grid, int nslot, cudaStream_t st);
+int gemv_grid(int rows, int num_sms);
+cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st);
 cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st);
-int ffn_nslot(int B, int d, size_t smem_budget);
 int ffn_grid(int F, int num_sms);
-cudaError_t ffn(const FfnArgs& a, int B, int grid, int nslot, cudaStream_t st);
+int attn_splits(int B, int KVr, int num_sms);
+cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st);
 cudaError_t attn_decode(const AttnArgs& a, int B, int hd, int group, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius
@@ -128,6 +128,15 @@ struct sirius_ctx {
   };
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
+  // CUDA graphs: every ABI call is captured once per distinct argument set and replayed
+  bool use_graphs = true;
+  cudaStream_t cap_stream = nullptr;
+  struct GraphEntry {
+    std::vector<uintptr_t> key;
+    cudaGraphExec_t exec;
+    unsigned long long kernels;
+  };
+  std::vector<GraphEntry> graphs;
   std::vector<void*> allocations;
   std::string last_error = "ok";
 };
@@ -205,6 +214,51 @@ sirius_status check_sticky(sirius_ctx* c) {
   return SIRIUS_OK;
 }
 
+typedef std::vector<uintptr_t> GraphKey;
+
+// Capture `enqueue` (which only enqueues work on c->stream) into a CUDA graph the first time a key
+// is seen, then replay the instantiated graph: one launch per ABI call instead of ~130 kernels.
+// Bypassed while per-kernel profiling is on.
+template <class F>
+sirius_status run_graphed(sirius_ctx* c, const GraphKey& key, F enqueue) {
+  if (!c->use_graphs || c->prof_on) return enqueue();
+  for (auto& g : c->graphs)
+    if (g.key == key) {
+      c->launches += g.kernels;
+      CU(cudaGraphLaunch(g.exec, c->stream));
+      return SIRIUS_OK;
+    }
+  // capture on a private stream (the caller's stream may be the legacy default stream, which cannot
+  // be captured); the instantiated graph is then launched on the caller's stream
+  if (!c->cap_stream) CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  const unsigned long long before = c->launches;
+  cudaStream_t user = c->stream;
+  CU(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+  c->stream = c->cap_stream;
+  sirius_status s = enqueue();
+  c->stream = user;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (s == SIRIUS_OK && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (s != SIRIUS_OK || e != cudaSuccess || !exec) {
+    // not capturable on this driver / configuration: fall back to direct launches for good
+    cudaGetLastError();
+    c->use_graphs = false;
+    c->sticky = SIRIUS_OK;
+    c->launches = before;
+    return enqueue();
+  }
+  if (c->graphs.size() >= 256) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  c->graphs.push_back({key, exec, c->launches - before});
+  CU(cudaGraphLaunch(exec, c->stream));
+  return SIRIUS_OK;
+}
+
 // enqueue a copy of the device error word into the pinned host mirror (read by the next call)
 void mirror_err(sirius_ctx* c) { cudaMemcpyAsync(c->err_host, c->err_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream); }
 
@@ -223,10 +277,7 @@ sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev,
 
 // ---- one GEMV (decode) launch
 sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
-  const int grid = a.rows < c->num_sms ? a.rows : c->num_sms;
-  const int nslot = launch::gemv_nslot(B, a.K, c->smem_optin);
-  if (nslot < 2) return fail(c, SIRIUS_ERR_UNSUPPORTED, "gemv: row too large for shared memory");
-  LCU(launch::gemv(a, B, grid, nslot, c->stream));
+  LCU(launch::gemv(a, B, launch::gemv_grid(a.rows, c->num_sms), c->stream));
   return SIRIUS_OK;
 }
 
@@ -398,11 +449,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     delete c;
     return s;
   }
-  {
-    int total = cf.batch * c->KVr;
-    int s = (2 * c->num_sms + total - 1) / total;
-    c->attn_splits = s < 1 ? 1 : (s > 64 ? 64 : s);
-  }
+  c->attn_splits = launch::attn_splits(cf.batch, c->KVr, c->num_sms);  // ~one wave of split CTAs
   auto cleanup_fail = [&](sirius_status s) {
     sirius_destroy(c);
     return s;
@@ -527,6 +574,8 @@ sirius_status sirius_destroy(sirius_ctx* c) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocations) cudaFree(p);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->pre_start_host) cudaFreeHost(c->pre_start_host);
@@ -591,18 +640,14 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
   return SIRIUS_OK;
 }
 
-sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
-                                 int32_t* token_out, float* logits_out, int32_t* n_active_out, float* gate_act_out) {
-  if (!c || !token_in || !pos || !token_out) return SIRIUS_ERR_INVALID_ARG;
-  if (flags & ~(uint32_t)SIRIUS_DENSE) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
-  OK(check_sticky(c));
+static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
+                                    int32_t* token_out, float* logits_out, int32_t* n_active_out,
+                                    float* gate_act_out) {
   const sirius_config& cf = c->cfg;
   const int B = cf.batch, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   const bool dense = flags & SIRIUS_DENSE;
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
   const int ffn_grid = launch::ffn_grid(c->Fr, c->num_sms);
-  const int ffn_nslot = launch::ffn_nslot(B, d, c->smem_optin);
-  if (ffn_nslot < 2) return fail(c, SIRIUS_ERR_UNSUPPORTED, "ffn: row too large for shared memory");
   for (int l = 0; l < L; ++l) {
     for (auto& R : c->ranks) {
       GemvArgs a = {};
@@ -688,7 +733,7 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
         f.gate_stride = (long long)L * F;
       }
       prof_begin(c, P_FFN);
-      LCU(launch::ffn(f, B, ffn_grid, ffn_nslot, c->stream));
+      LCU(launch::ffn(f, B, ffn_grid, c->stream));
       prof_end(c);
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
@@ -727,16 +772,22 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
   return SIRIUS_OK;
 }
 
-sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const int32_t* start_pos, int32_t gamma,
-                             float accept_threshold, int32_t accept_mode, int32_t* n_accept_out,
-                             int32_t* next_token_out, float* q_out, float* logits_out) {
-  if (!c || !kernel_tokens || !start_pos || !n_accept_out || !next_token_out) return SIRIUS_ERR_INVALID_ARG;
-  if (accept_mode != SIRIUS_ACCEPT_THRESHOLD && accept_mode != SIRIUS_ACCEPT_EXACT_ARGMAX)
-    return fail(c, SIRIUS_ERR_INVALID_ARG, "accept_mode");
-  if (!(accept_threshold >= 0.f && accept_threshold <= 1.f)) return fail(c, SIRIUS_ERR_INVALID_ARG, "r outside [0,1]");
-  if (gamma < 1) return fail(c, SIRIUS_ERR_INVALID_ARG, "gamma < 1");
-  if (gamma > c->cfg.max_gamma) return fail(c, SIRIUS_ERR_CAPACITY, "gamma > max_gamma");
+sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
+                                 int32_t* token_out, float* logits_out, int32_t* n_active_out, float* gate_act_out) {
+  if (!c || !token_in || !pos || !token_out) return SIRIUS_ERR_INVALID_ARG;
+  if (flags & ~(uint32_t)SIRIUS_DENSE) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
   OK(check_sticky(c));
+  GraphKey key = {0xDEC0u, flags, (uintptr_t)token_in, (uintptr_t)pos, (uintptr_t)token_out, (uintptr_t)logits_out,
+                  (uintptr_t)n_active_out, (uintptr_t)gate_act_out};
+  return run_graphed(c, key, [&] {
+    return enqueue_decode(c, token_in, pos, flags, token_out, logits_out, n_active_out, gate_act_out);
+  });
+}
+
+static sirius_status enqueue_correct(sirius_ctx* c, const int32_t* kernel_tokens, const int32_t* start_pos,
+                                     int32_t gamma, float accept_threshold, int32_t accept_mode,
+                                     int32_t* n_accept_out, int32_t* next_token_out, float* q_out,
+                                     float* logits_out) {
   const sirius_config& cf = c->cfg;
   const int B = cf.batch, d = cf.d_model, M = B * gamma;
   prof_begin(c, P_VERIFY);
@@ -793,15 +844,34 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
   prof_end(c);
   mirror_err(c);
   CU(cudaGetLastError());
+  return SIRIUS_OK;
+}
+
+sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const int32_t* start_pos, int32_t gamma,
+                             float accept_threshold, int32_t accept_mode, int32_t* n_accept_out,
+                             int32_t* next_token_out, float* q_out, float* logits_out) {
+  if (!c || !kernel_tokens || !start_pos || !n_accept_out || !next_token_out) return SIRIUS_ERR_INVALID_ARG;
+  if (accept_mode != SIRIUS_ACCEPT_THRESHOLD && accept_mode != SIRIUS_ACCEPT_EXACT_ARGMAX)
+    return fail(c, SIRIUS_ERR_INVALID_ARG, "accept_mode");
+  if (!(accept_threshold >= 0.f && accept_threshold <= 1.f)) return fail(c, SIRIUS_ERR_INVALID_ARG, "r outside [0,1]");
+  if (gamma < 1) return fail(c, SIRIUS_ERR_INVALID_ARG, "gamma < 1");
+  if (gamma > c->cfg.max_gamma) return fail(c, SIRIUS_ERR_CAPACITY, "gamma > max_gamma");
+  OK(check_sticky(c));
+  uint32_t rbits;
+  memcpy(&rbits, &accept_threshold, 4);
+  GraphKey key = {0xC0EEu, (uintptr_t)gamma, (uintptr_t)rbits, (uintptr_t)accept_mode, (uintptr_t)kernel_tokens,
+                  (uintptr_t)start_pos, (uintptr_t)n_accept_out, (uintptr_t)next_token_out, (uintptr_t)q_out,
+                  (uintptr_t)logits_out};
+  OK(run_graphed(c, key, [&] {
+    return enqueue_correct(c, kernel_tokens, start_pos, gamma, accept_threshold, accept_mode, n_accept_out,
+                           next_token_out, q_out, logits_out);
+  }));
   c->last_gamma = gamma;
   c->have_correct = true;
   return SIRIUS_OK;
 }
 
-sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t* n_rows) {
-  if (!c || !start_pos || !n_rows) return SIRIUS_ERR_INVALID_ARG;
-  if (!c->have_correct) return fail(c, SIRIUS_ERR_STATE, "kv_rewrite without a preceding correct_kernel");
-  OK(check_sticky(c));
+static sirius_status enqueue_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t* n_rows) {
   const sirius_config& cf = c->cfg;
   for (auto& R : c->ranks) {
     KvRewriteArgs a = {};
@@ -824,6 +894,15 @@ sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t*
   }
   mirror_err(c);
   CU(cudaGetLastError());
+  return SIRIUS_OK;
+}
+
+sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t* n_rows) {
+  if (!c || !start_pos || !n_rows) return SIRIUS_ERR_INVALID_ARG;
+  if (!c->have_correct) return fail(c, SIRIUS_ERR_STATE, "kv_rewrite without a preceding correct_kernel");
+  OK(check_sticky(c));
+  GraphKey key = {0xE11Eu, (uintptr_t)start_pos, (uintptr_t)n_rows, (uintptr_t)c->last_gamma};
+  OK(run_graphed(c, key, [&] { return enqueue_rewrite(c, start_pos, n_rows); }));
   c->have_correct = false;
   return SIRIUS_OK;
 }
@@ -850,6 +929,13 @@ int sirius_nccl_comm_destroy(void* comm) {
 
 // ---------------------------------------------------------------- bench / test instrumentation
 unsigned long long sirius_debug_launches(const sirius_ctx* c) { return c ? c->launches : 0ull; }
+// CUDA-graph replay of the ABI calls on (default) / off (every kernel launched from the host).
+// on = -1: query only.  Returns the (new) state: 1 = graphs in use.
+int sirius_debug_graphs(sirius_ctx* c, int on) {
+  if (!c) return -1;
+  if (on >= 0) c->use_graphs = on != 0;
+  return c->use_graphs ? 1 : 0;
+}
 // enable/disable per-kernel event timing (resets the accumulated records)
 int sirius_debug_profile(sirius_ctx* c, int on) {
   if (!c) return -1;

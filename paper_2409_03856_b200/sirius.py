@@ -81,6 +81,8 @@ def load():
         lib.sirius_debug_buffer.restype = I
         lib.sirius_debug_launches.argtypes = [P]
         lib.sirius_debug_launches.restype = ctypes.c_ulonglong
+        lib.sirius_debug_graphs.argtypes = [P, I]
+        lib.sirius_debug_graphs.restype = I
         lib.sirius_debug_profile.argtypes = [P, I]
         lib.sirius_debug_profile.restype = I
         lib.sirius_debug_profile_read.argtypes = [P, P, P]
@@ -172,6 +174,10 @@ class Sirius:
     def launches(self) -> int:
         """Kernels this context has launched so far (library-side counter)."""
         return int(self.lib.sirius_debug_launches(self.h))
+
+    def graphs(self, on: Optional[bool] = None) -> bool:
+        """CUDA-graph replay of the ABI calls (default on); None = query."""
+        return bool(self.lib.sirius_debug_graphs(self.h, -1 if on is None else (1 if on else 0)))
 
     def profile(self, on: bool) -> None:
         self.lib.sirius_debug_profile(self.h, 1 if on else 0)

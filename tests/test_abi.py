@@ -48,11 +48,11 @@ def test_binding_names_match_header():
 
 def test_sass_is_sm100a_with_tcgen05_and_bulk_copies():
     """Evidence the product path is Blackwell-native: tcgen05 MMA (UTCHMMA), TMEM loads (LDTM),
-    TMA tensor loads (UTMALDG) and bulk copies (UBLKCP) in the built library's SASS."""
+    TMA tensor loads (UTMALDG) and TMEM allocation (UTCATOMSWS) in the built library SASS."""
     if not os.path.exists(LIB):
         pytest.skip("library not built")
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", LIB], capture_output=True, text=True).stdout or \
         "arch = sm_100a" in sass
-    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UBLKCP"):
+    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UTCATOMSWS"):
         assert mnem in sass, mnem
