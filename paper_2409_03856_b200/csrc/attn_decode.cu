@@ -97,12 +97,23 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
     const int nb = min(KB, k1 - p0);
     // stage K (padded rows) and V for keys [p0, p0 + nb): 16-byte loads, all issued before use
     constexpr int VPR = HD / 8;  // uint4 per row
-    for (int idx = tid; idx < nb * VPR; idx += 128) {
-      const int kk = idx / VPR, e = idx % VPR;
-      const uint4 kv = *reinterpret_cast<const uint4*>(kc + (size_t)(p0 + kk) * HD + e * 8);
-      const uint4 vv = *reinterpret_cast<const uint4*>(vc + (size_t)(p0 + kk) * HD + e * 8);
-      *reinterpret_cast<uint4*>(k_s + kk * ROWB + e * 16) = kv;
-      *reinterpret_cast<uint4*>(&v_s[kk][e * 8]) = vv;
+    constexpr int NL = KB * VPR / 128;  // uint4 per thread per operand; all loads issued first
+    uint4 kv[NL], vv[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int idx = tid + 128 * j, kk = idx / VPR, e = idx % VPR;
+      if (kk < nb) {
+        kv[j] = *reinterpret_cast<const uint4*>(kc + (size_t)(p0 + kk) * HD + e * 8);
+        vv[j] = *reinterpret_cast<const uint4*>(vc + (size_t)(p0 + kk) * HD + e * 8);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int idx = tid + 128 * j, kk = idx / VPR, e = idx % VPR;
+      if (kk < nb) {
+        *reinterpret_cast<uint4*>(k_s + kk * ROWB + e * 16) = kv[j];
+        *reinterpret_cast<uint4*>(&v_s[kk][e * 8]) = vv[j];
+      }
     }
     __syncthreads();
     // scores: thread t -> key t % KB, heads (t / KB) * HPT + j

@@ -1,0 +1,270 @@
+// attn_rows.cu — causal multi-row attention of the verification / prefill forward (SURVEY.md §8(a)
+// S8; "the full model takes in the last kernel size of tokens ... in parallel").
+//
+// Query rows of one (sequence, kv head) — R = rows_per_seq x G q-heads, up to 64 per row block —
+// attend causally: row i (position T + i) sees cache[0, T) and the kernel's own rows [0, i] (verify:
+// in the staging area; prefill: already in the cache).  grid (splits, KVr x row_blocks, nseq),
+// 256 threads.  Each CTA walks its key range in 64-key blocks staged in shared memory:
+//   scores   thread -> (key t % 64, 16 rows)        k rows padded: conflict-free, q broadcast
+//   softmax  warp   -> 8 rows, online (running max / sum per row)
+//   P.V      thread -> (dim, 32 rows)              v reads consecutive, p broadcast
+// then writes its partial (M, L, A) per row; the last-arriving split combines and writes the output
+// as a bf16 hi/lo pair (the tensor-core operand of the O-projection).  fp32 throughout (D15).
+#include "common.cuh"
+#include "verify_kernels.cuh"
+
+namespace sirius {
+namespace {
+
+constexpr int kRows = 64, kKB = 64, kThreads = 256;
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads) attn_rows_kernel(AttnRowsArgs a, float scale) {
+  constexpr int KROW = HD + 8;                     // padded bf16 K row (elements)
+  constexpr int RPT = kRows * kKB / kThreads;      // score rows per thread (16)
+  constexpr int RSTEP = kThreads / kKB;            // 4
+  constexpr int DPT = kRows * HD / kThreads;       // P.V outputs per thread (32 for HD=128)
+  constexpr int DSTEP = kThreads / HD;             // row step in P.V (2 for HD=128)
+  extern __shared__ __align__(16) uint8_t smem[];
+  float* q_s = reinterpret_cast<float*>(smem);                                   // [kRows][HD]
+  uint16_t* k_s = reinterpret_cast<uint16_t*>(q_s + kRows * HD);                 // [kKB][KROW]
+  uint16_t* v_s = k_s + kKB * KROW;                                              // [kKB][HD]
+  float* p_s = reinterpret_cast<float*>(v_s + kKB * HD);                         // [kRows][kKB + 1]
+  float* m_s = p_s + kRows * (kKB + 1);                                          // [kRows]
+  float* l_s = m_s + kRows;
+  float* c_s = l_s + kRows;
+  __shared__ unsigned flag_last;
+
+  const int split = blockIdx.x, bz = blockIdx.z, b = a.b_base + bz;
+  const int kvh = blockIdx.y % a.KVr, rb = blockIdx.y / a.KVr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = a.G, rows = a.rows_per_seq;
+  const int T = a.start[b];
+  const int r_base = rb * kRows;                                  // row index r = i * G + g
+  const int nr = min(kRows, rows * G - r_base);                   // valid rows in this block
+  const int i_last = (r_base + nr - 1) / G;
+  const int nkeys = max(0, T + i_last + 1);
+  const int S = gridDim.x;
+  const int chunk = (nkeys + S - 1) / S;
+  const int k0 = min(nkeys, split * chunk), k1 = min(nkeys, k0 + chunk);
+  const size_t hb = (size_t)b * a.KVr + kvh;
+  const uint16_t* kc = a.k_cache + hb * a.max_seq * HD;
+  const uint16_t* vc = a.v_cache + hb * a.max_seq * HD;
+  const uint16_t* kf = a.fresh_in_cache ? kc + (size_t)T * HD : a.k_fresh + hb * a.fresh_stride * HD;
+  const uint16_t* vf = a.fresh_in_cache ? vc + (size_t)T * HD : a.v_fresh + hb * a.fresh_stride * HD;
+
+  // q rows (fp32, post-RoPE), score scale folded in
+  {
+    constexpr int NQ = kRows * HD / 4 / kThreads;  // float4 per thread, all loads issued first
+    float4 qv[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int idx = tid + kThreads * j, r = idx / (HD / 4), e4 = idx % (HD / 4);
+      qv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nr) {
+        const int rr = r_base + r, i = rr / G, g = rr % G;
+        qv[j] = __ldcg(reinterpret_cast<const float4*>(a.q + (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD) + e4);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int idx = tid + kThreads * j;
+      reinterpret_cast<float4*>(q_s)[idx] = make_float4(qv[j].x * scale, qv[j].y * scale, qv[j].z * scale, qv[j].w * scale);
+    }
+  }
+  if (tid < kRows) {
+    m_s[tid] = -INFINITY;
+    l_s[tid] = 0.f;
+  }
+  float acc[DPT];
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) acc[j] = 0.f;
+  const int od = tid % HD, orow0 = tid / HD;
+
+  for (int p0 = k0; p0 < k1; p0 += kKB) {
+    const int nb = min(kKB, k1 - p0);
+    __syncthreads();  // previous block's smem consumers done (and q_s / m_s init visible)
+    constexpr int VPR = HD / 8;
+    constexpr int NL = kKB * VPR / kThreads;  // uint4 per thread per operand; all loads issued first
+    uint4 kv[NL], vv[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int idx = tid + kThreads * j, kk = idx / VPR, e = idx % VPR, p = p0 + kk;
+      if (kk < nb) {
+        const uint16_t* ks = p < T ? kc + (size_t)p * HD : kf + (size_t)(p - T) * HD;
+        const uint16_t* vs = p < T ? vc + (size_t)p * HD : vf + (size_t)(p - T) * HD;
+        kv[j] = *reinterpret_cast<const uint4*>(ks + e * 8);
+        vv[j] = *reinterpret_cast<const uint4*>(vs + e * 8);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int idx = tid + kThreads * j, kk = idx / VPR, e = idx % VPR;
+      if (kk < nb) {
+        *reinterpret_cast<uint4*>(k_s + kk * KROW + e * 8) = kv[j];
+        *reinterpret_cast<uint4*>(v_s + kk * HD + e * 8) = vv[j];
+      }
+    }
+    __syncthreads();
+    // ---- scores s[r][kk] = q_r . k_kk  (masked: key p visible to row i iff p <= T + i)
+    {
+      const int kk = tid % kKB, r0 = tid / kKB;
+      float s[RPT];
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) s[j] = 0.f;
+      if (kk < nb) {
+        const uint16_t* kr = k_s + kk * KROW;
+#pragma unroll 2
+        for (int e = 0; e < HD / 8; ++e) {
+          const uint4 w = *reinterpret_cast<const uint4*>(kr + e * 8);
+          const float kf8[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
+                                bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            const float4 qa = *reinterpret_cast<const float4*>(q_s + (r0 + RSTEP * j) * HD + e * 8);
+            const float4 qb = *reinterpret_cast<const float4*>(q_s + (r0 + RSTEP * j) * HD + e * 8 + 4);
+            float t = s[j];
+            t = fmaf(kf8[0], qa.x, t); t = fmaf(kf8[1], qa.y, t); t = fmaf(kf8[2], qa.z, t); t = fmaf(kf8[3], qa.w, t);
+            t = fmaf(kf8[4], qb.x, t); t = fmaf(kf8[5], qb.y, t); t = fmaf(kf8[6], qb.z, t); t = fmaf(kf8[7], qb.w, t);
+            s[j] = t;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int r = r0 + RSTEP * j;
+        const int i = (r_base + r) / G;
+        const bool vis = kk < nb && r < nr && p0 + kk <= T + i;
+        p_s[r * (kKB + 1) + kk] = vis ? s[j] : -INFINITY;
+      }
+    }
+    __syncthreads();
+    // ---- online softmax per row: warp w -> rows 8w .. 8w+7
+    for (int r = warp * (kRows / 8); r < (warp + 1) * (kRows / 8); ++r) {
+      float* pr = p_s + r * (kKB + 1);
+      const float x0 = pr[lane], x1 = pr[lane + 32];
+      const float bm = warp_max(fmaxf(x0, x1));
+      const float mold = m_s[r];
+      const float mn = fmaxf(mold, bm);
+      const float e0 = mn == -INFINITY ? 0.f : expf(x0 - mn);
+      const float e1 = mn == -INFINITY ? 0.f : expf(x1 - mn);
+      pr[lane] = e0;
+      pr[lane + 32] = e1;
+      const float bs = warp_sum(e0 + e1);
+      if (lane == 0) {
+        const float corr = mold == -INFINITY ? 0.f : expf(mold - mn);
+        c_s[r] = corr;
+        l_s[r] = l_s[r] * corr + bs;
+        m_s[r] = mn;
+      }
+    }
+    __syncthreads();
+    // ---- P.V: thread -> (dim od, rows orow0 + DSTEP j)
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) acc[j] *= c_s[orow0 + DSTEP * j];
+    for (int kk = 0; kk < nb; ++kk) {
+      const float v = __uint_as_float((uint32_t)v_s[kk * HD + od] << 16);
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) acc[j] = fmaf(p_s[(orow0 + DSTEP * j) * (kKB + 1) + kk], v, acc[j]);
+    }
+  }
+  __syncthreads();
+  // ---- partial (M, L, A) of this split
+  const int RB = gridDim.y / a.KVr;
+  float* part = a.part + ((((size_t)bz * a.KVr + kvh) * RB + rb) * S + split) * kRows * (HD + 2);
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int r = orow0 + DSTEP * j;
+    part[r * (HD + 2) + 2 + od] = acc[j];
+  }
+  if (tid < kRows) {
+    part[tid * (HD + 2)] = m_s[tid];
+    part[tid * (HD + 2) + 1] = l_s[tid];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    unsigned* cnt = a.counters + ((size_t)bz * a.KVr + kvh) * RB + rb;
+    const unsigned old = atomicAdd(cnt, 1u);
+    const bool last = old == (unsigned)S - 1;
+    if (last) {
+      atomicExch(cnt, 0u);
+      __threadfence();
+    }
+    flag_last = last ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!flag_last) return;
+  // ---- combine the splits (weights per (split, row) first, then independent loads)
+  const float* pb = a.part + (((size_t)bz * a.KVr + kvh) * RB + rb) * S * kRows * (HD + 2);
+  const int s_active = chunk > 0 ? (nkeys + chunk - 1) / chunk : 0;
+  float* w_s = p_s;  // reuse: [S][kRows] weights (S <= kKB + 1)
+  if (tid < kRows) {
+    float M = -INFINITY;
+    for (int sp = 0; sp < s_active; ++sp) M = fmaxf(M, __ldcg(pb + ((size_t)sp * kRows + tid) * (HD + 2)));
+    float L = 0.f;
+    for (int sp = 0; sp < s_active; ++sp) {
+      const float* ps = pb + ((size_t)sp * kRows + tid) * (HD + 2);
+      const float Ms = __ldcg(ps);
+      const float f = (Ms == -INFINITY || M == -INFINITY) ? 0.f : expf(Ms - M);
+      L += __ldcg(ps + 1) * f;
+      w_s[sp * kRows + tid] = f;
+    }
+    l_s[tid] = L;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int j = 0; j < DPT; ++j) {
+    const int r = orow0 + DSTEP * j;
+    if (r >= nr) continue;
+    float o = 0.f;
+    for (int sp = 0; sp < s_active; ++sp)
+      o += __ldcg(pb + ((size_t)sp * kRows + r) * (HD + 2) + 2 + od) * w_s[sp * kRows + r];
+    const float v = l_s[r] > 0.f ? o / l_s[r] : 0.f;
+    const int rr = r_base + r, i = rr / G, g = rr % G;
+    const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + od;
+    const uint16_t hi = f2bf_bits(v);
+    a.out_hi[off] = hi;
+    a.out_lo[off] = f2bf_bits(v - __uint_as_float((uint32_t)hi << 16));
+  }
+}
+
+template <int HD>
+size_t attn_rows_smem() {
+  return (size_t)kRows * HD * 4 + (size_t)kKB * (HD + 8) * 2 + (size_t)kKB * HD * 2 + (size_t)kRows * (kKB + 1) * 4 +
+         3 * kRows * 4;
+}
+
+}  // namespace
+
+namespace launch {
+
+int attn_rows_splits(int nseq, int KVr, int row_blocks, int max_keys, int num_sms) {
+  int s = (num_sms + nseq * KVr * row_blocks - 1) / (nseq * KVr * row_blocks);
+  const int by_keys = (max_keys + kKB - 1) / kKB;  // no more splits than 64-key blocks
+  if (s > by_keys) s = by_keys;
+  if (s > kKB) s = kKB;  // combine weights buffer
+  return s < 1 ? 1 : s;
+}
+
+cudaError_t attn_rows(const AttnRowsArgs& a, int nseq, int hd, int splits, int row_blocks, cudaStream_t st) {
+  dim3 grid(splits, a.KVr * row_blocks, nseq);
+  const float scale = 1.0f / sqrtf((float)hd);
+  if (hd == 128) {
+    const size_t sm = attn_rows_smem<128>();
+    cudaError_t e = cudaFuncSetAttribute(attn_rows_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attn_rows_kernel<128><<<grid, kThreads, sm, st>>>(a, scale);
+  } else if (hd == 64) {
+    const size_t sm = attn_rows_smem<64>();
+    cudaError_t e = cudaFuncSetAttribute(attn_rows_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attn_rows_kernel<64><<<grid, kThreads, sm, st>>>(a, scale);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace launch
+}  // namespace sirius

@@ -31,41 +31,78 @@ constexpr int kFfnMaxChunks = kFfnMaxN / 32;
 
 // plane layout of an fp32 activation row of K elements: chunk c = 8 consecutive elements,
 // plane p = 0 holds elements 8c..8c+3, plane 1 holds 8c+4..8c+7 (float4 per chunk per plane)
-SIRIUS_DEV int plane_index(int b, int k, int CH) {
-  const int c = k >> 3, e = k & 7;
-  return ((b * 2 + (e >> 2)) * CH + c) * 4 + (e & 3);
-}
 
 // Prologue: activation rows h[b, :] (plane layout) in shared memory; all NT threads participate.
+// Thread t owns the 4-element groups g = t + NT j (plane-aligned: a group is one float4 of a plane);
+// all of its global loads are issued before any is used (one memory round trip, not K / NT).
+constexpr int kMaxGroups = 8;  // K <= 32 * NT
 template <int B>
 SIRIUS_DEV void prologue(const Prologue& p, int K, float* h_s, float* red_s, bool store_res) {
   const int tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarp = NT >> 5;
-  const int CH = K / 8;
+  const int CH = K / 8, NG = K / 4;
+  float4* hp = reinterpret_cast<float4*>(h_s);
+  auto slot = [&](int b, int g) { return (b * 2 + (g & 1)) * CH + (g >> 1); };  // group g = elements 4g..4g+3
   for (int b = 0; b < B; ++b) {
+    float4 x[kMaxGroups];
     if (p.mode == IN_F32) {
-      for (int k = tid; k < K; k += NT) h_s[plane_index(b, k, CH)] = p.in_f32[(size_t)b * K + k];
+      const float4* src = reinterpret_cast<const float4*>(p.in_f32 + (size_t)b * K);
+#pragma unroll
+      for (int j = 0; j < kMaxGroups; ++j) {
+        const int g = tid + NT * j;
+        if (g < NG) x[j] = __ldcg(src + g);
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxGroups; ++j) {
+        const int g = tid + NT * j;
+        if (g < NG) hp[slot(b, g)] = x[j];
+      }
       continue;
     }
-    const float* base = p.mode == IN_RESID ? p.base + (size_t)b * K : nullptr;
-    const float* delta = (p.mode == IN_RESID && p.delta) ? p.delta + (size_t)b * K : nullptr;
-    const uint16_t* erow = nullptr;
     if (p.mode == IN_EMBED) {
       int tok = p.tokens[b];
       tok = tok < 0 ? 0 : (tok >= p.vocab ? p.vocab - 1 : tok);
-      erow = p.embed + (size_t)tok * K;
+      const uint2* erow = reinterpret_cast<const uint2*>(p.embed + (size_t)tok * K);
+#pragma unroll
+      for (int j = 0; j < kMaxGroups; ++j) {
+        const int g = tid + NT * j;
+        if (g < NG) {
+          const uint2 e = erow[g];
+          x[j] = make_float4(bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y));
+        }
+      }
+    } else {
+      const float4* base = reinterpret_cast<const float4*>(p.base + (size_t)b * K);
+      const float4* delta = p.delta ? reinterpret_cast<const float4*>(p.delta + (size_t)b * K) : nullptr;
+      float4 dl[kMaxGroups];
+#pragma unroll
+      for (int j = 0; j < kMaxGroups; ++j) {
+        const int g = tid + NT * j;
+        if (g < NG) {
+          x[j] = __ldcg(base + g);
+          dl[j] = delta ? __ldcg(delta + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxGroups; ++j) {
+        x[j].x += dl[j].x; x[j].y += dl[j].y; x[j].z += dl[j].z; x[j].w += dl[j].w;
+      }
     }
     float ss = 0.f;
-    for (int k = tid; k < K; k += NT) {  // x -> h_s (raw), sum of squares (fixed order)
-      float v;
-      if (erow) {
-        v = __uint_as_float((uint32_t)erow[k] << 16);
-      } else {
-        v = base[k];
-        if (delta) v += delta[k];
+#pragma unroll
+    for (int j = 0; j < kMaxGroups; ++j) {  // sum of squares, fixed order
+      const int g = tid + NT * j;
+      if (g < NG) {
+        ss = fmaf(x[j].x, x[j].x, ss); ss = fmaf(x[j].y, x[j].y, ss);
+        ss = fmaf(x[j].z, x[j].z, ss); ss = fmaf(x[j].w, x[j].w, ss);
+        if (store_res && p.res_out) reinterpret_cast<float4*>(p.res_out + (size_t)b * K)[g] = x[j];
       }
-      h_s[plane_index(b, k, CH)] = v;
-      ss = fmaf(v, v, ss);
-      if (store_res && p.res_out) p.res_out[(size_t)b * K + k] = v;
+    }
+    uint2 wn[kMaxGroups];
+    const uint2* nw = reinterpret_cast<const uint2*>(p.norm_w);
+#pragma unroll
+    for (int j = 0; j < kMaxGroups; ++j) {
+      const int g = tid + NT * j;
+      if (g < NG) wn[j] = nw[g];
     }
     ss = warp_sum(ss);
     if (lane == 0) red_s[warp] = ss;
@@ -73,10 +110,12 @@ SIRIUS_DEV void prologue(const Prologue& p, int K, float* h_s, float* red_s, boo
     float tot = 0.f;
     for (int w = 0; w < nwarp; ++w) tot += red_s[w];
     const float r = 1.0f / sqrtf(tot / (float)K + p.eps);
-    for (int k = tid; k < K; k += NT) {
-      const float w = __uint_as_float((uint32_t)p.norm_w[k] << 16);
-      const int i = plane_index(b, k, CH);
-      h_s[i] = (h_s[i] * r) * w;  // this thread wrote h_s[i] above
+#pragma unroll
+    for (int j = 0; j < kMaxGroups; ++j) {
+      const int g = tid + NT * j;
+      if (g < NG)
+        hp[slot(b, g)] = make_float4((x[j].x * r) * bf16_lo(wn[j].x), (x[j].y * r) * bf16_hi(wn[j].x),
+                                     (x[j].z * r) * bf16_lo(wn[j].y), (x[j].w * r) * bf16_hi(wn[j].y));
     }
     __syncthreads();  // red_s reuse
   }

@@ -64,6 +64,7 @@ NcclApi& nccl() {
 }
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int kAttnRowUnits = 1024;  // (sequence, kv head, row block, split) partials of attn_rows
 }  // namespace
 
 // ----------------------------------------------------------------------------- context
@@ -366,8 +367,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       aa.out_hi = R.ob_hi;
       aa.out_lo = R.ob_lo;
       const int row_blocks = (rows_per_seq * c->G + 63) / 64;
-      int splits = (2 * c->num_sms + nseq * c->KVr * row_blocks - 1) / (nseq * c->KVr * row_blocks);
-      splits = splits < 1 ? 1 : (splits > 32 ? 32 : splits);
+      int splits = launch::attn_rows_splits(nseq, c->KVr, row_blocks, cf.max_seq, c->num_sms);
+      while (splits > 1 && nseq * c->KVr * row_blocks * splits > kAttnRowUnits) --splits;  // workspace bound
       LCU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
       OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d));
     }
@@ -519,7 +520,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
         alloc(c, &R.ob_lo, (size_t)M * c->Hr * hd) || alloc(c, &R.mb_hi, (size_t)M * c->Fr) ||
         alloc(c, &R.mb_lo, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * 4 * d) ||
         alloc(c, &R.ffn_cnt, (size_t)c->num_sms * 4) || alloc(c, &R.ffn_barrier, 8) ||
-        alloc(c, &R.attn_part, (size_t)B * c->KVr * 64 * 64 * (hd + 2) + (size_t)c->KVr * row_blocks_max * 32 * 64 * (hd + 2)) ||
+        alloc(c, &R.attn_part, (size_t)kAttnRowUnits * 64 * (hd + 2) + (size_t)B * c->KVr * 64 * 8 * (hd + 2)) ||
         alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) ||
         alloc(c, &R.gemm_part, launch::gemm_workspace_bytes(c->num_sms) / sizeof(float)) ||
         alloc(c, &R.gemm_cnt, (size_t)(c->Vr / 128 + 1024)) || alloc(c, &R.head_cnt, 16))

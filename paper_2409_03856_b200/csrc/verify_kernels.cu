@@ -3,8 +3,6 @@
 //
 //  * norm_rows_kernel      residual add (or embedding gather) + RMSNorm of M token rows -> bf16
 //  * rope_store_kernel     RoPE(q, k) at each row's position, bf16; K/V -> staging (verify) or cache
-//  * attn_rows_kernel      causal multi-row attention: row i of a kernel sees cache[0, T) and the
-//                          kernel's own rows [0, i]; split-K over keys + last-CTA combine
 //  * accept_stats_kernel   per logits row (rank shard, vocab split): max, lowest-index argmax,
 //                          sum of exp, and the draft token's logit
 //  * accept_finalize_kernel  LSE, q_i = softmax(l_i)[d_{i+1}], first rejection j, interleaved token
@@ -18,27 +16,51 @@ namespace sirius {
 
 // ===================================================================== norm rows
 __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
-  const int m = blockIdx.x, tid = threadIdx.x, d = a.d;
+  // thread t owns 4-element groups g = t + 256 j; every global load is issued before use
+  constexpr int MG = 8;  // d <= 8192
+  const int m = blockIdx.x, tid = threadIdx.x, d = a.d, NG = d / 4;
   __shared__ float red[8];
-  const float* base = a.base ? a.base + (size_t)m * d : nullptr;
-  const float* delta = a.delta ? a.delta + (size_t)m * d : nullptr;
-  const uint16_t* erow = nullptr;
+  float4 x[MG];
   if (a.tokens) {
     int tok = a.tokens[m];
     tok = tok < 0 ? 0 : (tok >= a.vocab ? a.vocab - 1 : tok);
-    erow = a.embed + (size_t)tok * d;
+    const uint2* erow = reinterpret_cast<const uint2*>(a.embed + (size_t)tok * d);
+#pragma unroll
+    for (int j = 0; j < MG; ++j) {
+      const int g = tid + 256 * j;
+      if (g < NG) {
+        const uint2 e = erow[g];
+        x[j] = make_float4(bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y));
+      }
+    }
+  } else {
+    const float4* base = reinterpret_cast<const float4*>(a.base + (size_t)m * d);
+    const float4* delta = a.delta ? reinterpret_cast<const float4*>(a.delta + (size_t)m * d) : nullptr;
+    float4 dl[MG];
+#pragma unroll
+    for (int j = 0; j < MG; ++j) {
+      const int g = tid + 256 * j;
+      if (g < NG) {
+        x[j] = __ldcg(base + g);
+        dl[j] = delta ? __ldcg(delta + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MG; ++j) {
+      x[j].x += dl[j].x; x[j].y += dl[j].y; x[j].z += dl[j].z; x[j].w += dl[j].w;
+    }
   }
-  auto xval = [&](int k) -> float {
-    if (erow) return __uint_as_float((uint32_t)erow[k] << 16);
-    float v = base[k];
-    if (delta) v += delta[k];
-    return v;
-  };
+  uint2 wn[MG];
   float ss = 0.f;
-  for (int k = tid; k < d; k += 256) {
-    const float v = xval(k);
-    ss = fmaf(v, v, ss);
-    if (a.res_out) a.res_out[(size_t)m * d + k] = v;
+#pragma unroll
+  for (int j = 0; j < MG; ++j) {
+    const int g = tid + 256 * j;
+    if (g < NG) {
+      wn[j] = reinterpret_cast<const uint2*>(a.norm_w)[g];
+      ss = fmaf(x[j].x, x[j].x, ss); ss = fmaf(x[j].y, x[j].y, ss);
+      ss = fmaf(x[j].z, x[j].z, ss); ss = fmaf(x[j].w, x[j].w, ss);
+      if (a.res_out) reinterpret_cast<float4*>(a.res_out + (size_t)m * d)[g] = x[j];
+    }
   }
   ss = warp_sum(ss);
   if ((tid & 31) == 0) red[tid >> 5] = ss;
@@ -46,12 +68,23 @@ __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
   float tot = 0.f;
   for (int w = 0; w < 8; ++w) tot += red[w];
   const float r = 1.0f / sqrtf(tot / (float)d + a.eps);
-  for (int k = tid; k < d; k += 256) {
-    const float w = __uint_as_float((uint32_t)a.norm_w[k] << 16);
-    const float h = (xval(k) * r) * w;
-    const uint16_t hi = f2bf_bits(h);
-    a.out_hi[(size_t)m * d + k] = hi;
-    a.out_lo[(size_t)m * d + k] = f2bf_bits(h - __uint_as_float((uint32_t)hi << 16));
+#pragma unroll
+  for (int j = 0; j < MG; ++j) {
+    const int g = tid + 256 * j;
+    if (g < NG) {
+      const float h[4] = {(x[j].x * r) * bf16_lo(wn[j].x), (x[j].y * r) * bf16_hi(wn[j].x),
+                          (x[j].z * r) * bf16_lo(wn[j].y), (x[j].w * r) * bf16_hi(wn[j].y)};
+      uint16_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hi[e] = f2bf_bits(h[e]);
+        lo[e] = f2bf_bits(h[e] - __uint_as_float((uint32_t)hi[e] << 16));
+      }
+      reinterpret_cast<uint2*>(a.out_hi + (size_t)m * d)[g] =
+          make_uint2(hi[0] | ((uint32_t)hi[1] << 16), hi[2] | ((uint32_t)hi[3] << 16));
+      reinterpret_cast<uint2*>(a.out_lo + (size_t)m * d)[g] =
+          make_uint2(lo[0] | ((uint32_t)lo[1] << 16), lo[2] | ((uint32_t)lo[3] << 16));
+    }
   }
 }
 
@@ -66,139 +99,63 @@ __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
     return;
   }
   const float* row = a.qkv + (size_t)m * (a.Hr + 2 * a.KVr) * hd;
-  const float* cs = a.rope_cos + (size_t)pos * half;
-  const float* sn = a.rope_sin + (size_t)pos * half;
-  for (int idx = tid; idx < (a.Hr + a.KVr) * half; idx += 128) {
-    const int h = idx / half, e = idx % half;
-    const float x0 = row[h * hd + e], x1 = row[h * hd + e + half], c = cs[e], s = sn[e];
-    const float y0 = x0 * c - x1 * s, y1 = x1 * c + x0 * s;
+  const float4* cs = reinterpret_cast<const float4*>(a.rope_cos + (size_t)pos * half);
+  const float4* sn = reinterpret_cast<const float4*>(a.rope_sin + (size_t)pos * half);
+  // rotate-half pairs (e, e + half) in groups of 4 consecutive e: items = (Hr + KVr) * half / 4
+  constexpr int MI = 8;  // items per thread per round
+  const int q4 = half / 4, items = (a.Hr + a.KVr) * q4;
+  for (int it0 = 0; it0 < items; it0 += 128 * MI) {
+  float4 x0[MI], x1[MI], c4[MI], s4[MI];
+#pragma unroll
+  for (int j = 0; j < MI; ++j) {
+    const int it = it0 + tid + 128 * j;
+    if (it < items) {
+      const int h = it / q4, e4 = it % q4;
+      x0[j] = __ldcg(reinterpret_cast<const float4*>(row + h * hd) + e4);
+      x1[j] = __ldcg(reinterpret_cast<const float4*>(row + h * hd + half) + e4);
+      c4[j] = cs[e4];
+      s4[j] = sn[e4];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MI; ++j) {
+    const int it = it0 + tid + 128 * j;
+    if (it >= items) continue;
+    const int h = it / q4, e = (it % q4) * 4;
+    const float4 a0 = x0[j], a1 = x1[j], c = c4[j], s = s4[j];
+    const float4 y0 = make_float4(a0.x * c.x - a1.x * s.x, a0.y * c.y - a1.y * s.y, a0.z * c.z - a1.z * s.z,
+                                  a0.w * c.w - a1.w * s.w);
+    const float4 y1 = make_float4(a1.x * c.x + a0.x * s.x, a1.y * c.y + a0.y * s.y, a1.z * c.z + a0.z * s.z,
+                                  a1.w * c.w + a0.w * s.w);
     if (h < a.Hr) {
-      a.q_out[(size_t)m * a.Hr * hd + h * hd + e] = y0;
-      a.q_out[(size_t)m * a.Hr * hd + h * hd + e + half] = y1;
+      *reinterpret_cast<float4*>(a.q_out + (size_t)m * a.Hr * hd + h * hd + e) = y0;
+      *reinterpret_cast<float4*>(a.q_out + (size_t)m * a.Hr * hd + h * hd + e + half) = y1;
     } else {
-      const uint16_t r0 = f2bf_bits(y0), r1 = f2bf_bits(y1);
       const int kvh = h - a.Hr;
       uint16_t* dst = a.to_cache ? a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_seq + pos) * hd
                                  : a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + i) * hd;
-      dst[e] = r0;
-      dst[e + half] = r1;
+      *reinterpret_cast<uint2*>(dst + e) = make_uint2(pack_bf16(y0.x, y0.y), pack_bf16(y0.z, y0.w));
+      *reinterpret_cast<uint2*>(dst + e + half) = make_uint2(pack_bf16(y1.x, y1.y), pack_bf16(y1.z, y1.w));
     }
   }
-  for (int idx = tid; idx < a.KVr * hd; idx += 128) {
-    const int kvh = idx / hd, e = idx % hd;
-    const float v = row[(a.Hr + a.KVr + kvh) * hd + e];
+  }
+  const int v4 = a.KVr * hd / 4;
+  for (int it0 = 0; it0 < v4; it0 += 128 * 4) {
+  float4 vv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int it = it0 + tid + 128 * j;
+    if (it < v4) vv[j] = __ldcg(reinterpret_cast<const float4*>(row + (a.Hr + a.KVr) * hd) + it);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int it = it0 + tid + 128 * j;
+    if (it >= v4) continue;
+    const int kvh = (it * 4) / hd, e = (it * 4) % hd;
     uint16_t* dst = a.to_cache ? a.v_dst + (((size_t)b * a.KVr + kvh) * a.max_seq + pos) * hd
                                : a.v_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + i) * hd;
-    dst[e] = f2bf_bits(v);
+    *reinterpret_cast<uint2*>(dst + e) = make_uint2(pack_bf16(vv[j].x, vv[j].y), pack_bf16(vv[j].z, vv[j].w));
   }
-}
-
-// ===================================================================== multi-row causal attention
-// grid (splits, KVr * row_blocks, B); 128 threads = 64 query rows x 2 halves of head_dim.
-template <int HD>
-__global__ void __launch_bounds__(128) attn_rows_kernel(AttnRowsArgs a, float scale) {
-  constexpr int H2 = HD / 2, KB = 32, LD = H2 + 1;
-  const int split = blockIdx.x, bz = blockIdx.z, b = a.b_base + bz;  // bz: sequence within this launch
-  const int kvh = blockIdx.y % a.KVr, rb = blockIdx.y / a.KVr;
-  const int tid = threadIdx.x, half = tid & 1;
-  const int G = a.G, rows = a.rows_per_seq;
-  const int r = rb * 64 + (tid >> 1);  // row index within (b, kvh): r = i * G + g
-  const int i = r / G, g = r % G;
-  const bool valid = i < rows;
-  __shared__ float k_s[KB][2][LD];
-  __shared__ float v_s[KB][2][LD];
-  const int T = a.start[b];
-  // keys 0..T-1 from the cache prefix, T.. from the fresh rows (staging or cache)
-  const int i_last = min(rows - 1, (rb * 64 + 63) / G);
-  const int nkeys = max(0, T + i_last + 1);
-  const int S = gridDim.x;
-  const int chunk = (nkeys + S - 1) / S;
-  const int k0 = min(nkeys, split * chunk), k1 = min(nkeys, k0 + chunk);
-  const size_t hb = (size_t)b * a.KVr + kvh;
-  const uint16_t* kc = a.k_cache + hb * a.max_seq * HD;
-  const uint16_t* vc = a.v_cache + hb * a.max_seq * HD;
-  const uint16_t* kf = a.fresh_in_cache ? kc + (size_t)T * HD : a.k_fresh + hb * a.fresh_stride * HD;
-  const uint16_t* vf = a.fresh_in_cache ? vc + (size_t)T * HD : a.v_fresh + hb * a.fresh_stride * HD;
-
-  float q[H2], acc[H2];
-  float mrun = -INFINITY, lrun = 0.f;
-  {
-    const int m = bz * rows + (valid ? i : 0);
-    const float* qp = a.q + (size_t)m * a.Hr * HD + (kvh * G + g) * HD + half * H2;
-#pragma unroll
-    for (int e = 0; e < H2; ++e) {
-      q[e] = qp[e];
-      acc[e] = 0.f;
-    }
-  }
-  const int vis = T + i;  // last visible key for this row
-  for (int p0 = k0; p0 < k1; p0 += KB) {
-    __syncthreads();
-    for (int idx = tid; idx < KB * HD; idx += 128) {
-      const int pp = idx / HD, e = idx % HD, p = p0 + pp;
-      float kv = 0.f, vv = 0.f;
-      if (p < k1) {
-        const uint16_t* ks = p < T ? kc + (size_t)p * HD : kf + (size_t)(p - T) * HD;
-        const uint16_t* vs = p < T ? vc + (size_t)p * HD : vf + (size_t)(p - T) * HD;
-        kv = __uint_as_float((uint32_t)ks[e] << 16);
-        vv = __uint_as_float((uint32_t)vs[e] << 16);
-      }
-      k_s[pp][e / H2][e % H2] = kv;
-      v_s[pp][e / H2][e % H2] = vv;
-    }
-    __syncthreads();
-    const int np = min(KB, k1 - p0);
-    for (int pp = 0; pp < np; ++pp) {
-      float s = 0.f;
-#pragma unroll
-      for (int e = 0; e < H2; ++e) s = fmaf(q[e], k_s[pp][half][e], s);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s *= scale;
-      if (valid && p0 + pp <= vis) {
-        const float mn = fmaxf(mrun, s);
-        const float corr = expf(mrun - mn), pe = expf(s - mn);
-        lrun = lrun * corr + pe;
-#pragma unroll
-        for (int e = 0; e < H2; ++e) acc[e] = fmaf(pe, v_s[pp][half][e], acc[e] * corr);
-        mrun = mn;
-      }
-    }
-  }
-  // partial (M, L, A) for this split
-  const int RB = gridDim.y / a.KVr;
-  float* part = a.part + ((((size_t)bz * a.KVr + kvh) * RB + rb) * S + split) * 64 * (HD + 2);
-  float* pr = part + (tid >> 1) * (HD + 2);
-  if (half == 0) {
-    pr[0] = mrun;
-    pr[1] = lrun;
-  }
-#pragma unroll
-  for (int e = 0; e < H2; ++e) pr[2 + half * H2 + e] = acc[e];
-  if (!arrive_last(a.counters + ((size_t)bz * a.KVr + kvh) * RB + rb, S)) return;
-  if (!valid) return;
-  const float* pb = a.part + (((size_t)bz * a.KVr + kvh) * RB + rb) * S * 64 * (HD + 2) + (tid >> 1) * (HD + 2);
-  float M = -INFINITY;
-  for (int sp = 0; sp < S; ++sp) M = fmaxf(M, __ldcg(pb + (size_t)sp * 64 * (HD + 2)));
-  float L = 0.f;
-  float o[H2];
-#pragma unroll
-  for (int e = 0; e < H2; ++e) o[e] = 0.f;
-  for (int sp = 0; sp < S; ++sp) {
-    const float* ps = pb + (size_t)sp * 64 * (HD + 2);
-    const float Ms = __ldcg(ps);
-    if (Ms == -INFINITY) continue;
-    const float f = expf(Ms - M);
-    L += __ldcg(ps + 1) * f;
-#pragma unroll
-    for (int e = 0; e < H2; ++e) o[e] += __ldcg(ps + 2 + half * H2 + e) * f;
-  }
-  const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + half * H2;
-#pragma unroll
-  for (int e = 0; e < H2; ++e) {
-    const float v = L > 0.f ? o[e] / L : 0.f;
-    const uint16_t hi = f2bf_bits(v);
-    a.out_hi[off + e] = hi;
-    a.out_lo[off + e] = f2bf_bits(v - __uint_as_float((uint32_t)hi << 16));
   }
 }
 
@@ -350,14 +307,6 @@ cudaError_t norm_rows(const NormRowsArgs& a, int M, cudaStream_t st) {
 }
 cudaError_t rope_store(const RopeStoreArgs& a, int M, cudaStream_t st) {
   rope_store_kernel<<<M, 128, 0, st>>>(a);
-  return cudaGetLastError();
-}
-cudaError_t attn_rows(const AttnRowsArgs& a, int nseq, int hd, int splits, int row_blocks, cudaStream_t st) {
-  dim3 grid(splits, a.KVr * row_blocks, nseq);
-  const float scale = 1.0f / sqrtf((float)hd);
-  if (hd == 128) attn_rows_kernel<128><<<grid, 128, 0, st>>>(a, scale);
-  else if (hd == 64) attn_rows_kernel<64><<<grid, 128, 0, st>>>(a, scale);
-  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 cudaError_t accept_stats(const AcceptStatsArgs& a, int splits, cudaStream_t st) {

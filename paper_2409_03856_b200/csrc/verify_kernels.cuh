@@ -85,6 +85,7 @@ namespace launch {
 cudaError_t norm_rows(const NormRowsArgs& a, int M, cudaStream_t st);
 cudaError_t rope_store(const RopeStoreArgs& a, int M, cudaStream_t st);
 cudaError_t attn_rows(const AttnRowsArgs& a, int nseq, int hd, int splits, int row_blocks, cudaStream_t st);
+int attn_rows_splits(int nseq, int KVr, int row_blocks, int max_keys, int num_sms);
 cudaError_t accept_stats(const AcceptStatsArgs& a, int splits, cudaStream_t st);
 cudaError_t accept_finalize(const AcceptFinalArgs& a, int B, cudaStream_t st);
 cudaError_t kv_rewrite(const KvRewriteArgs& a, int L, cudaStream_t st);
