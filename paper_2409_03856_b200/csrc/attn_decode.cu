@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
   __shared__ __align__(16) uint16_t v_s[KB][HD];
   __shared__ float sc[G][KB];
   __shared__ float m_s[G], l_s[G], c_s[G];
-  __shared__ float cw[64][G];  // combine weights
+  __shared__ float cw[64][G];  // combine weights (M_s, then exp(M_s - M))
+  __shared__ float cl2[64][G]; // L_s
   __shared__ float cl[G];
 
   const int S = a.splits, Hr = a.Hr, KVr = a.KVr;
@@ -193,12 +194,29 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
       }
     }
   }
-  if (!arrive_last(a.counters + b * KVr + kvh, S)) return;
-  // last CTA for (b, kvh): combine the active splits (weights first, then independent loads)
+  group_barrier(a.group_bar + 2 * (b * KVr + kvh), S);
+  // ---- distributed combine: split s finalises outputs (g, d) in [G HD s / S, G HD (s+1) / S)
   const float* pb = a.part + ((size_t)b * KVr + kvh) * S * G * (HD + 2);
-  for (int idx = tid; idx < s_active * G; idx += 128) {
-    const int sp = idx / G, g = idx % G;
-    cw[sp][g] = __ldcg(pb + ((size_t)sp * G + g) * (HD + 2));       // M_s
+  {  // (M_s, L_s) of every active split: one parallel round trip into shared memory
+    constexpr int NMW = (64 * G + 127) / 128;
+    float mv[NMW], lv[NMW];
+#pragma unroll
+    for (int j = 0; j < NMW; ++j) {
+      const int idx = tid + 128 * j;
+      if (idx < s_active * G) {
+        const float* ps = pb + (size_t)idx * (HD + 2);  // idx = sp * G + g
+        mv[j] = __ldcg(ps);
+        lv[j] = __ldcg(ps + 1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NMW; ++j) {
+      const int idx = tid + 128 * j;
+      if (idx < s_active * G) {
+        cw[idx / G][idx % G] = mv[j];
+        cl2[idx / G][idx % G] = lv[j];
+      }
+    }
   }
   __syncthreads();
   if (tid < G) {
@@ -207,21 +225,26 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, float scal
     float L = 0.f;
     for (int sp = 0; sp < s_active; ++sp) {
       const float f = cw[sp][tid] == -INFINITY ? 0.f : expf(cw[sp][tid] - M);
-      L += __ldcg(pb + ((size_t)sp * G + tid) * (HD + 2) + 1) * f;
+      L += cl2[sp][tid] * f;
       cw[sp][tid] = f;
     }
     cl[tid] = L;
   }
   __syncthreads();
+  const int oa = G * HD * split / S, oz = G * HD * (split + 1) / S;
+  for (int o0 = oa + tid; o0 < oz; o0 += 128) {
+    const int g = o0 / HD, d = o0 % HD;
+    float o = 0.f;
+    for (int sp0 = 0; sp0 < s_active; sp0 += 16) {  // 16 independent loads in flight
+      float v[16];
 #pragma unroll
-  for (int j = 0; j < NHO; ++j) {
-    const int g = og0 + GSTEP * j;
-    if (g < G) {
-      float o = 0.f;
-#pragma unroll 4
-      for (int sp = 0; sp < s_active; ++sp) o += __ldcg(pb + ((size_t)sp * G + g) * (HD + 2) + 2 + od) * cw[sp][g];
-      a.out[(size_t)b * Hr * HD + (kvh * G + g) * HD + od] = cl[g] > 0.f ? o / cl[g] : 0.f;
+      for (int u = 0; u < 16; ++u)
+        v[u] = sp0 + u < s_active ? __ldcg(pb + ((size_t)(sp0 + u) * G + g) * (HD + 2) + 2 + d) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (sp0 + u < s_active) o += v[u] * cw[sp0 + u][g];
     }
+    a.out[(size_t)b * Hr * HD + (kvh * G + g) * HD + d] = cl[g] > 0.f ? o / cl[g] : 0.f;
   }
 }
 
@@ -234,18 +257,24 @@ cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out,
 }
 
 int attn_splits(int B, int KVr, int num_sms) {
-  int s = (num_sms + B * KVr - 1) / (B * KVr);
+  int s = num_sms / (B * KVr);  // one wave
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
 cudaError_t attn_decode(const AttnArgs& a, int B, int hd, int group, cudaStream_t st) {
   dim3 grid(a.splits, a.KVr, B);
   const float scale = 1.0f / sqrtf((float)hd);
-#define SIRIUS_ATTN(HD, GG)                                       \
-  if (hd == HD && group == GG) {                                  \
-    attn_decode_kernel<HD, GG><<<grid, 128, 0, st>>>(a, scale);   \
-    return cudaGetLastError();                                    \
-  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the per-(b, kvh) split barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.splits > 1 ? 1 : 0;
+#define SIRIUS_ATTN(HD, GG) \
+  if (hd == HD && group == GG) return cudaLaunchKernelEx(&cfg, attn_decode_kernel<HD, GG>, a, scale);
   SIRIUS_ATTN(128, 1) SIRIUS_ATTN(128, 2) SIRIUS_ATTN(128, 4) SIRIUS_ATTN(128, 8)
   SIRIUS_ATTN(64, 1) SIRIUS_ATTN(64, 2) SIRIUS_ATTN(64, 4) SIRIUS_ATTN(64, 8)
 #undef SIRIUS_ATTN

@@ -3,13 +3,15 @@
 //
 // Query rows of one (sequence, kv head) — R = rows_per_seq x G q-heads, up to 64 per row block —
 // attend causally: row i (position T + i) sees cache[0, T) and the kernel's own rows [0, i] (verify:
-// in the staging area; prefill: already in the cache).  grid (splits, KVr x row_blocks, nseq),
-// 256 threads.  Each CTA walks its key range in 64-key blocks staged in shared memory:
-//   scores   thread -> (key t % 64, 16 rows)        k rows padded: conflict-free, q broadcast
+// in the staging area; prefill: already in the cache).  grid (S splits, KVr x row_blocks, nseq),
+// 256 threads, cooperative (one wave, all CTAs co-resident).  Each CTA walks its key range in
+// 64-key blocks staged in shared memory:
+//   scores   thread -> (key t % 64, 16 rows)          k rows padded: conflict-free, q broadcast
 //   softmax  warp   -> 8 rows, online (running max / sum per row)
-//   P.V      thread -> (dim, 32 rows)              v reads consecutive, p broadcast
-// then writes its partial (M, L, A) per row; the last-arriving split combines and writes the output
-// as a bf16 hi/lo pair (the tensor-core operand of the O-projection).  fp32 throughout (D15).
+//   P.V      thread -> (4 dims, 8 rows)               v: 8-byte reads, p broadcast
+// then writes its partial (M, L, A) per row; after a barrier among the S splits of the group, split s
+// combines rows [64 s / S, 64 (s+1) / S) and writes them as a bf16 hi/lo pair (the tensor-core
+// operand of the O-projection).  fp32 throughout (D15).
 #include "common.cuh"
 #include "verify_kernels.cuh"
 
@@ -19,12 +21,12 @@ namespace {
 constexpr int kRows = 64, kKB = 64, kThreads = 256;
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_rows_kernel(AttnRowsArgs a, float scale) {
+__global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, float scale) {
   constexpr int KROW = HD + 8;                     // padded bf16 K row (elements)
   constexpr int RPT = kRows * kKB / kThreads;      // score rows per thread (16)
   constexpr int RSTEP = kThreads / kKB;            // 4
-  constexpr int DPT = kRows * HD / kThreads;       // P.V outputs per thread (32 for HD=128)
-  constexpr int DSTEP = kThreads / HD;             // row step in P.V (2 for HD=128)
+  constexpr int DPL = HD / 32;                     // P.V dims per thread (4 for HD=128)
+  constexpr int RPW = kRows / (kThreads / 32);     // P.V rows per thread (8)
   extern __shared__ __align__(16) uint8_t smem[];
   float* q_s = reinterpret_cast<float*>(smem);                                   // [kRows][HD]
   uint16_t* k_s = reinterpret_cast<uint16_t*>(q_s + kRows * HD);                 // [kKB][KROW]
@@ -33,7 +35,6 @@ __global__ void __launch_bounds__(kThreads) attn_rows_kernel(AttnRowsArgs a, flo
   float* m_s = p_s + kRows * (kKB + 1);                                          // [kRows]
   float* l_s = m_s + kRows;
   float* c_s = l_s + kRows;
-  __shared__ unsigned flag_last;
 
   const int split = blockIdx.x, bz = blockIdx.z, b = a.b_base + bz;
   const int kvh = blockIdx.y % a.KVr, rb = blockIdx.y / a.KVr;
@@ -53,9 +54,9 @@ __global__ void __launch_bounds__(kThreads) attn_rows_kernel(AttnRowsArgs a, flo
   const uint16_t* kf = a.fresh_in_cache ? kc + (size_t)T * HD : a.k_fresh + hb * a.fresh_stride * HD;
   const uint16_t* vf = a.fresh_in_cache ? vc + (size_t)T * HD : a.v_fresh + hb * a.fresh_stride * HD;
 
-  // q rows (fp32, post-RoPE), score scale folded in
+  // q rows (fp32, post-RoPE), score scale folded in; all loads issued first
   {
-    constexpr int NQ = kRows * HD / 4 / kThreads;  // float4 per thread, all loads issued first
+    constexpr int NQ = kRows * HD / 4 / kThreads;
     float4 qv[NQ];
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
@@ -67,19 +68,20 @@ __global__ void __launch_bounds__(kThreads) attn_rows_kernel(AttnRowsArgs a, flo
       }
     }
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) {
-      const int idx = tid + kThreads * j;
-      reinterpret_cast<float4*>(q_s)[idx] = make_float4(qv[j].x * scale, qv[j].y * scale, qv[j].z * scale, qv[j].w * scale);
-    }
+    for (int j = 0; j < NQ; ++j)
+      reinterpret_cast<float4*>(q_s)[tid + kThreads * j] =
+          make_float4(qv[j].x * scale, qv[j].y * scale, qv[j].z * scale, qv[j].w * scale);
   }
   if (tid < kRows) {
     m_s[tid] = -INFINITY;
     l_s[tid] = 0.f;
   }
-  float acc[DPT];
+  const int dg = lane, rg = warp;  // P.V: dims 4 dg .. 4 dg + 3, rows 8 rg .. 8 rg + 7
+  float acc[RPW][DPL];
 #pragma unroll
-  for (int j = 0; j < DPT; ++j) acc[j] = 0.f;
-  const int od = tid % HD, orow0 = tid / HD;
+  for (int j = 0; j < RPW; ++j)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[j][e] = 0.f;
 
   for (int p0 = k0; p0 < k1; p0 += kKB) {
     const int nb = min(kKB, k1 - p0);
@@ -159,73 +161,87 @@ __global__ void __launch_bounds__(kThreads) attn_rows_kernel(AttnRowsArgs a, flo
       }
     }
     __syncthreads();
-    // ---- P.V: thread -> (dim od, rows orow0 + DSTEP j)
+    // ---- P.V: thread -> (dims 4 dg.., rows 8 rg..)
 #pragma unroll
-    for (int j = 0; j < DPT; ++j) acc[j] *= c_s[orow0 + DSTEP * j];
+    for (int j = 0; j < RPW; ++j) {
+      const float c = c_s[rg * RPW + j];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] *= c;
+    }
     for (int kk = 0; kk < nb; ++kk) {
-      const float v = __uint_as_float((uint32_t)v_s[kk * HD + od] << 16);
+      float vf4[DPL];
+      if constexpr (DPL == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(v_s + kk * HD + dg * 4);
+        vf4[0] = bf16_lo(w.x); vf4[1] = bf16_hi(w.x); vf4[2] = bf16_lo(w.y); vf4[3] = bf16_hi(w.y);
+      } else {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(v_s + kk * HD + dg * 2);
+        vf4[0] = bf16_lo(w); vf4[1] = bf16_hi(w);
+      }
 #pragma unroll
-      for (int j = 0; j < DPT; ++j) acc[j] = fmaf(p_s[(orow0 + DSTEP * j) * (kKB + 1) + kk], v, acc[j]);
+      for (int j = 0; j < RPW; ++j) {
+        const float p = p_s[(rg * RPW + j) * (kKB + 1) + kk];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(p, vf4[e], acc[j][e]);
+      }
     }
   }
   __syncthreads();
-  // ---- partial (M, L, A) of this split
+  // ---- partial (M, L, A) of this split -> group barrier over the S splits
   const int RB = gridDim.y / a.KVr;
-  float* part = a.part + ((((size_t)bz * a.KVr + kvh) * RB + rb) * S + split) * kRows * (HD + 2);
+  const size_t grp = ((size_t)bz * a.KVr + kvh) * RB + rb;
+  float* pbase = a.part + grp * S * kRows * (HD + 2);
+  float* part = pbase + (size_t)split * kRows * (HD + 2);
 #pragma unroll
-  for (int j = 0; j < DPT; ++j) {
-    const int r = orow0 + DSTEP * j;
-    part[r * (HD + 2) + 2 + od] = acc[j];
+  for (int j = 0; j < RPW; ++j) {
+    float* pr = part + (rg * RPW + j) * (HD + 2) + 2 + dg * DPL;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) pr[e] = acc[j][e];
   }
   if (tid < kRows) {
     part[tid * (HD + 2)] = m_s[tid];
     part[tid * (HD + 2) + 1] = l_s[tid];
   }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    unsigned* cnt = a.counters + ((size_t)bz * a.KVr + kvh) * RB + rb;
-    const unsigned old = atomicAdd(cnt, 1u);
-    const bool last = old == (unsigned)S - 1;
-    if (last) {
-      atomicExch(cnt, 0u);
-      __threadfence();
-    }
-    flag_last = last ? 1u : 0u;
-  }
-  __syncthreads();
-  if (!flag_last) return;
-  // ---- combine the splits (weights per (split, row) first, then independent loads)
-  const float* pb = a.part + (((size_t)bz * a.KVr + kvh) * RB + rb) * S * kRows * (HD + 2);
+  group_barrier(a.group_bar + 2 * grp, S);
+  // ---- distributed combine: split s finalises rows [64 s / S, 64 (s+1) / S)
   const int s_active = chunk > 0 ? (nkeys + chunk - 1) / chunk : 0;
-  float* w_s = p_s;  // reuse: [S][kRows] weights (S <= kKB + 1)
-  if (tid < kRows) {
+  const int ra = kRows * split / S, rz = kRows * (split + 1) / S, nrow = rz - ra;
+  float* w_s = p_s;            // [nrow][S] weights exp(M_s - M)
+  if (tid < nrow) {
+    const int r = ra + tid;
     float M = -INFINITY;
-    for (int sp = 0; sp < s_active; ++sp) M = fmaxf(M, __ldcg(pb + ((size_t)sp * kRows + tid) * (HD + 2)));
+    float mv[kKB];
+#pragma unroll 8
+    for (int sp = 0; sp < s_active; ++sp) mv[sp] = __ldcg(pbase + ((size_t)sp * kRows + r) * (HD + 2));
+    for (int sp = 0; sp < s_active; ++sp) M = fmaxf(M, mv[sp]);
     float L = 0.f;
+#pragma unroll 8
     for (int sp = 0; sp < s_active; ++sp) {
-      const float* ps = pb + ((size_t)sp * kRows + tid) * (HD + 2);
-      const float Ms = __ldcg(ps);
-      const float f = (Ms == -INFINITY || M == -INFINITY) ? 0.f : expf(Ms - M);
-      L += __ldcg(ps + 1) * f;
-      w_s[sp * kRows + tid] = f;
+      const float f = (mv[sp] == -INFINITY || M == -INFINITY) ? 0.f : expf(mv[sp] - M);
+      L += __ldcg(pbase + ((size_t)sp * kRows + r) * (HD + 2) + 1) * f;
+      w_s[tid * kKB + sp] = f;
     }
     l_s[tid] = L;
   }
   __syncthreads();
-#pragma unroll 4
-  for (int j = 0; j < DPT; ++j) {
-    const int r = orow0 + DSTEP * j;
+  for (int idx = tid; idx < nrow * HD; idx += kThreads) {
+    const int rl = idx / HD, d = idx % HD, r = ra + rl;
     if (r >= nr) continue;
     float o = 0.f;
-    for (int sp = 0; sp < s_active; ++sp)
-      o += __ldcg(pb + ((size_t)sp * kRows + r) * (HD + 2) + 2 + od) * w_s[sp * kRows + r];
-    const float v = l_s[r] > 0.f ? o / l_s[r] : 0.f;
+    for (int sp0 = 0; sp0 < s_active; sp0 += 16) {  // 16 independent loads in flight
+      float v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        v[u] = sp0 + u < s_active ? __ldcg(pbase + ((size_t)(sp0 + u) * kRows + r) * (HD + 2) + 2 + d) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (sp0 + u < s_active) o += v[u] * w_s[rl * kKB + sp0 + u];
+    }
+    const float val = l_s[rl] > 0.f ? o / l_s[rl] : 0.f;
     const int rr = r_base + r, i = rr / G, g = rr % G;
-    const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + od;
-    const uint16_t hi = f2bf_bits(v);
+    const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + d;
+    const uint16_t hi = f2bf_bits(val);
     a.out_hi[off] = hi;
-    a.out_lo[off] = f2bf_bits(v - __uint_as_float((uint32_t)hi << 16));
+    a.out_lo[off] = f2bf_bits(val - __uint_as_float((uint32_t)hi << 16));
   }
 }
 
@@ -235,35 +251,43 @@ size_t attn_rows_smem() {
          3 * kRows * 4;
 }
 
+template <int HD>
+cudaError_t launch_hd(const AttnRowsArgs& a, dim3 grid, float scale, cudaStream_t st) {
+  const size_t sm = attn_rows_smem<HD>();
+  cudaError_t e = cudaFuncSetAttribute(attn_rows_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the per-group barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = grid.x > 1 ? 1 : 0;  // S == 1: no barrier partner, plain launch
+  return cudaLaunchKernelEx(&cfg, attn_rows_kernel<HD>, a, scale);
+}
+
 }  // namespace
 
 namespace launch {
 
+// splits per (sequence, kv head, row block): one wave of 1-CTA-per-SM blocks in total
 int attn_rows_splits(int nseq, int KVr, int row_blocks, int max_keys, int num_sms) {
-  int s = (num_sms + nseq * KVr * row_blocks - 1) / (nseq * KVr * row_blocks);
+  int s = num_sms / (nseq * KVr * row_blocks);
   const int by_keys = (max_keys + kKB - 1) / kKB;  // no more splits than 64-key blocks
   if (s > by_keys) s = by_keys;
-  if (s > kKB) s = kKB;  // combine weights buffer
+  if (s > kKB) s = kKB;                             // combine weights buffer
   return s < 1 ? 1 : s;
 }
 
 cudaError_t attn_rows(const AttnRowsArgs& a, int nseq, int hd, int splits, int row_blocks, cudaStream_t st) {
   dim3 grid(splits, a.KVr * row_blocks, nseq);
   const float scale = 1.0f / sqrtf((float)hd);
-  if (hd == 128) {
-    const size_t sm = attn_rows_smem<128>();
-    cudaError_t e = cudaFuncSetAttribute(attn_rows_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attn_rows_kernel<128><<<grid, kThreads, sm, st>>>(a, scale);
-  } else if (hd == 64) {
-    const size_t sm = attn_rows_smem<64>();
-    cudaError_t e = cudaFuncSetAttribute(attn_rows_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attn_rows_kernel<64><<<grid, kThreads, sm, st>>>(a, scale);
-  } else {
-    return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  if (hd == 128) return launch_hd<128>(a, grid, scale, st);
+  if (hd == 64) return launch_hd<64>(a, grid, scale, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace launch

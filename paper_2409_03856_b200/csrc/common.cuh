@@ -163,6 +163,27 @@ SIRIUS_DEV void grid_barrier(unsigned long long* counter, unsigned nblocks) {
   __syncthreads();
 }
 
+// Barrier among the n co-resident CTAs that share bar[0] (arrival count) / bar[1] (generation), a
+// subset of a cooperative grid.  Self-resetting, so the same counter may be used by later launches
+// with a different n (each counter is used at most once per launch).
+SIRIUS_DEV void group_barrier(unsigned* bar, unsigned n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;  // read the generation BEFORE arriving
+    __threadfence();
+    if (atomicAdd(bar, 1u) == n - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // "last CTA to arrive" election for split reductions; returns true in exactly one CTA per group
 // of `n` arrivals.  The last arrival resets the counter to 0 for the next launch.
 SIRIUS_DEV bool arrive_last(unsigned* counter, unsigned n) {

@@ -68,7 +68,8 @@ struct AttnArgs {
   uint16_t* v_cache;
   int Hr, KVr, max_seq, splits;
   float* part;             // workspace [B, KVr, splits, G, hd + 2]
-  unsigned* counters;      // [B, KVr]
+  unsigned* counters;      // unused
+  unsigned* group_bar;     // [B, KVr][2] barrier (count, generation) of the split groups
   float* out;              // [B, Hr * hd] fp32
   int* err;                // sticky device error word
 };

@@ -89,6 +89,7 @@ struct RankState {
   float *ffn_part = nullptr, *attn_part = nullptr, *gemm_part = nullptr;
   int* ffn_cnt = nullptr;
   unsigned long long* ffn_barrier = nullptr;
+  unsigned* attn_bar = nullptr;  // split-group barriers (count, generation) of the attention kernels
   unsigned *attn_cnt = nullptr, *gemm_cnt = nullptr, *head_cnt = nullptr;
   // tensor maps
   std::vector<TmapBuf> tm_qkv, tm_o, tm_gate, tm_up, tm_down;
@@ -364,6 +365,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       aa.fresh_in_cache = to_cache ? 1 : 0;
       aa.part = R.attn_part;
       aa.counters = R.attn_cnt;
+      aa.group_bar = R.attn_bar;
       aa.out_hi = R.ob_hi;
       aa.out_lo = R.ob_lo;
       const int row_blocks = (rows_per_seq * c->G + 63) / 64;
@@ -521,7 +523,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
         alloc(c, &R.mb_lo, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * 4 * d) ||
         alloc(c, &R.ffn_cnt, (size_t)c->num_sms * 4) || alloc(c, &R.ffn_barrier, 8) ||
         alloc(c, &R.attn_part, (size_t)kAttnRowUnits * 64 * (hd + 2) + (size_t)B * c->KVr * 64 * 8 * (hd + 2)) ||
-        alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) ||
+        alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) || alloc(c, &R.attn_bar, 8192) ||
         alloc(c, &R.gemm_part, launch::gemm_workspace_bytes(c->num_sms) / sizeof(float)) ||
         alloc(c, &R.gemm_cnt, (size_t)(c->Vr / 128 + 1024)) || alloc(c, &R.head_cnt, 16))
       return cleanup_fail(SIRIUS_ERR_CUDA);
@@ -688,6 +690,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       at.splits = c->attn_splits;
       at.part = R.attn_part;
       at.counters = R.attn_cnt;
+      at.group_bar = R.attn_bar;
       at.out = R.ob;
       at.err = c->err_dev;
       prof_begin(c, P_ATTN);

@@ -43,7 +43,8 @@ struct AttnRowsArgs {
   const uint16_t* v_fresh;
   int fresh_stride, fresh_in_cache;
   float* part;              // workspace
-  unsigned* counters;       // [nseq * KVr * row_blocks]
+  unsigned* counters;       // unused (kept for ABI-internal layout)
+  unsigned* group_bar;      // [nseq * KVr * row_blocks][2] barrier (count, generation) of the split groups
   uint16_t* out_hi;         // [nseq * rows, Hr * hd] attention output as a bf16 hi/lo pair
   uint16_t* out_lo;
 };

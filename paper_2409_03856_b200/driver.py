@@ -79,13 +79,14 @@ class Driver:
         self.kidx = 0
         self.log: List[KernelLog] = []
 
-    def _upload(self, gamma: int) -> None:
+    def _upload(self, gamma: int, T=None) -> None:
         B = self.B
+        T = self.T if T is None else T
         h = self.h_out.numpy()
         h[0:B] = self.n_rows_h
-        h[B:2 * B] = self.T
+        h[B:2 * B] = T
         h[2 * B:3 * B] = self.pending
-        pos = (np.asarray(self.T, dtype=np.int64)[None, :] + np.arange(gamma)[:, None]).astype(np.int32)
+        pos = (np.asarray(T, dtype=np.int64)[None, :] + np.arange(gamma)[:, None]).astype(np.int32)
         h[3 * B:3 * B + gamma * B] = pos.reshape(-1)
         n = 3 * B + gamma * B
         self.d_out[:n].copy_(self.h_out[:n], non_blocking=True)
@@ -175,3 +176,22 @@ class Driver:
         flags = S.SIRIUS_DENSE if dense else 0
         for i in range(first, first + n):
             self.ctx.sparse_decode_step(toks[i], pos[i], flags, toks[i + 1])
+
+    def greedy_run(self, pending, T, n: int, dense: bool) -> None:
+        """n greedy decode steps (dense M_F or CS-only M_S) continuing from `pending` at positions
+        T, T+1, ...: chunks of max_gamma steps over fixed buffer slots (so each step replays a cached
+        CUDA graph), one H2D of the chunk's positions per chunk, no host sync."""
+        B, m = self.B, self.gmax
+        flags = S.SIRIUS_DENSE if dense else 0
+        T = list(T)
+        self.drafts[0].copy_(self.torch.tensor(pending, dtype=self.torch.int32), non_blocking=False)
+        done = 0
+        while done < n:
+            k = min(m, n - done)
+            self._upload(m, T)  # positions T .. T + m - 1 of this chunk into d_out
+            self.pos[:m].copy_(self.d_out[3 * B:3 * B + m * B].view(m, B))
+            for i in range(k):
+                self.ctx.sparse_decode_step(self.drafts[i], self.pos[i], flags, self.drafts[i + 1])
+            self.drafts[0].copy_(self.drafts[k])
+            T = [t + k for t in T]
+            done += k
