@@ -186,7 +186,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2409_03856_b200 import driver, sirius as S
+    from paper_2409_03856_b200 import driver, sirius as S, tp as TP
     from synth import gpu as sg
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,17 +204,7 @@ def main():
     thr = synth.layer_thresholds(cfg, a.rho)
     comm = None
     if tp > 1:
-        lib = S.load()
-        import ctypes
-        uid = (ctypes.c_char * 128)()
-        if rank == 0:
-            assert lib.sirius_nccl_unique_id(uid) == 0
-        obj = [bytes(uid) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctypes.memmove(uid, obj[0], 128)
-        h = ctypes.c_void_p()
-        assert lib.sirius_nccl_comm_init(tp, uid, rank, ctypes.byref(h)) == 0, "ncclCommInitRank failed"
-        comm = h.value
+        comm = TP.nccl_bootstrap(S.load(), tp, rank)
     n_gen_max = (a.warmup + 2 * a.steps + 2) * a.gamma + a.baseline_tokens + 64
     max_seq = a.prompt + n_gen_max + 2 * a.gamma
     ctx = S.Sirius(cfg, weights, thr, batch=1, max_seq=max_seq, max_gamma=a.gamma, tp_size=tp, tp_rank=rank,
@@ -224,16 +214,7 @@ def main():
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    barrier, max_over_ranks = TP.barrier, TP.max_over_ranks
 
     stream = torch.cuda.current_stream()
     # ---------------- Sirius: W warm-up kernels, then K timed kernels

@@ -115,7 +115,8 @@ size_t kv_index(const Oracle* o, int l, int slot, int nslots, int kvh) {
 // One decoder layer's attention block for a row at position pos.
 // Visible keys: if stage_row < 0, cache slots [0, pos] (the row's own K/V were just written to
 // slot pos); else cache slots [0, pos - stage_row) followed by staging rows [0, stage_row].
-void attention_block(Oracle* o, int l, double* x, int pos, int stage_row) {
+// kv_only: stop after the row's K/V are stored (nothing downstream of them is wanted).
+void attention_block(Oracle* o, int l, double* x, int pos, int stage_row, bool kv_only = false) {
   const int d = o->d, H = o->H, KV = o->KV, hd = o->hd, rows = (H + 2 * KV) * hd;
   std::vector<double> h(d), qkv(rows), attn(H * hd), y(d);
   rmsnorm(o, x, o->attn_norm[l], h.data());
@@ -138,6 +139,7 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row) {
         o->vs[kv_index(o, l, stage_row, o->max_gamma, kh) + i] = v[kh * hd + i];
       }
     }
+  if (kv_only) return;
   const int n_cache = stage_row < 0 ? pos + 1 : pos - stage_row;
   const int n_stage = stage_row < 0 ? 0 : stage_row + 1;
   const int n_vis = n_cache + n_stage;
@@ -282,6 +284,22 @@ void oracle_forward_row(void* h, int tok, int pos, int sparse, const float* thre
     rmsnorm(o, x.data(), o->final_norm, hf.data());
     matvec(o, o->lm_head, o->vocab, d, hf.data(), logits);
   }
+}
+
+// Prompt row whose only wanted output is its K/V cache rows (every prefill row but the last):
+// the full row for layers [0, L-1), then the last layer's K/V store.  The stored values are those
+// oracle_forward_row writes for the same row (the skipped work — last-layer attention, MLP and
+// head — does not feed them).
+void oracle_prefill_kv_row(void* h, int tok, int pos) {
+  Oracle* o = (Oracle*)h;
+  const int d = o->d;
+  std::vector<double> x(d);
+  for (int k = 0; k < d; ++k) x[k] = bf16_value(o->embed[(size_t)tok * d + k]);
+  for (int l = 0; l + 1 < o->L; ++l) {
+    attention_block(o, l, x.data(), pos, -1);
+    mlp_block(o, l, x.data(), 0, 0.0, nullptr, nullptr, nullptr);
+  }
+  attention_block(o, o->L - 1, x.data(), pos, -1, true);
 }
 
 // Layer-isolated MLP (kernel-level parity at full shapes): x[d] in/out.

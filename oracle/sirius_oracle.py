@@ -54,6 +54,7 @@ def _lib():
         lib.oracle_set_global.argtypes = [P, P, P, P]
         lib.oracle_set_layer.argtypes = [P, ctypes.c_int] + [P] * 7
         lib.oracle_forward_row.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P, P, P]
+        lib.oracle_prefill_kv_row.argtypes = [P, ctypes.c_int, ctypes.c_int]
         lib.oracle_mlp.argtypes = [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_float, P, P, P]
         lib.oracle_kv_rewrite.argtypes = [P, ctypes.c_int, ctypes.c_int]
         lib.oracle_read_cache.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
@@ -153,6 +154,16 @@ class OracleModel:
         """Dense prefill (PAPER.md:471 'most use full weights for prefilling', reading D17).
         Writes the cache rows [0, P); returns the logits of every prompt position [P, vocab]."""
         return np.stack([self.forward_row(t, i).logits for i, t in enumerate(tokens)])
+
+    def prefill_last(self, tokens: Sequence[int]) -> np.ndarray:
+        """Dense prefill that returns only the last position's logits: rows [0, P-1) write their
+        K/V cache rows only (oracle_prefill_kv_row), the last row runs in full.  Same cache
+        contents as prefill(); used where long prompts would make the full version slow."""
+        lib = _lib()
+        for i, t in enumerate(tokens[:-1]):
+            assert 0 <= t < self.cfg.vocab and i < self.max_seq
+            lib.oracle_prefill_kv_row(self.h, int(t), i)
+        return self.forward_row(tokens[-1], len(tokens) - 1).logits
 
     def decode(self, tok: int, pos: int, sparse: bool, thresholds=None, **kw) -> RowOut:
         """One decode step of M_S (sparse) or M_F (dense): writes K/V at cache slot pos."""

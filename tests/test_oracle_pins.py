@@ -96,6 +96,21 @@ def test_kv_identity_and_chunk_equals_sequential(tiny):
     assert np.all(k[32:] == 0) and np.any(k[:32] != 0)
 
 
+def test_prefill_last_writes_the_same_cache_as_prefill(tiny):
+    """prefill_last (K/V-only rows for all but the last prompt position) leaves the cache and the
+    last logits bitwise equal to the full prefill: the skipped work does not feed them."""
+    cfg, w = tiny
+    prompt = synth.eval_prompt(cfg, 4, 37)
+    a = so.OracleModel(cfg, w, max_seq=64, max_gamma=8)
+    full = a.prefill(prompt)
+    b = so.OracleModel(cfg, w, max_seq=64, max_gamma=8)
+    last = b.prefill_last(prompt)
+    np.testing.assert_array_equal(last, full[-1])
+    for l in range(cfg.n_layers):
+        for x, y in zip(a.read_cache(l, 37), b.read_cache(l, 37)):
+            np.testing.assert_array_equal(x, y)
+
+
 def test_rewrite_equivalence(tiny):
     """SPEC S:147 / S:553: after kv_rewrite the cache rows [0,len) equal those of a
     dense prefill of the committed tokens, bitwise."""

@@ -1,0 +1,239 @@
+"""GPU parity at Llama-3-8B shapes, in the launch configuration bench.py times.
+
+bench.py (BASELINE.json configs[1]) runs the 8B shape with batch 1, gamma 16, a ~900-1300 token
+context and TP 1.  Every kernel grid of the decode and verify paths is a function of (d_model,
+ffn_dim, vocab, heads, batch, gamma, #SMs) only, never of the layer count, so the 1- and 2-layer
+truncations of the 8B model below launch exactly the kernels bench.py launches per layer, and
+the oracle can follow them element by element:
+
+  * 8B-1L, prompt 1230 (> 18 splits x 64 keys: the multi-block attention path and a ragged last
+    block), B = 1, gamma 16: prefill -> sparse / dense decode -> correct_kernel -> kv_rewrite ->
+    decode, every logit compared, active sets and decisions pinned (SURVEY.md §8(c) rules);
+  * 8B-2L, B = 2 with different prompt lengths (per-sequence positions and active sets, the union
+    of active rows loaded, inactive (b, n) pairs contributing exact zeros — reading D19);
+  * 8B-2L tensor-parallel emulation, TP 2 and 8 on one GPU (each rank thresholds its own neuron
+    shard with the same t_l; partial sums combined in rank order; vocab-parallel head).
+Tolerances are the north star's: |l_gpu - l_ref| <= 2e-2 + 1e-2 |l_ref|.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import sirius_oracle as so
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ABS, REL = 2e-2, 1e-2
+GAMMA = 16
+
+
+def check_logits(gpu, ref):
+    err = np.abs(gpu - ref)
+    assert np.all(err <= ABS + REL * np.abs(ref)), (float(err.max()), int(np.argmax(err)))
+    return float(err.max())
+
+
+def margin(ref):
+    s = np.sort(ref)
+    return float(s[-1] - s[-2])
+
+
+def i32(x):
+    return torch.tensor(np.asarray(x, dtype=np.int32), device="cuda")
+
+
+def make_ctx(cfg, wd, thr, batch, max_seq, tp=1):
+    from paper_2409_03856_b200 import sirius as S
+    return S.Sirius(cfg, wd, thr, batch=batch, max_seq=max_seq, max_gamma=GAMMA, tp_size=tp)
+
+
+def gpu_decode(ctx, cfg, toks, pos, dense, tp_full=True):
+    from paper_2409_03856_b200 import sirius as S
+    B, L, F, V = len(toks), cfg.n_layers, cfg.ffn_dim, cfg.vocab
+    to = torch.zeros(B, dtype=torch.int32, device="cuda")
+    lo = torch.zeros((B, V), dtype=torch.float32, device="cuda")
+    na = torch.zeros((B, L), dtype=torch.int32, device="cuda")
+    ga = torch.zeros((B, L, F), dtype=torch.float32, device="cuda")
+    ctx.sparse_decode_step(i32(toks), i32(pos), S.SIRIUS_DENSE if dense else 0, to, lo, na, ga)
+    torch.cuda.synchronize()
+    return to.cpu().numpy(), lo.cpu().numpy(), na.cpu().numpy(), ga.cpu().numpy()
+
+
+def check_decode_row(cfg, thr, ref, tok_gpu, lg, na, ga, sparse):
+    """One sequence's decode row against the oracle's: logits, a = SiLU(g), active set (every
+    mismatch explained by the float error of a), count, argmax (pinned by the top-2 margin)."""
+    eps = check_logits(lg, ref.logits)
+    bad = np.abs(ga - ref.gate) > 1e-3 + 1e-3 * np.abs(ref.gate)
+    assert not bad.any(), ("gate activations", np.argwhere(bad)[:8].tolist(), ga[bad][:8], ref.gate[bad][:8])
+    if sparse:
+        act = np.abs(ga) >= thr[:, None]
+        mism = act != ref.mask.astype(bool)
+        tt = np.repeat(thr[:, None], cfg.ffn_dim, 1)
+        assert np.all(np.abs(np.abs(ref.gate[mism]) - tt[mism]) <= np.abs(ga[mism] - ref.gate[mism]) + 1e-7)
+        assert np.array_equal(na, act.sum(1))
+        assert int(mism.sum()) <= 8
+    else:
+        assert np.all(na == cfg.ffn_dim)
+    if margin(ref.logits) > 2 * eps:
+        assert int(tok_gpu) == so.argmax_lowest(ref.logits)
+    assert int(tok_gpu) == int(np.argmax(lg))
+
+
+def gpu_correct(ctx, cfg, kernel_tokens, T, r):
+    B = len(kernel_tokens)
+    g = len(kernel_tokens[0])
+    na = torch.zeros(B, dtype=torch.int32, device="cuda")
+    nx = torch.zeros(B, dtype=torch.int32, device="cuda")
+    q = torch.zeros((B, g), dtype=torch.float32, device="cuda")
+    lo = torch.zeros((B, g, cfg.vocab), dtype=torch.float32, device="cuda")
+    ctx.correct_kernel(i32(kernel_tokens), i32(T), g, r, 0, na, nx, q, lo)
+    torch.cuda.synchronize()
+    return na.cpu().numpy(), nx.cpu().numpy(), q.cpu().numpy(), lo.cpu().numpy()
+
+
+def check_correct(lf, ins, r, j_gpu, nx_gpu, q_gpu, lo_gpu):
+    eps = max(check_logits(lo_gpu[i], lf[i]) for i in range(len(ins)))
+    j_ref, q_ref = so.accept_scan(lf, ins, r)
+    np.testing.assert_allclose(q_gpu, q_ref, rtol=0.05, atol=1e-4)
+    pinned = all(abs(np.log(max(q_ref[i], 1e-30)) - np.log(r)) > 2 * eps + 1e-5 for i in range(len(ins) - 1))
+    if pinned:
+        assert int(j_gpu) == j_ref
+        if margin(lf[j_ref]) > 2 * eps:
+            assert int(nx_gpu) == so.argmax_lowest(lf[j_ref])
+    return j_ref
+
+
+# ------------------------------------------------------------------ 8B-1L, long context, B = 1
+@pytest.fixture(scope="module")
+def l1():
+    from synth import gpu as sg
+    cfg = synth.LLAMA3_8B.with_layers(1)
+    return cfg, synth.host_weights(cfg), sg.device_weights(cfg)
+
+
+def test_8b_long_context_decode_verify_rewrite(l1):
+    cfg, wh, wd = l1
+    thr = synth.layer_thresholds(cfg, 0.5)
+    P, max_seq = 1230, 1400
+    prompt = synth.eval_prompt(cfg, 0, P)
+    om = so.OracleModel(cfg, wh, max_seq=max_seq, max_gamma=GAMMA)
+    l_last = om.prefill_last(prompt)
+    ctx = make_ctx(cfg, wd, thr, 1, max_seq)
+    first = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [P], first)
+    torch.cuda.synchronize()
+    tok = so.argmax_lowest(l_last)
+    if margin(l_last) > 0.1:
+        assert int(first.item()) == tok
+    # decode: sparse, sparse, dense (teacher-forced on the oracle's tokens)
+    T = P
+    for step, sparse in enumerate((True, True, False)):
+        ref = om.decode(tok, T, sparse, thr, want_gate=True, want_mask=True)
+        to, lo, na, ga = gpu_decode(ctx, cfg, [tok], [T], not sparse)
+        check_decode_row(cfg, thr, ref, to[0], lo[0], na[0], ga[0], sparse)
+        tok = so.argmax_lowest(ref.logits)
+        T += 1
+    # one correction kernel of gamma = 16 rows: the oracle drafts, both verify
+    ins = [tok]
+    for i in range(GAMMA - 1):
+        ref = om.decode(ins[i], T + i, True, thr)
+        gpu_decode(ctx, cfg, [ins[i]], [T + i], False)
+        ins.append(so.argmax_lowest(ref.logits))
+    lf = om.verify(ins, T)
+    for r in (0.1, 0.3):
+        j, nx, q, lo = gpu_correct(ctx, cfg, [ins], [T], r)
+        j_ref = check_correct(lf, ins, r, j[0], nx[0], q[0], lo[0])
+    # commit a partial span (rollback) and decode once more after the rewrite
+    n = 7
+    om.kv_rewrite(T, n)
+    ctx.kv_rewrite(i32([T]), i32([n]))
+    nxt = so.argmax_lowest(lf[n - 1])
+    ref = om.decode(nxt, T + n, True, thr, want_gate=True, want_mask=True)
+    to, lo, na, ga = gpu_decode(ctx, cfg, [nxt], [T + n], False)
+    check_decode_row(cfg, thr, ref, to[0], lo[0], na[0], ga[0], True)
+
+
+# ------------------------------------------------------------------ 8B-2L: batch 2, TP emulation
+@pytest.fixture(scope="module")
+def l2():
+    cfg = synth.LLAMA3_8B.with_layers(2)
+    return cfg, synth.host_weights(cfg)
+
+
+def oracle_script(cfg, wh, thr, prompt, n_decode, gamma, max_seq):
+    """The oracle's side of a teacher-forced session: prefill, n_decode sparse decode rows, one
+    verify of gamma rows, rewrite of 5 rows, one more sparse row."""
+    om = so.OracleModel(cfg, wh, max_seq=max_seq, max_gamma=GAMMA)
+    out = {"first": om.prefill_last(prompt), "dec": [], "toks": []}
+    T = len(prompt)
+    tok = so.argmax_lowest(out["first"])
+    for i in range(n_decode):
+        ref = om.decode(tok, T + i, True, thr, want_gate=True, want_mask=True)
+        out["dec"].append(ref)
+        out["toks"].append(tok)
+        tok = so.argmax_lowest(ref.logits)
+    T += n_decode
+    ins = [tok]
+    for i in range(gamma - 1):
+        ins.append(so.argmax_lowest(om.decode(ins[i], T + i, True, thr).logits))
+    out["ins"], out["T"] = ins, T
+    out["lf"] = om.verify(ins, T)
+    om.kv_rewrite(T, 5)
+    nxt = so.argmax_lowest(out["lf"][4])
+    out["after"] = om.decode(nxt, T + 5, True, thr, want_gate=True, want_mask=True)
+    out["nxt"] = nxt
+    return out
+
+
+def gpu_script(ctx, cfg, thr, prompts, refs, n_decode, gamma):
+    B = len(prompts)
+    first = torch.zeros(B, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(np.concatenate(prompts)), [len(p) for p in prompts], first)
+    torch.cuda.synchronize()
+    for b in range(B):
+        if margin(refs[b]["first"]) > 0.1:
+            assert int(first[b].item()) == so.argmax_lowest(refs[b]["first"])
+    T = [len(p) for p in prompts]
+    for i in range(n_decode):
+        to, lo, na, ga = gpu_decode(ctx, cfg, [r["toks"][i] for r in refs], [t + i for t in T], False)
+        for b in range(B):
+            check_decode_row(cfg, thr, refs[b]["dec"][i], to[b], lo[b], na[b], ga[b], True)
+    for b in range(B):
+        assert refs[b]["T"] == T[b] + n_decode
+    T = [r["T"] for r in refs]
+    for i in range(gamma - 1):  # drafts (teacher forced), all sequences in one step
+        gpu_decode(ctx, cfg, [r["ins"][i] for r in refs], [t + i for t in T], False)
+    j, nx, q, lo = gpu_correct(ctx, cfg, [r["ins"] for r in refs], T, 0.1)
+    for b in range(B):
+        check_correct(refs[b]["lf"], refs[b]["ins"], 0.1, j[b], nx[b], q[b], lo[b])
+    ctx.kv_rewrite(i32(T), i32([5] * B))
+    to, lo, na, ga = gpu_decode(ctx, cfg, [r["nxt"] for r in refs], [t + 5 for t in T], False)
+    for b in range(B):
+        check_decode_row(cfg, thr, refs[b]["after"], to[b], lo[b], na[b], ga[b], True)
+
+
+def test_8b2l_batch2_per_sequence_sets(l2):
+    from synth import gpu as sg
+    cfg, wh = l2
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 1, 33), synth.eval_prompt(cfg, 2, 70)]
+    refs = [oracle_script(cfg, wh, thr, p, 2, 8, 256) for p in prompts]
+    ctx = make_ctx(cfg, sg.device_weights(cfg), thr, 2, 256)
+    gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
+
+
+@pytest.mark.parametrize("tp", [2, 8])
+def test_8b2l_tensor_parallel_emulation(l2, tp):
+    """TP over `tp` ranks emulated on one GPU (sirius_init with tp_size > 1 and no NCCL comm):
+    every rank's shard runs through the same kernels, the O-proj / down-proj partials are summed
+    in rank order and the vocab-parallel head's argmax / softmax statistics are combined — the
+    outputs must match the TP 1 oracle."""
+    from synth import gpu as sg
+    cfg, wh = l2
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 3, 41)]
+    refs = [oracle_script(cfg, wh, thr, prompts[0], 2, GAMMA, 256)]
+    shards = [sg.device_weights(cfg, tp, r) for r in range(tp)]
+    ctx = make_ctx(cfg, shards, thr, 1, 256, tp=tp)
+    gpu_script(ctx, cfg, thr, prompts, refs, 2, GAMMA)

@@ -1,0 +1,80 @@
+"""Per-kernel summary of ncu --set full reports -> JSON (profiles/ncu_summary_<tag>.json).
+usage: ncu_summary.py <tag> <report.ncu-rep> [...]
+For each kernel name: launches captured, mean duration, DRAM bytes read+write per launch, DRAM
+throughput % of peak, achieved GB/s, SM / tensor-pipe utilisation where present."""
+import csv, io, json, subprocess, sys, collections
+
+METRICS = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
+    "lts__t_bytes.sum": "l2_bytes",
+    "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pct",
+    "launch__registers_per_thread": "regs",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
+}
+UNIT = {"duration": {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3, "ms": 1e-3},
+        "bytes": {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}}
+
+
+def short(name):
+    n = name.replace("(anonymous namespace)::", "").replace("sirius::", "").replace("void ", "")
+    return n.split("<")[0].split("(")[0]
+
+
+def rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    return r[0], r[1], r[2:]
+
+
+def main():
+    tag, reps = sys.argv[1], sys.argv[2:]
+    agg = collections.defaultdict(lambda: collections.defaultdict(list))
+    for rep in reps:
+        hdr, units, data = rows(rep)
+        ik = hdr.index("Kernel Name")
+        for d in data:
+            k = short(d[ik])
+            for m, key in METRICS.items():
+                if m not in hdr:
+                    continue
+                i = hdr.index(m)
+                try:
+                    v = float(d[i].replace(",", ""))
+                except ValueError:
+                    continue
+                u = units[i]
+                if key == "duration":
+                    v *= UNIT["duration"].get(u, 1e-9)
+                elif key in ("dram_read", "dram_write", "l2_bytes"):
+                    v *= UNIT["bytes"].get(u, 1)
+                agg[k][key].append(v)
+    out = {}
+    for k, m in agg.items():
+        mean = {key: sum(v) / len(v) for key, v in m.items()}
+        e = {"launches_captured": len(m.get("duration", [])), "avg_duration_us": mean.get("duration", 0) * 1e6,
+             "dram_bytes_per_launch": mean.get("dram_read", 0) + mean.get("dram_write", 0),
+             "dram_read_per_launch": mean.get("dram_read"), "dram_write_per_launch": mean.get("dram_write"),
+             "dram_pct_of_peak": mean.get("dram_pct"), "sm_pct": mean.get("sm_pct"),
+             "tensor_pct": mean.get("tensor_pct"), "regs": mean.get("regs"), "occupancy_pct": mean.get("occupancy_pct"),
+             "l2_bytes_per_launch": mean.get("l2_bytes")}
+        if mean.get("duration"):
+            e["dram_gbs"] = e["dram_bytes_per_launch"] / mean["duration"] / 1e9
+        out[k] = e
+    # the bench's dominant kernel is the fused CATS FFN
+    if "ffn_kernel" in out:
+        out["cats_ffn"] = out["ffn_kernel"]
+    json.dump({"tag": tag, "reports": reps, "kernels": out, **({"cats_ffn": out["cats_ffn"]} if "cats_ffn" in out else {})},
+              open(f"profiles/ncu_summary_{tag}.json", "w"), indent=1)
+    for k, e in out.items():
+        print(f"{k:28s} n={e['launches_captured']:3d} {e['avg_duration_us']:9.2f}us dram {e['dram_bytes_per_launch']/1e6:9.2f}MB "
+              f"{e.get('dram_gbs', 0):8.1f}GB/s dram% {e['dram_pct_of_peak']}")
+
+
+if __name__ == "__main__":
+    main()
