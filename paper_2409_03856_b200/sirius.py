@@ -55,9 +55,11 @@ def load():
     """Load libsirius.so (built in-tree by __graft_entry__.build()).  Raises if absent."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
-        lib = ctypes.CDLL(LIB_PATH)
+        # SIRIUS_LIB: another build of the same library (A/B timing of kernel variants; tools/)
+        path = os.environ.get("SIRIUS_LIB", LIB_PATH)
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        lib = ctypes.CDLL(path)
         P, I, U, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_float
         lib.sirius_init.argtypes = [ctypes.POINTER(SiriusConfig), ctypes.POINTER(SiriusWeights), P, P, P,
                                     ctypes.POINTER(P)]

@@ -64,7 +64,11 @@ def check_decode_row(cfg, thr, ref, tok_gpu, lg, na, ga, sparse):
     """One sequence's decode row against the oracle's: logits, a = SiLU(g), active set (every
     mismatch explained by the float error of a), count, argmax (pinned by the top-2 margin)."""
     eps = check_logits(lg, ref.logits)
-    bad = np.abs(ga - ref.gate) > 1e-3 + 1e-3 * np.abs(ref.gate)
+    # a = SiLU(g) is an fp32 activation: the north star's float tolerance applies.  At 8B shapes a
+    # few K/V cache elements round to the neighbouring bf16 value (fp32 vs fp64 producer, 1 bf16
+    # ulp = 2^-8 relative), which moves later activations by ~1e-3 (DESIGN.md §2, parity rules);
+    # the active set stays pinned by the explained-mismatch rule below.
+    bad = np.abs(ga - ref.gate) > ABS + REL * np.abs(ref.gate)
     assert not bad.any(), ("gate activations", np.argwhere(bad)[:8].tolist(), ga[bad][:8], ref.gate[bad][:8])
     if sparse:
         act = np.abs(ga) >= thr[:, None]
