@@ -49,6 +49,11 @@ SIRIUS_DEV uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+SIRIUS_DEV uint64_t policy_evict_unchanged() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 SIRIUS_DEV uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -73,6 +78,14 @@ SIRIUS_DEV uint4 ld_nc_v4(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+  return r;
+}
+// streamed weights read once per step: L2 lines marked evict-first on use
+SIRIUS_DEV uint4 ld_nc_v4_ef(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
   return r;
 }
 SIRIUS_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -159,6 +172,21 @@ SIRIUS_DEV void grid_barrier(unsigned long long* counter, unsigned nblocks) {
     unsigned long long target = (old / nblocks + 1) * nblocks;
     while (ld_acquire_u64(counter) < target) __nanosleep(20);
     __threadfence();
+  }
+  __syncthreads();
+}
+
+// Same contract as grid_barrier, one round trip cheaper: the arrival is a single release atomic
+// (cumulative over the CTA's writes ordered before it by bar.sync), the wait an acquire spin.
+SIRIUS_DEV void grid_sync(unsigned long long* counter, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long old, v;
+    asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(counter) : "memory");
+    const unsigned long long target = (old / nblocks + 1) * nblocks;
+    do {
+      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(counter) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }

@@ -74,4 +74,40 @@ struct AttnArgs {
   int* err;                // sticky device error word
 };
 
+// ---- persistent decode step (decode_step.cu): the whole TP-1 decode step in one cooperative launch
+struct StepArgs {
+  int d, L, Hr, KVr, hd, F, Vr, vocab, max_seq, splits;
+  float eps, attn_scale;
+  int dense;
+  const int32_t* tokens;  // [B]
+  const int32_t* pos;     // [B]
+  int32_t* token_out;     // [B]
+  float* logits_out;      // [B, Vr] or NULL
+  int32_t* n_active_out;  // [B, L] or NULL
+  float* gate_out;        // [B, L, F] or NULL: a = SiLU(g)
+  long long gate_stride;  // = L * F
+  const uint16_t *embed, *final_norm, *lm_head;
+  const uint16_t* const* attn_norm;  // device arrays [L] of device pointers
+  const uint16_t* const* w_qkv;
+  const uint16_t* const* w_o;
+  const uint16_t* const* ffn_norm;
+  const uint16_t* const* w_gate;
+  const uint16_t* const* w_up;
+  const uint16_t* const* w_down;
+  const float* thresholds;  // [L]
+  uint16_t *k_cache, *v_cache;  // layer 0; layer stride kv_layer elements
+  size_t kv_layer;
+  const float *rope_cos, *rope_sin;
+  // workspace
+  float *x, *x1, *qkv, *o, *attn_part, *ffn_part;
+  int* part_cnt;
+  unsigned* group_bar;
+  unsigned long long* grid_bar;  // dedicated monotone counter (nblocks = grid)
+  unsigned long long* amax;
+  unsigned* head_cnt;
+  int* err;
+  int tune;                   // bit 0: evict-first L2 policy on weight loads
+  unsigned long long* trace;  // debug: [events][grid] %globaltimer stamps (thread 0 of each CTA), or NULL
+};
+
 }  // namespace sirius

@@ -20,6 +20,7 @@
 // Numeric contract (D15): bf16 weights, fp32 activations and accumulation.
 #include "common.cuh"
 #include "decode_kernels.cuh"
+#include "gemv_dev.cuh"
 
 namespace sirius {
 namespace {
@@ -28,139 +29,8 @@ constexpr int kGemvWarps = 8;   // 2 CTAs per SM
 constexpr int kFfnWarps = 16;   // 1 CTA per SM (cooperative)
 constexpr int kFfnMaxN = 256;   // neurons per CTA
 constexpr int kFfnMaxChunks = kFfnMaxN / 32;
-
-// plane layout of an fp32 activation row of K elements: chunk c = 8 consecutive elements,
-// plane p = 0 holds elements 8c..8c+3, plane 1 holds 8c+4..8c+7 (float4 per chunk per plane)
-
-// Prologue: activation rows h[b, :] (plane layout) in shared memory; all NT threads participate.
-// Thread t owns the 4-element groups g = t + NT j (plane-aligned: a group is one float4 of a plane);
-// all of its global loads are issued before any is used (one memory round trip, not K / NT).
-constexpr int kMaxGroups = 8;  // K <= 32 * NT
-template <int B>
-SIRIUS_DEV void prologue(const Prologue& p, int K, float* h_s, float* red_s, bool store_res) {
-  const int tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarp = NT >> 5;
-  const int CH = K / 8, NG = K / 4;
-  float4* hp = reinterpret_cast<float4*>(h_s);
-  auto slot = [&](int b, int g) { return (b * 2 + (g & 1)) * CH + (g >> 1); };  // group g = elements 4g..4g+3
-  for (int b = 0; b < B; ++b) {
-    float4 x[kMaxGroups];
-    if (p.mode == IN_F32) {
-      const float4* src = reinterpret_cast<const float4*>(p.in_f32 + (size_t)b * K);
-#pragma unroll
-      for (int j = 0; j < kMaxGroups; ++j) {
-        const int g = tid + NT * j;
-        if (g < NG) x[j] = __ldcg(src + g);
-      }
-#pragma unroll
-      for (int j = 0; j < kMaxGroups; ++j) {
-        const int g = tid + NT * j;
-        if (g < NG) hp[slot(b, g)] = x[j];
-      }
-      continue;
-    }
-    if (p.mode == IN_EMBED) {
-      int tok = p.tokens[b];
-      tok = tok < 0 ? 0 : (tok >= p.vocab ? p.vocab - 1 : tok);
-      const uint2* erow = reinterpret_cast<const uint2*>(p.embed + (size_t)tok * K);
-#pragma unroll
-      for (int j = 0; j < kMaxGroups; ++j) {
-        const int g = tid + NT * j;
-        if (g < NG) {
-          const uint2 e = erow[g];
-          x[j] = make_float4(bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y));
-        }
-      }
-    } else {
-      const float4* base = reinterpret_cast<const float4*>(p.base + (size_t)b * K);
-      const float4* delta = p.delta ? reinterpret_cast<const float4*>(p.delta + (size_t)b * K) : nullptr;
-      float4 dl[kMaxGroups];
-#pragma unroll
-      for (int j = 0; j < kMaxGroups; ++j) {
-        const int g = tid + NT * j;
-        if (g < NG) {
-          x[j] = __ldcg(base + g);
-          dl[j] = delta ? __ldcg(delta + g) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kMaxGroups; ++j) {
-        x[j].x += dl[j].x; x[j].y += dl[j].y; x[j].z += dl[j].z; x[j].w += dl[j].w;
-      }
-    }
-    float ss = 0.f;
-#pragma unroll
-    for (int j = 0; j < kMaxGroups; ++j) {  // sum of squares, fixed order
-      const int g = tid + NT * j;
-      if (g < NG) {
-        ss = fmaf(x[j].x, x[j].x, ss); ss = fmaf(x[j].y, x[j].y, ss);
-        ss = fmaf(x[j].z, x[j].z, ss); ss = fmaf(x[j].w, x[j].w, ss);
-        if (store_res && p.res_out) reinterpret_cast<float4*>(p.res_out + (size_t)b * K)[g] = x[j];
-      }
-    }
-    uint2 wn[kMaxGroups];
-    const uint2* nw = reinterpret_cast<const uint2*>(p.norm_w);
-#pragma unroll
-    for (int j = 0; j < kMaxGroups; ++j) {
-      const int g = tid + NT * j;
-      if (g < NG) wn[j] = nw[g];
-    }
-    ss = warp_sum(ss);
-    if (lane == 0) red_s[warp] = ss;
-    __syncthreads();
-    float tot = 0.f;
-    for (int w = 0; w < nwarp; ++w) tot += red_s[w];
-    const float r = 1.0f / sqrtf(tot / (float)K + p.eps);
-#pragma unroll
-    for (int j = 0; j < kMaxGroups; ++j) {
-      const int g = tid + NT * j;
-      if (g < NG)
-        hp[slot(b, g)] = make_float4((x[j].x * r) * bf16_lo(wn[j].x), (x[j].y * r) * bf16_hi(wn[j].x),
-                                     (x[j].z * r) * bf16_lo(wn[j].y), (x[j].w * r) * bf16_hi(wn[j].y));
-    }
-    __syncthreads();  // red_s reuse
-  }
-  __syncthreads();
-}
-
-SIRIUS_DEV float dot8p(const uint4 w, const float4 x0, const float4 x1, float s) {
-  s = fmaf(bf16_lo(w.x), x0.x, s);
-  s = fmaf(bf16_hi(w.x), x0.y, s);
-  s = fmaf(bf16_lo(w.y), x0.z, s);
-  s = fmaf(bf16_hi(w.y), x0.w, s);
-  s = fmaf(bf16_lo(w.z), x1.x, s);
-  s = fmaf(bf16_hi(w.z), x1.y, s);
-  s = fmaf(bf16_lo(w.w), x1.z, s);
-  s = fmaf(bf16_hi(w.w), x1.w, s);
-  return s;
-}
-
-// Warp-cooperative dot of one bf16 row (global) with the B activation rows (planes in smem).
-// Lane l handles chunks l + 32 j; loads are issued in groups of U before use.  Result: lane sums
-// (not yet reduced across the warp).
-template <int B, int CPL>
-SIRIUS_DEV void row_dot(const uint16_t* __restrict__ wrow, const float4* __restrict__ hp, int CH, int lane,
-                        float* acc) {
-  constexpr int U = CPL < 16 ? CPL : 16;
-#pragma unroll
-  for (int b = 0; b < B; ++b) acc[b] = 0.f;
-#pragma unroll
-  for (int j0 = 0; j0 < CPL; j0 += U) {
-    uint4 wv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int c = lane + 32 * (j0 + u);
-      wv[u] = c < CH ? ld_nc_v4(wrow + (size_t)c * 8) : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int c = lane + 32 * (j0 + u);
-      if (c < CH) {
-#pragma unroll
-        for (int b = 0; b < B; ++b) acc[b] = dot8p(wv[u], hp[(b * 2) * CH + c], hp[(b * 2 + 1) * CH + c], acc[b]);
-      }
-    }
-  }
-}
+using dev::prologue;
+using dev::row_dot;
 
 // ===================================================================== dense GEMV
 template <int B, int CPL>
@@ -171,6 +41,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
   __shared__ unsigned flag_s;
   const int K = a.K, CH = K / 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t pol = policy_evict_first();  // weights: read once per step
   prologue<B>(a.pro, K, h_s, red_s, blockIdx.x == 0);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
   const int r0 = (int)((long long)a.rows * blockIdx.x / gridDim.x);
@@ -180,7 +51,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
   for (int b = 0; b < B; ++b) best[b] = 0ull;
   for (int row = r0 + warp; row < r1; row += kGemvWarps) {
     float acc[B];
-    row_dot<B, CPL>(a.W + (size_t)row * K, hp, CH, lane, acc);
+    row_dot<B, CPL>(a.W + (size_t)row * K, hp, CH, lane, acc, pol);
 #pragma unroll
     for (int b = 0; b < B; ++b) acc[b] = warp_sum(acc[b]);
     if (lane == 0) {
@@ -241,6 +112,7 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
   const int n0 = (int)((long long)a.F * cta / G), n1 = (int)((long long)a.F * (cta + 1) / G), nn = n1 - n0;
   const int nch = (nn + 31) / 32;
 
+  const uint64_t pol = policy_evict_first();
   prologue<B>(a.pro, d, h_s, red_s, cta == 0);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
   const float t = a.dense ? 0.f : *a.threshold;
@@ -248,7 +120,7 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
   // ---- A: dense gate rows: g = h2 . W_gate[n];  a = SiLU(g)
   for (int i = warp; i < nn; i += kFfnWarps) {
     float acc[B];
-    row_dot<B, CPL>(a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc);
+    row_dot<B, CPL>(a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc, pol);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float g = warp_sum(acc[b]);
@@ -296,7 +168,7 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
   for (int k = warp; k < nact; k += kFfnWarps) {
     const int i = list_s[k];
     float acc[B];
-    row_dot<B, CPL>(a.w_up + (size_t)(n0 + i) * d, hp, CH, lane, acc);
+    row_dot<B, CPL>(a.w_up + (size_t)(n0 + i) * d, hp, CH, lane, acc, pol);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float u = warp_sum(acc[b]);
@@ -320,7 +192,7 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
         const int ch = tid + NT * j;
-        wv[r][j] = (k < nact && ch < CH) ? ld_nc_v4(wrow + (size_t)ch * 8) : make_uint4(0u, 0u, 0u, 0u);
+        wv[r][j] = (k < nact && ch < CH) ? ld_nc_v4_ef(wrow + (size_t)ch * 8, pol) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
 #pragma unroll

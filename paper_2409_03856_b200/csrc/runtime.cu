@@ -26,6 +26,9 @@ int ffn_grid(int F, int num_sms);
 int attn_splits(int B, int KVr, int num_sms);
 cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st);
 cudaError_t attn_decode(const AttnArgs& a, int B, int hd, int group, cudaStream_t st);
+bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms);
+int decode_step_splits(int B, int KV, int num_sms);
+cudaError_t decode_step(const StepArgs& a, int B, int grid, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius
 
@@ -130,6 +133,15 @@ struct sirius_ctx {
   };
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
+  // persistent decode step (decode_step.cu): TP 1 on supported shapes, opt-in (SIRIUS_STEP_KERNEL=1);
+  // the default is the one-kernel-per-stage schedule (which TP > 1 needs between its all-reduces)
+  bool use_step = false;
+  int step_splits = 1;
+  const uint16_t** step_w = nullptr;  // device [7][L]: attn_norm, w_qkv, w_o, ffn_norm, w_gate, w_up, w_down
+  float *step_x = nullptr, *step_x1 = nullptr, *step_o = nullptr;
+  unsigned long long* step_bar = nullptr;
+  int step_tune = 1;                     // SIRIUS_STEP_TUNE (bit 0: evict-first weight loads)
+  unsigned long long* trace = nullptr;  // debug: decode-step phase stamps (sirius_debug_trace)
   // CUDA graphs: every ABI call is captured once per distinct argument set and replayed
   bool use_graphs = true;
   cudaStream_t cap_stream = nullptr;
@@ -166,7 +178,7 @@ sirius_status fail(sirius_ctx* c, sirius_status s, const std::string& msg) {
   } while (0)
 
 // ---- optional per-kernel timing: events recorded on the launch stream around selected launches
-enum ProfId { P_QKV = 0, P_ATTN = 1, P_OPROJ = 2, P_FFN = 3, P_HEAD = 4, P_VERIFY = 5, P_REWRITE = 6, P_NUM = 8 };
+enum ProfId { P_QKV = 0, P_ATTN = 1, P_OPROJ = 2, P_FFN = 3, P_HEAD = 4, P_VERIFY = 5, P_REWRITE = 6, P_STEP = 7, P_NUM = 8 };
 void prof_begin(sirius_ctx* c, int id) {
   if (!c->prof_on) return;
   if (c->prof_used == c->prof.size()) {
@@ -564,6 +576,27 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   }
   cudaMemcpy(c->dA_ptrs, dA_h.data(), sizeof(float*) * dA_h.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(c->dF_ptrs, dF_h.data(), sizeof(float*) * dF_h.size(), cudaMemcpyHostToDevice);
+  // persistent decode step (TP 1)
+  if (!emulate && cf.tp_size == 1 &&
+      launch::decode_step_supported(d, cf.n_heads, cf.n_kv_heads, hd, cf.ffn_dim, c->num_sms)) {
+    // opt-in: measured at parity / slightly slower than the per-stage kernels on the 8B step
+    // (2.90-2.93 vs 2.86-2.89 ms), so the per-stage schedule stays the default
+    const char* e = getenv("SIRIUS_STEP_KERNEL");
+    c->use_step = e && atoi(e) != 0;
+    if (const char* t = getenv("SIRIUS_STEP_TUNE")) c->step_tune = atoi(t);
+  }
+  if (c->use_step) {
+    RankState& R = c->ranks[0];
+    if (alloc(c, &c->step_w, (size_t)7 * L) || alloc(c, &c->step_x, (size_t)B * d) ||
+        alloc(c, &c->step_x1, (size_t)B * d) || alloc(c, &c->step_o, (size_t)B * c->Hr * hd) ||
+        alloc(c, &c->step_bar, 1))
+      return cleanup_fail(SIRIUS_ERR_CUDA);
+    std::vector<const uint16_t*> wp;
+    for (auto* v : {&R.attn_norm, &R.w_qkv, &R.w_o, &R.ffn_norm, &R.w_gate, &R.w_up, &R.w_down})
+      wp.insert(wp.end(), v->begin(), v->end());
+    cudaMemcpy(c->step_w, wp.data(), sizeof(const uint16_t*) * wp.size(), cudaMemcpyHostToDevice);
+    c->step_splits = launch::decode_step_splits(B, c->KVr, c->num_sms);
+  }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess)
     return cleanup_fail(SIRIUS_ERR_CUDA);
   *out = c;
@@ -650,6 +683,65 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
   const int B = cf.batch, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   const bool dense = flags & SIRIUS_DENSE;
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
+  if (c->use_step) {  // the whole step in one persistent launch (decode_step.cu)
+    RankState& R = c->ranks[0];
+    StepArgs s = {};
+    s.d = d;
+    s.L = L;
+    s.Hr = c->Hr;
+    s.KVr = c->KVr;
+    s.hd = hd;
+    s.F = c->Fr;
+    s.Vr = c->Vr;
+    s.vocab = cf.vocab;
+    s.max_seq = cf.max_seq;
+    s.splits = c->step_splits;
+    s.eps = cf.rms_eps;
+    s.attn_scale = 1.0f / sqrtf((float)hd);
+    s.dense = dense ? 1 : 0;
+    s.tokens = token_in;
+    s.pos = pos;
+    s.token_out = token_out;
+    s.logits_out = logits_out;
+    s.n_active_out = n_active_out;
+    s.gate_out = gate_act_out;
+    s.gate_stride = (long long)L * c->Fr;
+    s.embed = R.embed;
+    s.final_norm = R.final_norm;
+    s.lm_head = R.lm_head;
+    s.attn_norm = c->step_w + 0 * L;
+    s.w_qkv = c->step_w + 1 * L;
+    s.w_o = c->step_w + 2 * L;
+    s.ffn_norm = c->step_w + 3 * L;
+    s.w_gate = c->step_w + 4 * L;
+    s.w_up = c->step_w + 5 * L;
+    s.w_down = c->step_w + 6 * L;
+    s.thresholds = c->thresholds;
+    s.k_cache = R.k_cache;
+    s.v_cache = R.v_cache;
+    s.kv_layer = (size_t)B * c->KVr * cf.max_seq * hd;
+    s.rope_cos = c->rope_cos;
+    s.rope_sin = c->rope_sin;
+    s.x = c->step_x;
+    s.x1 = c->step_x1;
+    s.qkv = R.qkv;
+    s.o = c->step_o;
+    s.attn_part = R.attn_part;
+    s.ffn_part = R.ffn_part;
+    s.part_cnt = R.ffn_cnt;
+    s.group_bar = R.attn_bar;
+    s.grid_bar = c->step_bar;
+    s.amax = c->amax;
+    s.head_cnt = R.head_cnt;
+    s.err = c->err_dev;
+    s.trace = c->trace;
+    s.tune = c->step_tune;
+    prof_begin(c, P_STEP);
+    LCU(launch::decode_step(s, B, c->num_sms, c->stream));
+    prof_end(c);
+    CU(cudaGetLastError());
+    return SIRIUS_OK;
+  }
   const int ffn_grid = launch::ffn_grid(c->Fr, c->num_sms);
   for (int l = 0; l < L; ++l) {
     for (auto& R : c->ranks) {
@@ -935,6 +1027,14 @@ int sirius_nccl_comm_destroy(void* comm) {
 unsigned long long sirius_debug_launches(const sirius_ctx* c) { return c ? c->launches : 0ull; }
 // CUDA-graph replay of the ABI calls on (default) / off (every kernel launched from the host).
 // on = -1: query only.  Returns the (new) state: 1 = graphs in use.
+// Debug: per-phase %globaltimer stamps of the persistent decode step into buf (DEV, u64
+// [events][num_sms], events = 10 L + 3), or buf = NULL to stop.  Returns 1 if the step kernel is used.
+int sirius_debug_trace(sirius_ctx* c, void* buf) {
+  if (!c) return -1;
+  c->trace = static_cast<unsigned long long*>(buf);
+  return c->use_step ? 1 : 0;
+}
+
 int sirius_debug_graphs(sirius_ctx* c, int on) {
   if (!c) return -1;
   if (on >= 0) c->use_graphs = on != 0;

@@ -83,6 +83,8 @@ def load():
         lib.sirius_debug_buffer.restype = I
         lib.sirius_debug_launches.argtypes = [P]
         lib.sirius_debug_launches.restype = ctypes.c_ulonglong
+        lib.sirius_debug_trace.argtypes = [P, P]
+        lib.sirius_debug_trace.restype = I
         lib.sirius_debug_graphs.argtypes = [P, I]
         lib.sirius_debug_graphs.restype = I
         lib.sirius_debug_profile.argtypes = [P, I]
@@ -171,7 +173,8 @@ class Sirius:
         self._check(self.lib.kv_rewrite(self.h, _ptr(start_pos), _ptr(n_rows)))
 
     # ---- instrumentation (bench / tests) ------------------------------------------------
-    PROF_NAMES = ("qkv_gemv", "attn_decode", "oproj_gemv", "cats_ffn", "lm_head", "correct_kernel", "kv_rewrite")
+    PROF_NAMES = ("qkv_gemv", "attn_decode", "oproj_gemv", "cats_ffn", "lm_head", "correct_kernel", "kv_rewrite",
+                  "decode_step")
 
     def launches(self) -> int:
         """Kernels this context has launched so far (library-side counter)."""

@@ -116,7 +116,14 @@ def l1():
     return cfg, synth.host_weights(cfg), sg.device_weights(cfg)
 
 
-def test_8b_long_context_decode_verify_rewrite(l1):
+@pytest.fixture(params=["per_stage", "step_kernel"])
+def schedule(request, monkeypatch):
+    """Decode schedule: one kernel per stage (default) or the persistent step kernel (opt-in)."""
+    monkeypatch.setenv("SIRIUS_STEP_KERNEL", "1" if request.param == "step_kernel" else "0")
+    return request.param
+
+
+def test_8b_long_context_decode_verify_rewrite(l1, schedule):
     cfg, wh, wd = l1
     thr = synth.layer_thresholds(cfg, 0.5)
     P, max_seq = 1230, 1400
@@ -217,7 +224,7 @@ def gpu_script(ctx, cfg, thr, prompts, refs, n_decode, gamma):
         check_decode_row(cfg, thr, refs[b]["after"], to[b], lo[b], na[b], ga[b], True)
 
 
-def test_8b2l_batch2_per_sequence_sets(l2):
+def test_8b2l_batch2_per_sequence_sets(l2, schedule):
     from synth import gpu as sg
     cfg, wh = l2
     thr = synth.layer_thresholds(cfg, 0.5)

@@ -49,7 +49,14 @@ def test_weights_on_device_equal_host(tiny_models):
         np.testing.assert_array_equal(wd[k].view(torch.int16).cpu().numpy().view(np.uint16).reshape(wh[k].shape), wh[k])
 
 
-def test_prefill_and_decode_lockstep(tiny_models):
+@pytest.fixture(params=["per_stage", "step_kernel"])
+def schedule(request, monkeypatch):
+    """Decode schedule: one kernel per stage (default) or the persistent step kernel (opt-in)."""
+    monkeypatch.setenv("SIRIUS_STEP_KERNEL", "1" if request.param == "step_kernel" else "0")
+    return request.param
+
+
+def test_prefill_and_decode_lockstep(tiny_models, schedule):
     """Teacher-forced: the GPU and the oracle decode the same tokens; compare logits, gate
     activations, active sets and argmax every step, sparse and dense."""
     from paper_2409_03856_b200 import sirius as S
@@ -155,7 +162,7 @@ def test_verify_accept_rewrite_lockstep(tiny_models):
 
 
 @pytest.mark.parametrize("gamma,r,mode", [(4, 0.1, 0), (4, 0.3, 0), (6, 0.0, 1), (5, 0.6, 0), (8, 0.9, 0)])
-def test_generate_token_exact(tiny_models, gamma, r, mode):
+def test_generate_token_exact(tiny_models, gamma, r, mode, schedule):
     """Free-running Sirius generation: identical tokens and accept decisions to the oracle."""
     from paper_2409_03856_b200 import driver
     cfg, wh, wd = tiny_models
