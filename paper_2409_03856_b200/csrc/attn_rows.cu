@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
   float* l_s = m_s + kRows;
   float* c_s = l_s + kRows;
 
+  pdl_trigger();
+  pdl_wait();
   const int split = blockIdx.x, bz = blockIdx.z, b = a.b_base + bz;
   const int kvh = blockIdx.y % a.KVr, rb = blockIdx.y / a.KVr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -261,11 +263,19 @@ cudaError_t launch_hd(const AttnRowsArgs& a, dim3 grid, float scale, cudaStream_
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
+  // The per-group split barrier needs the S splits of a group co-resident: the grid is one wave
+  // (attn_rows_splits); with PDL the predecessor's CTAs finish without waiting on this grid and the
+  // successor launches only after every CTA of this grid has triggered (is resident).
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the per-group barrier
-  attr[0].val.cooperative = 1;
+  if (launch::g_chain_pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = grid.x > 1 ? 1 : 0;  // S == 1: no barrier partner, plain launch
+  cfg.numAttrs = (launch::g_chain_pdl || grid.x > 1) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, attn_rows_kernel<HD>, a, scale);
 }
 

@@ -69,8 +69,30 @@ SIRIUS_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint6
 }
 
 // ------------------------------------------------------------------ PDL (programmatic dependent launch)
+// Kernels of the verify / prefill chain call pdl_trigger() then pdl_wait() before touching anything a
+// predecessor writes (both are no-ops when a kernel is launched without the PDL attribute).
 SIRIUS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 SIRIUS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+namespace launch {
+extern bool g_chain_pdl;  // verify / prefill chain launched with PDL (runtime.cu; SIRIUS_VERIFY_PDL)
+// <<<grid, block, smem, st>>> with the programmatic-stream-serialization attribute when g_chain_pdl
+template <class... KArgs, class... Args>
+inline cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_chain_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+}  // namespace launch
 
 // ------------------------------------------------------------------ loads
 SIRIUS_DEV uint4 ld_nc_v4(const void* p) {

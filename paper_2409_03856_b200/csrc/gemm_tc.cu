@@ -138,6 +138,37 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((128u >> 4) << 24);
   const uint32_t tx_bytes = NACC * A_BYTES + NB * b_bytes;
 
+  // PDL: the weight (A) tiles of the first stages do not depend on the predecessor kernel; request
+  // them before the dependency wait, the activation (B) tiles after it.
+  pdl_trigger();
+  int npre = 0;
+  {
+    const long long wend0 = min(w1, (w0 / g.kb + 1) * g.kb);
+    npre = (int)min((long long)stages, wend0 - w0);
+  }
+  if (warp == 0 && lane == 0) {
+    const uint64_t pol_w = policy_evict_first();
+    for (int i = 0; i < npre; ++i) {
+      uint8_t* st = smem + (size_t)i * stage_bytes;
+      mbar_arrive_expect_tx(&full[i], tx_bytes);
+      const int t = (int)(w0 / g.kb), kc = (int)((w0 % g.kb) + i) * 64;
+      tma_load_2d(st, &tmA0, kc, t * 128, &full[i], pol_w);
+      if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[i], pol_w);
+    }
+  }
+  pdl_wait();
+  if (warp == 0 && lane == 0) {
+    const uint64_t pol_x = policy_evict_last();
+    for (int i = 0; i < npre; ++i) {
+      uint8_t* st = smem + (size_t)i * stage_bytes;
+      const int kc = (int)((w0 % g.kb) + i) * 64;
+      for (int r = 0; r < MP / 16; ++r) {
+        tma_load_2d(st + NACC * A_BYTES + r * 2048, &tmB, kc, r * 16, &full[i], pol_x);
+        if (has_lo) tma_load_2d(st + NACC * A_BYTES + b_bytes + r * 2048, &tmBlo, kc, r * 16, &full[i], pol_x);
+      }
+    }
+  }
+
   long long it = 0;  // global k-iteration counter: stage = it % stages, parity = (it / stages) & 1
   int sidx = 0;
   for (long long w = w0; w < w1; ++sidx) {
@@ -149,6 +180,7 @@ __global__ void __launch_bounds__(128, 1)
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
       for (int i = 0; i < nk; ++i) {
         const long long q = it + i;
+        if (q < npre) continue;  // requested before the dependency wait
         const int s = (int)(q % stages);
         mbar_wait(&empty[s], ((uint32_t)(q / stages) & 1u) ^ 1u);
         uint8_t* st = smem + (size_t)s * stage_bytes;
@@ -301,11 +333,13 @@ cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void
   if (dual) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    gemm_tc_kernel<true><<<grid, 128, smem, st>>>(*a0, *a1, *b, *blo, g, MP, stages, has_lo);
+    return launch_chain(gemm_tc_kernel<true>, dim3(grid), dim3(128), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
+                        has_lo);
   } else {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    gemm_tc_kernel<false><<<grid, 128, smem, st>>>(*a0, *a1, *b, *blo, g, MP, stages, has_lo);
+    return launch_chain(gemm_tc_kernel<false>, dim3(grid), dim3(128), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
+                        has_lo);
   }
   return cudaGetLastError();
 }

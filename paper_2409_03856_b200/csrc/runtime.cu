@@ -465,6 +465,8 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     return s;
   }
   c->attn_splits = launch::attn_splits(cf.batch, c->KVr, c->num_sms);  // ~one wave of split CTAs
+  // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
+  if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
   auto cleanup_fail = [&](sirius_status s) {
     sirius_destroy(c);
     return s;

@@ -16,6 +16,8 @@ namespace sirius {
 
 // ===================================================================== norm rows
 __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
+  pdl_trigger();
+  pdl_wait();
   // thread t owns 4-element groups g = t + 256 j; every global load is issued before use
   constexpr int MG = 8;  // d <= 8192
   const int m = blockIdx.x, tid = threadIdx.x, d = a.d, NG = d / 4;
@@ -90,6 +92,8 @@ __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
 
 // ===================================================================== RoPE + K/V store
 __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x, tid = threadIdx.x, hd = a.hd, half = hd / 2;
   const int b = a.b_base + m / a.rows_per_seq, i = m % a.rows_per_seq;
   const int pos = a.start[b] + i;
@@ -161,6 +165,8 @@ __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
 
 // ===================================================================== acceptance
 __global__ void __launch_bounds__(256) accept_stats_kernel(AcceptStatsArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x, split = blockIdx.y, S = gridDim.y, tid = threadIdx.x;
   const int b = m / a.gamma, i = m % a.gamma;
   const int draft = (i < a.gamma - 1) ? a.tokens[b * a.gamma + i + 1] : -1;
@@ -211,6 +217,7 @@ __global__ void __launch_bounds__(256) accept_stats_kernel(AcceptStatsArgs a) {
 
 // one CTA per sequence; thread i = verify row i (gamma <= 64)
 __global__ void __launch_bounds__(64) accept_finalize_kernel(AcceptFinalArgs a) {
+  pdl_wait();
   const int b = blockIdx.x, i = threadIdx.x, gam = a.gamma;
   __shared__ float q_s[64];
   __shared__ int am_s[64];
@@ -301,20 +308,27 @@ __global__ void sum_ranks_kernel(float* const* bufs, int nranks, size_t n, size_
 
 namespace launch {
 
+bool g_chain_pdl = true;
+#define LAUNCH_CHECK(x)                 \
+  do {                                  \
+    const cudaError_t e_ = (x);         \
+    if (e_ != cudaSuccess) return e_;   \
+  } while (0)
+
 cudaError_t norm_rows(const NormRowsArgs& a, int M, cudaStream_t st) {
-  norm_rows_kernel<<<M, 256, 0, st>>>(a);
+  LAUNCH_CHECK(launch_chain(norm_rows_kernel, dim3(M), dim3(256), 0, st, a));
   return cudaGetLastError();
 }
 cudaError_t rope_store(const RopeStoreArgs& a, int M, cudaStream_t st) {
-  rope_store_kernel<<<M, 128, 0, st>>>(a);
+  LAUNCH_CHECK(launch_chain(rope_store_kernel, dim3(M), dim3(128), 0, st, a));
   return cudaGetLastError();
 }
 cudaError_t accept_stats(const AcceptStatsArgs& a, int splits, cudaStream_t st) {
-  accept_stats_kernel<<<dim3(a.M, splits), 256, 0, st>>>(a);
+  LAUNCH_CHECK(launch_chain(accept_stats_kernel, dim3(a.M, splits), dim3(256), 0, st, a));
   return cudaGetLastError();
 }
 cudaError_t accept_finalize(const AcceptFinalArgs& a, int B, cudaStream_t st) {
-  accept_finalize_kernel<<<B, 64, 0, st>>>(a);
+  LAUNCH_CHECK(launch_chain(accept_finalize_kernel, dim3(B), dim3(64), 0, st, a));
   return cudaGetLastError();
 }
 cudaError_t kv_rewrite(const KvRewriteArgs& a, int L, cudaStream_t st) {
