@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--gamma", type=int, default=16)
     ap.add_argument("--r", type=float, default=0.1)
     ap.add_argument("--rho", type=float, default=0.5)
+    ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1, 2, 4, 8)")
     ap.add_argument("--baseline-tokens", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -58,15 +59,15 @@ def peaks():
 
 
 # ---------------------------------------------------------------- algorithmic bytes
-def step_bytes(cfg, tp, ctx_len, rho_layers=None):
-    """Bytes the method must move for one decode row per rank: weights (dense or CATS-sparse
-    FFN) + KV-cache read of ctx_len positions + the head.  rho_layers: measured active fraction
-    per layer (None = dense)."""
+def step_bytes(cfg, tp, ctx_len, rho_layers=None, batch=1):
+    """Bytes the method must move for one decode step of `batch` sequences per rank: weights (dense,
+    or CATS-sparse FFN with rho_layers = the active fraction per layer, the union over the batch
+    for batch > 1) read once + each sequence's KV-cache read of ctx_len positions + the head."""
     d, F, L, hd = cfg.d_model, cfg.ffn_dim // tp, cfg.n_layers, cfg.head_dim
     qkv = cfg.qkv_rows // tp * d * 2
     wo = d * (cfg.n_heads // tp * hd) * 2
     gate = F * d * 2
-    kv = 2 * (cfg.n_kv_heads // tp) * hd * 2 * ctx_len
+    kv = batch * 2 * (cfg.n_kv_heads // tp) * hd * 2 * ctx_len
     tot = 0.0
     for l in range(L):
         rho = 1.0 if rho_layers is None else float(rho_layers[l])
@@ -75,11 +76,11 @@ def step_bytes(cfg, tp, ctx_len, rho_layers=None):
     return tot
 
 
-def verify_bytes(cfg, tp, T, gamma):
+def verify_bytes(cfg, tp, T, gamma, batch=1):
     d, F, L, hd = cfg.d_model, cfg.ffn_dim // tp, cfg.n_layers, cfg.head_dim
     w = L * (cfg.qkv_rows // tp * d + d * cfg.n_heads // tp * hd + 3 * F * d) * 2 + cfg.vocab // tp * d * 2
     kvrow = 2 * (cfg.n_kv_heads // tp) * hd * 2 * L
-    return w + T * kvrow + gamma * kvrow + gamma * cfg.vocab // tp * 4
+    return w + batch * (T * kvrow + gamma * kvrow + gamma * cfg.vocab // tp * 4)
 
 
 # ---------------------------------------------------------------- clocks sampler
@@ -207,10 +208,11 @@ def main():
         comm = TP.nccl_bootstrap(S.load(), tp, rank)
     n_gen_max = (a.warmup + 2 * a.steps + 2) * a.gamma + a.baseline_tokens + 64
     max_seq = a.prompt + n_gen_max + 2 * a.gamma
-    ctx = S.Sirius(cfg, weights, thr, batch=1, max_seq=max_seq, max_gamma=a.gamma, tp_size=tp, tp_rank=rank,
+    B = a.batch
+    ctx = S.Sirius(cfg, weights, thr, batch=B, max_seq=max_seq, max_gamma=a.gamma, tp_size=tp, tp_rank=rank,
                    nccl_comm=comm)
     drv = driver.Driver(ctx)
-    prompt = synth.eval_prompt(cfg, 0, a.prompt)
+    prompts = [synth.eval_prompt(cfg, b, a.prompt) for b in range(B)]
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 
@@ -218,7 +220,7 @@ def main():
 
     stream = torch.cuda.current_stream()
     # ---------------- Sirius: W warm-up kernels, then K timed kernels
-    drv.begin([prompt])
+    drv.begin(prompts)
     for _ in range(a.warmup):
         drv.step(a.gamma, a.r)
     clocks = Clocks(local)
@@ -230,9 +232,8 @@ def main():
     h2d0, d2h0 = drv.h2d_bytes, drv.d2h_bytes
     wall0 = time.perf_counter()
     ev0.record(stream)
-    committed = 0
     for _ in range(a.steps):
-        committed += drv.step(a.gamma, a.r)
+        drv.step(a.gamma, a.r)
     ev1.record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -243,9 +244,12 @@ def main():
     wall_ms = max_over_ranks(wall * 1e3)
     h2d = (drv.h2d_bytes - h2d0) / a.steps
     d2h = (drv.d2h_bytes - d2h0) / a.steps
-    advances = [int(k.j[0]) + 1 for k in drv.log[a.warmup:a.warmup + a.steps]]
+    timed = drv.log[a.warmup:a.warmup + a.steps]
+    advances = [[int(x) + 1 for x in k.j] for k in timed]  # [kernel][sequence]
+    committed_total = sum(sum(v) for v in advances)
+    committed = committed_total / B  # per sequence
     aal = committed / a.steps
-    sirius_ms_tok = t_ms / committed
+    sirius_ms_tok = t_ms / committed  # per-sequence latency per committed token
     # ---------------- roofline pass: per-kernel CUDA events over K more kernels
     ctx.profile(True)
     for _ in range(a.steps):
@@ -254,59 +258,90 @@ def main():
     ctx.profile(False)
     T_now = drv.T[0]
     drv.flush()
-    # measured CATS density per layer (sparse steps with n_active export)
-    L = cfg.n_layers
-    na = torch.zeros((1, L), dtype=torch.int32, device="cuda")
-    tok = torch.zeros(2, dtype=torch.int32, device="cuda")
-    tok[0] = drv.pending[0]
-    dens = []
+    # measured CATS density per layer (sparse steps with gate-activation export): per sequence and
+    # the union over the batch (the rows a batched step must load, reading D19)
+    L, Fr_ = cfg.n_layers, cfg.ffn_dim // tp
+    tok = torch.tensor(drv.pending, dtype=torch.int32, device="cuda")
+    tok2 = torch.zeros(B, dtype=torch.int32, device="cuda")
+    ga = torch.zeros((B, L, Fr_), dtype=torch.float32, device="cuda")
+    thr_np = np.asarray(thr, dtype=np.float32)[None, :, None]
+    dens, union = [], []
     for i in range(8):
-        p = torch.tensor([T_now + i], dtype=torch.int32, device="cuda")
-        ctx.sparse_decode_step(tok[0:1], p, 0, tok[1:2], None, na)
-        tok[0:1].copy_(tok[1:2])
-        dens.append(na.cpu().numpy()[0] / (cfg.ffn_dim // tp))
+        p = torch.tensor([t + i for t in drv.T], dtype=torch.int32, device="cuda")
+        ctx.sparse_decode_step(tok, p, 0, tok2, None, None, ga)
+        tok.copy_(tok2)
+        act = np.abs(ga.cpu().numpy()) >= thr_np  # [B, L, F]
+        dens.append(act.mean(axis=2).mean(axis=0))
+        union.append(act.any(axis=0).mean(axis=1))
     rho_layers = np.mean(np.array(dens), axis=0)
+    rho_union = np.mean(np.array(union), axis=0)
     # ---------------- dense and CS-only baselines (same library, same context)
     n_b = a.baseline_tokens
-    T0 = [T_now + 8]
+    T0 = [t + 8 for t in drv.T]
     base = {}
     for name, dense in (("dense", True), ("cs_only", False)):
-        drv.greedy_run([drv.pending[0]], T0, a.gamma, dense)  # warm-up: captures the chunk's graphs
+        drv.greedy_run(drv.pending, T0, a.gamma, dense)  # warm-up: captures the chunk's graphs
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        drv.greedy_run([drv.pending[0]], T0, n_b, dense)
+        drv.greedy_run(drv.pending, T0, n_b, dense)
         e1.record(stream)
         torch.cuda.synchronize()
         base[name] = max_over_ranks(e0.elapsed_time(e1)) / n_b
-    # ---------------- roofline of the dominant kernel (CATS FFN)
+    # ---------------- roofline of the dominant kernel: the persistent decode step (TP 1), else the CATS FFN
     pk = peaks()
-    ffn_ms, ffn_n = prof["cats_ffn"]
     d, Fr = cfg.d_model, cfg.ffn_dim // tp
     rho_mean = float(np.mean(rho_layers))
-    ffn_bytes = Fr * d * 2 + 2 * rho_mean * Fr * d * 2  # dense gate + active up/down rows (per launch)
-    ffn_avg_s = ffn_ms / max(ffn_n, 1) / 1e3
-    achieved = ffn_bytes / ffn_avg_s / 1e9
+    rho_union_mean = float(np.mean(rho_union))
     traffic = None
+    summ = {}
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")))["cats_ffn"]["dram_bytes_per_launch"]
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")))
     except Exception:
         pass
-    roof = {"bound": "hbm", "kernel": "ffn_fused_kernel (CATS gate+SiLU+threshold+ballot, active up/down gathers)",
-            "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-            "traffic": traffic, "algorithmic_bytes_per_launch": ffn_bytes, "avg_launch_us": ffn_avg_s * 1e6,
-            "launches_timed": ffn_n, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback"}
+    if prof.get("decode_step", (0.0, 0))[1] > 0:
+        st_ms, st_n = prof["decode_step"]
+        # algorithmic bytes of one CATS-sparse step at the mean context of the timed kernels
+        ctx_mid = T_now - a.steps * a.gamma / 2
+        st_bytes = step_bytes(cfg, tp, ctx_mid, rho_union, B)
+        avg_s = st_ms / st_n / 1e3
+        achieved = st_bytes / avg_s / 1e9
+        try:
+            traffic = summ["kernels"]["decode_step_kernel"]["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": "decode_step_kernel (persistent CATS-sparse decode step: QKV, attention, "
+                "O-proj, gate+SiLU+threshold+ballot, active up/down gathers, head+argmax)",
+                "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                "traffic": traffic, "algorithmic_bytes_per_launch": st_bytes, "avg_launch_us": avg_s * 1e6,
+                "launches_timed": st_n,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback (B200_PROFILING.md)"}
+    else:
+        ffn_ms, ffn_n = prof["cats_ffn"]
+        ffn_bytes = Fr * d * 2 + 2 * rho_union_mean * Fr * d * 2  # dense gate + active (union) up/down rows
+        ffn_avg_s = ffn_ms / max(ffn_n, 1) / 1e3
+        achieved = ffn_bytes / ffn_avg_s / 1e9
+        try:
+            traffic = summ["cats_ffn"]["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": "ffn_kernel (CATS gate+SiLU+threshold+ballot, active up/down gathers)",
+                "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                "traffic": traffic, "algorithmic_bytes_per_launch": ffn_bytes, "avg_launch_us": ffn_avg_s * 1e6,
+                "launches_timed": ffn_n,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback (B200_PROFILING.md)"}
     # whole-step HBM GB/s for each mode (algorithmic bytes / time)
     ctxlen = T_now
-    gbs = {"dense": step_bytes(cfg, tp, ctxlen) / (base["dense"] / 1e3) / 1e9,
-           "cs_only": step_bytes(cfg, tp, ctxlen, rho_layers) / (base["cs_only"] / 1e3) / 1e9}
-    kernel_bytes = (a.gamma - 1) * step_bytes(cfg, tp, ctxlen, rho_layers) + verify_bytes(cfg, tp, ctxlen, a.gamma)
+    gbs = {"dense": step_bytes(cfg, tp, ctxlen, None, B) / (base["dense"] / 1e3) / 1e9,
+           "cs_only": step_bytes(cfg, tp, ctxlen, rho_union, B) / (base["cs_only"] / 1e3) / 1e9}
+    kernel_bytes = ((a.gamma - 1) * step_bytes(cfg, tp, ctxlen, rho_union, B)
+                    + verify_bytes(cfg, tp, ctxlen, a.gamma, B))
     gbs["sirius"] = kernel_bytes / (t_ms / a.steps / 1e3) / 1e9
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items()}
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and B == 1 and not a.no_cpu_baseline:
         s = cpu_oracle_sample(cfg, a.gamma, a.r, a.rho)
         kernel_s = (a.gamma - 1) * s["row_sparse_s"] + a.gamma * s["row_dense_s"]
         cpu = {"value": kernel_s / aal * 1e3, "unit": "ms/token", "cores": s["threads"], "kind": "oracle",
@@ -320,16 +355,20 @@ def main():
             "value": sirius_ms_tok, "unit": "ms/token", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": t_ms / a.steps, "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "model": a.model, "batch": 1, "prompt": a.prompt, "gamma": a.gamma,
+            "config": {"workload": WORKLOAD if B == 1 else WORKLOAD.replace("batch 1", f"batch {B}"), "model": a.model,
+                       "batch": B, "prompt": a.prompt, "gamma": a.gamma,
                        "r": a.r, "rho_target": a.rho, "parallelism": f"tp{world}",
                        "l2": "weights (15 GB) >> 126 MB L2: every step streams from HBM, no flush needed"},
-            "sirius": {"ms_per_token": sirius_ms_tok, "aal": aal, "advances": advances,
-                       "tokens_per_s": 1e3 / sirius_ms_tok, "hbm_gbs_algorithmic": gbs["sirius"]},
+            "sirius": {"ms_per_token": sirius_ms_tok, "aal": aal,
+                       "advances": advances if B > 1 else [v[0] for v in advances],
+                       "tokens_per_s": 1e3 / sirius_ms_tok, "tokens_per_s_aggregate": B * 1e3 / sirius_ms_tok,
+                       "hbm_gbs_algorithmic": gbs["sirius"]},
             "dense": {"ms_per_token": base["dense"], "tokens_per_s": 1e3 / base["dense"], "hbm_gbs": gbs["dense"],
                       "frac_of_measured_hbm": gbs["dense"] / pk["hbm_gbs"]},
             "cs_only": {"ms_per_token": base["cs_only"], "tokens_per_s": 1e3 / base["cs_only"],
                         "hbm_gbs": gbs["cs_only"], "frac_of_measured_hbm": gbs["cs_only"] / pk["hbm_gbs"],
-                        "density_per_layer_mean": rho_mean},
+                        "density_per_layer_mean": rho_mean, "density_union_over_batch": rho_union_mean,
+                        "tokens_per_s_aggregate": B * 1e3 / base["cs_only"]},
             "sirius_vs_dense": sirius_ms_tok / base["dense"],
             "roofline": roof, "per_kernel_device_ms": per_kernel,
             "cpu_baseline": cpu,

@@ -64,7 +64,8 @@ typedef enum {
 typedef struct {
   int32_t vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn_dim;
   float rope_theta, rms_eps;
-  int32_t batch;     /* number of sequences (slots 0..batch-1), fixed for the context's life     */
+  int32_t batch;     /* number of sequences (slots 0..batch-1), fixed for the context's life;
+                        one of 1, 2, 4, 8 (else SIRIUS_ERR_UNSUPPORTED); batch * max_gamma <= 256     */
   int32_t max_seq;   /* KV capacity per sequence (>= prompt + generated + max_gamma)              */
   int32_t max_gamma; /* max verify rows per sequence per correct_kernel call (<= 64)              */
   int32_t tp_size, tp_rank; /* n_heads, n_kv_heads, ffn_dim, vocab divisible by tp_size          */

@@ -20,6 +20,17 @@ namespace {
 
 constexpr int kRows = 64, kKB = 64, kThreads = 256;
 
+SIRIUS_DEV void rstamp(const AttnRowsArgs& a, int slot) {  // debug phase stamps (a.trace != NULL)
+  if (!a.trace) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    a.trace[(size_t)slot * gridDim.x * gridDim.y * gridDim.z + cta] = t;
+  }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, float scale) {
   constexpr int KROW = HD + 8;                     // padded bf16 K row (elements)
@@ -38,6 +49,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
 
   pdl_trigger();
   pdl_wait();
+  rstamp(a, 0);
   const int split = blockIdx.x, bz = blockIdx.z, b = a.b_base + bz;
   const int kvh = blockIdx.y % a.KVr, rb = blockIdx.y / a.KVr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -78,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
     m_s[tid] = -INFINITY;
     l_s[tid] = 0.f;
   }
+  rstamp(a, 1);
   const int dg = lane, rg = warp;  // P.V: dims 4 dg .. 4 dg + 3, rows 8 rg .. 8 rg + 7
   float acc[RPW][DPL];
 #pragma unroll
@@ -110,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
       }
     }
     __syncthreads();
+    rstamp(a, 2);
     // ---- scores s[r][kk] = q_r . k_kk  (masked: key p visible to row i iff p <= T + i)
     {
       const int kk = tid % kKB, r0 = tid / kKB;
@@ -143,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
       }
     }
     __syncthreads();
+    rstamp(a, 3);
     // ---- online softmax per row: warp w -> rows 8w .. 8w+7
     for (int r = warp * (kRows / 8); r < (warp + 1) * (kRows / 8); ++r) {
       float* pr = p_s + r * (kKB + 1);
@@ -188,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
     }
   }
   __syncthreads();
+  rstamp(a, 4);
   // ---- partial (M, L, A) of this split -> group barrier over the S splits
   const int RB = gridDim.y / a.KVr;
   const size_t grp = ((size_t)bz * a.KVr + kvh) * RB + rb;
@@ -203,7 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
     part[tid * (HD + 2)] = m_s[tid];
     part[tid * (HD + 2) + 1] = l_s[tid];
   }
+  rstamp(a, 5);
   group_barrier(a.group_bar + 2 * grp, S);
+  rstamp(a, 6);
   // ---- distributed combine: split s finalises rows [64 s / S, 64 (s+1) / S)
   const int s_active = chunk > 0 ? (nkeys + chunk - 1) / chunk : 0;
   const int ra = kRows * split / S, rz = kRows * (split + 1) / S, nrow = rz - ra;
@@ -245,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
     a.out_hi[off] = hi;
     a.out_lo[off] = f2bf_bits(val - __uint_as_float((uint32_t)hi << 16));
   }
+  rstamp(a, 7);
 }
 
 template <int HD>

@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
   }
   __syncthreads();
   // ---- D: active down rows only: y += m * W_down[n]; thread owns column chunks tid + NT j
-  constexpr int RU = CPT == 1 ? 16 : (CPT == 2 ? 8 : 4);  // rows in flight per thread
+  // rows in flight per thread (fewer for B = 8: the y[B][.] accumulators share the registers)
+  constexpr int RU = (CPT == 1 ? 16 : (CPT == 2 ? 8 : 4)) / (B >= 8 ? 2 : 1);
   float y[B][CPT * 8];
 #pragma unroll
   for (int b = 0; b < B; ++b)
@@ -290,6 +291,7 @@ cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st) {
     case 1: return gemv_b<1>(a, grid, st);
     case 2: return gemv_b<2>(a, grid, st);
     case 4: return gemv_b<4>(a, grid, st);
+    case 8: return gemv_b<8>(a, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -339,6 +341,7 @@ cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st) {
     case 1: return ffn_b<1>(a, grid, st);
     case 2: return ffn_b<2>(a, grid, st);
     case 4: return ffn_b<4>(a, grid, st);
+    case 8: return ffn_b<8>(a, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }

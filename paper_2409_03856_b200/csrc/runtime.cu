@@ -140,6 +140,7 @@ struct sirius_ctx {
   const uint16_t** step_w = nullptr;  // device [7][L]: attn_norm, w_qkv, w_o, ffn_norm, w_gate, w_up, w_down
   float *step_x = nullptr, *step_x1 = nullptr, *step_o = nullptr;
   unsigned long long* step_bar = nullptr;
+  int trace_layer = -1;                  // debug: attn_rows trace of this verify layer (sirius_debug_trace_verify)
   int step_tune = 1;                     // SIRIUS_STEP_TUNE (bit 0: evict-first weight loads)
   unsigned long long* trace = nullptr;  // debug: decode-step phase stamps (sirius_debug_trace)
   // CUDA graphs: every ABI call is captured once per distinct argument set and replayed
@@ -380,6 +381,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       aa.group_bar = R.attn_bar;
       aa.out_hi = R.ob_hi;
       aa.out_lo = R.ob_lo;
+      aa.trace = (!to_cache && l == c->trace_layer) ? c->trace : nullptr;
       const int row_blocks = (rows_per_seq * c->G + 63) / 64;
       int splits = launch::attn_rows_splits(nseq, c->KVr, row_blocks, cf.max_seq, c->num_sms);
       while (splits > 1 && nseq * c->KVr * row_blocks * splits > kAttnRowUnits) --splits;  // workspace bound
@@ -432,7 +434,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   if (cf.d_model % 256 || ((cf.n_heads / cf.tp_size) * cf.head_dim) % 64 || (cf.ffn_dim / cf.tp_size) % 8)
     return SIRIUS_ERR_UNSUPPORTED;
   if (cf.max_gamma > 64 || (long)cf.batch * cf.max_gamma > 256) return SIRIUS_ERR_UNSUPPORTED;
-  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4) return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4 && cf.batch != 8) return SIRIUS_ERR_UNSUPPORTED;
   for (int l = 0; l < cf.n_layers; ++l)
     if (!(cats_threshold[l] >= 0.f)) return SIRIUS_ERR_INVALID_ARG;
   const bool emulate = cf.tp_size > 1 && nccl_comm == nullptr;
@@ -579,7 +581,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   cudaMemcpy(c->dA_ptrs, dA_h.data(), sizeof(float*) * dA_h.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(c->dF_ptrs, dF_h.data(), sizeof(float*) * dF_h.size(), cudaMemcpyHostToDevice);
   // persistent decode step (TP 1)
-  if (!emulate && cf.tp_size == 1 &&
+  if (!emulate && cf.tp_size == 1 && cf.batch <= 4 &&
       launch::decode_step_supported(d, cf.n_heads, cf.n_kv_heads, hd, cf.ffn_dim, c->num_sms)) {
     // opt-in: measured at parity / slightly slower than the per-stage kernels on the 8B step
     // (2.90-2.93 vs 2.86-2.89 ms), so the per-stage schedule stays the default
@@ -1035,6 +1037,15 @@ int sirius_debug_trace(sirius_ctx* c, void* buf) {
   if (!c) return -1;
   c->trace = static_cast<unsigned long long*>(buf);
   return c->use_step ? 1 : 0;
+}
+
+// Debug: %globaltimer phase stamps of the verify attention of `layer` into buf (DEV u64 [8][CTAs]);
+// layer < 0 stops.  Graphs should be off (the pointer is captured into graphs).
+int sirius_debug_trace_verify(sirius_ctx* c, void* buf, int layer) {
+  if (!c) return -1;
+  c->trace = static_cast<unsigned long long*>(buf);
+  c->trace_layer = layer;
+  return 0;
 }
 
 int sirius_debug_graphs(sirius_ctx* c, int on) {

@@ -47,6 +47,7 @@ struct AttnRowsArgs {
   unsigned* group_bar;      // [nseq * KVr * row_blocks][2] barrier (count, generation) of the split groups
   uint16_t* out_hi;         // [nseq * rows, Hr * hd] attention output as a bf16 hi/lo pair
   uint16_t* out_lo;
+  unsigned long long* trace;  // debug: [8][grid CTAs] %globaltimer stamps, or NULL
 };
 
 struct RowStat {

@@ -248,3 +248,16 @@ def test_8b2l_tensor_parallel_emulation(l2, tp):
     shards = [sg.device_weights(cfg, tp, r) for r in range(tp)]
     ctx = make_ctx(cfg, shards, thr, 1, 256, tp=tp)
     gpu_script(ctx, cfg, thr, prompts, refs, 2, GAMMA)
+
+
+def test_tiny_batch8_per_sequence_sets():
+    """Batch 8 (the smallest of BASELINE configs[2]'s batch range): eight independent sequences of
+    different lengths, per-sequence positions, active sets, decisions and rewrites."""
+    from synth import gpu as sg
+    cfg = synth.TINY
+    wh = synth.host_weights(cfg)
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 10 + b, 20 + 7 * b) for b in range(8)]
+    refs = [oracle_script(cfg, wh, thr, p, 2, 8, 256) for p in prompts]
+    ctx = make_ctx(cfg, sg.device_weights(cfg), thr, 8, 256)
+    gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
