@@ -27,7 +27,7 @@ SIRIUS_DEV void rstamp(const AttnRowsArgs& a, int slot) {  // debug phase stamps
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    a.trace[(size_t)slot * gridDim.x * gridDim.y * gridDim.z + cta] = t;
+    a.trace[(size_t)slot * 1024 + cta] = t;  // [8][1024]
   }
 }
 

@@ -86,6 +86,13 @@ SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
   }
 }
 
+SIRIUS_DEV void gstamp(const GemmArgs& g, int slot) {
+  if (!g.trace) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g.trace[(size_t)slot * 1024 + blockIdx.x] = t;  // [8][1024]
+}
+
 template <bool DUAL>
 __global__ void __launch_bounds__(128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
@@ -99,6 +106,7 @@ __global__ void __launch_bounds__(128, 1)
   const long long w0 = W * c / G, w1 = W * (c + 1) / G;
   if (w0 == w1) return;
 
+  if (tid == 0) gstamp(g, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t b_bytes = (uint32_t)MP * 128;
@@ -156,7 +164,9 @@ __global__ void __launch_bounds__(128, 1)
       if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[i], pol_w);
     }
   }
+  if (tid == 0) gstamp(g, 1);
   pdl_wait();
+  if (tid == 0) gstamp(g, 2);
   if (warp == 0 && lane == 0) {
     const uint64_t pol_x = policy_evict_last();
     for (int i = 0; i < npre; ++i) {
@@ -198,6 +208,7 @@ __global__ void __launch_bounds__(128, 1)
         const long long q = it + i;
         const int s = (int)(q % stages);
         mbar_wait(&full[s], (uint32_t)(q / stages) & 1u);
+        if (q == 0) gstamp(g, 3);  // first stage landed (MMA thread)
         tc_fence_after();
         uint8_t* st = smem + (size_t)s * stage_bytes;
         const uint64_t a0 = sw128_desc(st), b0 = sw128_desc(st + NACC * A_BYTES);
@@ -221,6 +232,7 @@ __global__ void __launch_bounds__(128, 1)
     __syncwarp();
     // ---- epilogue (all 128 threads; thread = TMEM lane = weight row of the tile)
     mbar_wait(accum, (uint32_t)sidx & 1u);
+    if (tid == 0 && sidx == 0) gstamp(g, 4);  // first segment's accumulator complete
     tc_fence_after();
     const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
     const int n = t * 128 + tid;
@@ -272,6 +284,7 @@ __global__ void __launch_bounds__(128, 1)
     w = wend;
   }
   __syncthreads();
+  if (tid == 0) gstamp(g, 5);  // all segments (epilogue + fix-up) done
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
 }

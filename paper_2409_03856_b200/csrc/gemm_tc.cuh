@@ -14,6 +14,7 @@ struct GemmArgs {
   int ldc;
   float* part;          // stream-K partials [num_sms, 2, NACC, 256, 128]
   unsigned* counters;   // [n_tiles] (self-resetting)
+  unsigned long long* trace;  // debug: [8][grid] %globaltimer stamps of thread 0 / the MMA thread, or NULL
 };
 
 namespace launch {

@@ -297,8 +297,10 @@ sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
 }
 
 sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x_hi,
-                       const TmapBuf& x_lo, int N, int K, int M, void* out, int ldc, void* out2 = nullptr) {
-  GemmArgs g;
+                       const TmapBuf& x_lo, int N, int K, int M, void* out, int ldc, void* out2 = nullptr,
+                       unsigned long long* trace = nullptr) {
+  GemmArgs g = {};
+  g.trace = trace;
   g.N = N;
   g.K = K;
   g.M = M;
@@ -340,7 +342,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.out_hi = R.xn_hi;
       na.out_lo = R.xn_lo;
       LCU(launch::norm_rows(na, M, c->stream));
-      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Nqkv, d, M, R.qkv, c->Nqkv));
+      unsigned long long* gtr = (!to_cache && l == c->trace_layer && c->trace) ? c->trace + 8 * 1024 : nullptr;
+      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Nqkv, d, M, R.qkv, c->Nqkv, nullptr, gtr));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
       RopeStoreArgs ra = {};
@@ -386,7 +389,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       int splits = launch::attn_rows_splits(nseq, c->KVr, row_blocks, cf.max_seq, c->num_sms);
       while (splits > 1 && nseq * c->KVr * row_blocks * splits > kAttnRowUnits) --splits;  // workspace bound
       LCU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
-      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d));
+      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d, nullptr,
+                  gtr ? gtr + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
     for (auto& R : c->ranks) {
@@ -401,8 +405,11 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.out_hi = R.xn_hi;
       na.out_lo = R.xn_lo;
       LCU(launch::norm_rows(na, M, c->stream));
-      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn_hi, R.tm_xn_lo, c->Fr, d, M, R.mb_hi, c->Fr, R.mb_lo));
-      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb_hi, R.tm_mb_lo, d, c->Fr, M, R.dF, d));
+      unsigned long long* gtr2 = (!to_cache && l == c->trace_layer && c->trace) ? c->trace + 3 * 8 * 1024 : nullptr;
+      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn_hi, R.tm_xn_lo, c->Fr, d, M, R.mb_hi, c->Fr, R.mb_lo,
+                  gtr2));
+      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb_hi, R.tm_mb_lo, d, c->Fr, M, R.dF, d, nullptr,
+                  gtr2 ? gtr2 + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
   }
@@ -536,8 +543,8 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
         alloc(c, &R.xn_lo, (size_t)M * d) || alloc(c, &R.qb, (size_t)M * c->Hr * hd) ||
         alloc(c, &R.ob, (size_t)M * c->Hr * hd) || alloc(c, &R.ob_hi, (size_t)M * c->Hr * hd) ||
         alloc(c, &R.ob_lo, (size_t)M * c->Hr * hd) || alloc(c, &R.mb_hi, (size_t)M * c->Fr) ||
-        alloc(c, &R.mb_lo, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * 4 * d) ||
-        alloc(c, &R.ffn_cnt, (size_t)c->num_sms * 4) || alloc(c, &R.ffn_barrier, 8) ||
+        alloc(c, &R.mb_lo, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * std::max(4, B) * d) ||
+        alloc(c, &R.ffn_cnt, (size_t)c->num_sms * std::max(4, B)) || alloc(c, &R.ffn_barrier, 8) ||
         alloc(c, &R.attn_part, (size_t)kAttnRowUnits * 64 * (hd + 2) + (size_t)B * c->KVr * 64 * 8 * (hd + 2)) ||
         alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) || alloc(c, &R.attn_bar, 8192) ||
         alloc(c, &R.gemm_part, launch::gemm_workspace_bytes(c->num_sms) / sizeof(float)) ||
@@ -1112,7 +1119,7 @@ int sirius_debug_gemm(const void* X, const void* Xlo, int x_rows, const void* Wt
   if (!launch::make_tmap(ta.b, Wt, N, K, 128) || !launch::make_tmap(tx.b, X, x_rows, K, 16)) return -2;
   if (Xlo && !launch::make_tmap(txl.b, Xlo, x_rows, K, 16)) return -2;
   if (W2 && !launch::make_tmap(tb.b, W2, N, K, 128)) return -2;
-  GemmArgs g;
+  GemmArgs g = {};
   g.N = N;
   g.K = K;
   g.M = M;
