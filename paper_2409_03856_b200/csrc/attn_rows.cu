@@ -225,38 +225,37 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
   // ---- distributed combine: split s finalises rows [64 s / S, 64 (s+1) / S)
   const int s_active = chunk > 0 ? (nkeys + chunk - 1) / chunk : 0;
   const int ra = kRows * split / S, rz = kRows * (split + 1) / S, nrow = rz - ra;
-  float* w_s = p_s;            // [nrow][S] weights exp(M_s - M)
-  if (tid < nrow) {
-    const int r = ra + tid;
-    float M = -INFINITY;
-    float mv[kKB];
-#pragma unroll 8
-    for (int sp = 0; sp < s_active; ++sp) mv[sp] = __ldcg(pbase + ((size_t)sp * kRows + r) * (HD + 2));
-    for (int sp = 0; sp < s_active; ++sp) M = fmaxf(M, mv[sp]);
-    float L = 0.f;
-#pragma unroll 8
-    for (int sp = 0; sp < s_active; ++sp) {
-      const float f = (mv[sp] == -INFINITY || M == -INFINITY) ? 0.f : expf(mv[sp] - M);
-      L += __ldcg(pbase + ((size_t)sp * kRows + r) * (HD + 2) + 1) * f;
-      w_s[tid * kKB + sp] = f;
-    }
-    l_s[tid] = L;
-  }
-  __syncthreads();
+  // every output (row, dim): the partial values AND (M_s, L_s) of its row for all splits requested
+  // together (one round trip per 32 splits), then M = max M_s, o = sum e^(M_s-M) A_s / sum e^(M_s-M) L_s
   for (int idx = tid; idx < nrow * HD; idx += kThreads) {
     const int rl = idx / HD, d = idx % HD, r = ra + rl;
     if (r >= nr) continue;
-    float o = 0.f;
-    for (int sp0 = 0; sp0 < s_active; sp0 += 16) {  // 16 independent loads in flight
-      float v[16];
+    float M = -INFINITY, Ls = 0.f, o = 0.f;
+    for (int sp0 = 0; sp0 < s_active; sp0 += 32) {
+      float mv[32], lv[32], av[32];
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
-        v[u] = sp0 + u < s_active ? __ldcg(pbase + ((size_t)(sp0 + u) * kRows + r) * (HD + 2) + 2 + d) : 0.f;
+      for (int u = 0; u < 32; ++u) {
+        const float* ps = pbase + ((size_t)(sp0 + u) * kRows + r) * (HD + 2);
+        const bool ok = sp0 + u < s_active;
+        mv[u] = ok ? __ldcg(ps) : -INFINITY;
+        lv[u] = ok ? __ldcg(ps + 1) : 0.f;
+        av[u] = ok ? __ldcg(ps + 2 + d) : 0.f;
+      }
+      float Mb = M;
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (sp0 + u < s_active) o += v[u] * w_s[rl * kKB + sp0 + u];
+      for (int u = 0; u < 32; ++u) Mb = fmaxf(Mb, mv[u]);
+      const float sc = M == -INFINITY ? 0.f : expf(M - Mb);  // rescale earlier batches (s_active > 32)
+      Ls *= sc;
+      o *= sc;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const float f = mv[u] == -INFINITY ? 0.f : expf(mv[u] - Mb);
+        Ls += lv[u] * f;
+        o += av[u] * f;
+      }
+      M = Mb;
     }
-    const float val = l_s[rl] > 0.f ? o / l_s[rl] : 0.f;
+    const float val = Ls > 0.f ? o / Ls : 0.f;
     const int rr = r_base + r, i = rr / G, g = rr % G;
     const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + d;
     const uint16_t hi = f2bf_bits(val);

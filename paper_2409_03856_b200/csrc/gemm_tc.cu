@@ -93,8 +93,32 @@ SIRIUS_DEV void gstamp(const GemmArgs& g, int slot) {
   g.trace[(size_t)slot * 1024 + blockIdx.x] = t;  // [8][1024]
 }
 
+// Epilogue-only barrier (warps 0-3) and "last of n arrivals" election among them.
+SIRIUS_DEV void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+SIRIUS_DEV bool epi_arrive_last(unsigned* counter, unsigned n, unsigned* flag_s) {
+  epi_sync();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(counter, 1u);
+    const bool last = old == n - 1;
+    if (last) {
+      atomicExch(counter, 0u);
+      __threadfence();
+    }
+    *flag_s = last ? 1u : 0u;
+  }
+  epi_sync();
+  return *flag_s != 0;
+}
+
+// Warp-specialised (192 threads): warps 0-3 epilogue (TMEM lane = weight row = threadIdx.x), warp 4
+// lane 0 TMA producer, warp 5 lane 0 MMA issuer (+ TMEM allocation).  The producer streams the CTA's
+// whole stream-K range without stopping at tile (segment) boundaries, and the accumulator is double
+// buffered in TMEM when 2 NACC MP <= 512 columns, so a segment's epilogue / fix-up overlaps the next
+// segment's loads and MMAs (r01 trace: the second segment of a CTA used to wait for the first's
+// epilogue and refill the pipeline, up to 17 us per GEMM).
 template <bool DUAL>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo, GemmArgs g,
                    int MP, int stages, int has_lo) {
@@ -114,24 +138,30 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t stage_bytes = ((NACC * A_BYTES + NB * b_bytes) + 1023) & ~1023u;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* accum = empty + stages;
-  uint32_t* tmem_ptr_s = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* acc_full = empty + stages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint32_t* tmem_ptr_s = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  unsigned* flag_s = tmem_ptr_s + 1;
+  const int NBUF = 2 * NACC * MP <= 512 ? 2 : 1;
   uint32_t ncols = 32;
-  while (ncols < (uint32_t)(NACC * MP)) ncols <<= 1;
+  while (ncols < (uint32_t)(NBUF * NACC * MP)) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
     fence_mbar_init();
     prefetch_tmap(&tmA0);
     if (DUAL) prefetch_tmap(&tmA1);
     prefetch_tmap(&tmB);
     if (has_lo) prefetch_tmap(&tmBlo);
   }
-  if (warp == 2) {
+  if (warp == 5) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_ptr_s)),
                  "r"(ncols)
                  : "memory");
@@ -145,148 +175,149 @@ __global__ void __launch_bounds__(128, 1)
   // both K-major, N>>3 at [17,23), M>>4 at [24,29)
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((128u >> 4) << 24);
   const uint32_t tx_bytes = NACC * A_BYTES + NB * b_bytes;
-
-  // PDL: the weight (A) tiles of the first stages do not depend on the predecessor kernel; request
-  // them before the dependency wait, the activation (B) tiles after it.
+  const long long nq = w1 - w0;  // the CTA's k-iterations, over all its segments
   pdl_trigger();
-  int npre = 0;
-  {
-    const long long wend0 = min(w1, (w0 / g.kb + 1) * g.kb);
-    npre = (int)min((long long)stages, wend0 - w0);
-  }
-  if (warp == 0 && lane == 0) {
-    const uint64_t pol_w = policy_evict_first();
-    for (int i = 0; i < npre; ++i) {
-      uint8_t* st = smem + (size_t)i * stage_bytes;
-      mbar_arrive_expect_tx(&full[i], tx_bytes);
-      const int t = (int)(w0 / g.kb), kc = (int)((w0 % g.kb) + i) * 64;
-      tma_load_2d(st, &tmA0, kc, t * 128, &full[i], pol_w);
-      if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[i], pol_w);
-    }
-  }
-  if (tid == 0) gstamp(g, 1);
-  pdl_wait();
-  if (tid == 0) gstamp(g, 2);
-  if (warp == 0 && lane == 0) {
-    const uint64_t pol_x = policy_evict_last();
-    for (int i = 0; i < npre; ++i) {
-      uint8_t* st = smem + (size_t)i * stage_bytes;
-      const int kc = (int)((w0 % g.kb) + i) * 64;
-      for (int r = 0; r < MP / 16; ++r) {
-        tma_load_2d(st + NACC * A_BYTES + r * 2048, &tmB, kc, r * 16, &full[i], pol_x);
-        if (has_lo) tma_load_2d(st + NACC * A_BYTES + b_bytes + r * 2048, &tmBlo, kc, r * 16, &full[i], pol_x);
-      }
-    }
-  }
 
-  long long it = 0;  // global k-iteration counter: stage = it % stages, parity = (it / stages) & 1
-  int sidx = 0;
-  for (long long w = w0; w < w1; ++sidx) {
-    const int t = (int)(w / g.kb);
-    const int kbeg = (int)(w % g.kb);
-    const long long wend = min(w1, (long long)(t + 1) * g.kb);
-    const int nk = (int)(wend - w);
-    if (warp == 0 && lane == 0) {  // ---- TMA producer
+  if (warp == 4) {
+    if (lane == 0) {  // ---------------- TMA producer
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-      for (int i = 0; i < nk; ++i) {
-        const long long q = it + i;
-        if (q < npre) continue;  // requested before the dependency wait
+      // PDL: weight (A) tiles of the first stages before the dependency wait, activations after it
+      const int npre = (int)min((long long)stages, nq);
+      for (int i = 0; i < npre; ++i) {
+        const long long w = w0 + i;
+        uint8_t* st = smem + (size_t)i * stage_bytes;
+        mbar_arrive_expect_tx(&full[i], tx_bytes);
+        const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64;
+        tma_load_2d(st, &tmA0, kc, t * 128, &full[i], pol_w);
+        if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[i], pol_w);
+      }
+      gstamp(g, 1);
+      pdl_wait();
+      gstamp(g, 2);
+      for (long long q = 0; q < nq; ++q) {
+        const long long w = w0 + q;
         const int s = (int)(q % stages);
-        mbar_wait(&empty[s], ((uint32_t)(q / stages) & 1u) ^ 1u);
+        const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64;
         uint8_t* st = smem + (size_t)s * stage_bytes;
-        mbar_arrive_expect_tx(&full[s], tx_bytes);
-        const int kc = (kbeg + i) * 64;
-        tma_load_2d(st, &tmA0, kc, t * 128, &full[s], pol_w);
-        if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[s], pol_w);
+        if (q >= npre) {
+          mbar_wait(&empty[s], ((uint32_t)(q / stages) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&full[s], tx_bytes);
+          tma_load_2d(st, &tmA0, kc, t * 128, &full[s], pol_w);
+          if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[s], pol_w);
+        }
         for (int r = 0; r < MP / 16; ++r) {
           tma_load_2d(st + NACC * A_BYTES + r * 2048, &tmB, kc, r * 16, &full[s], pol_x);
           if (has_lo) tma_load_2d(st + NACC * A_BYTES + b_bytes + r * 2048, &tmBlo, kc, r * 16, &full[s], pol_x);
         }
       }
-    } else if (warp == 1 && lane == 0) {  // ---- MMA issuer
-      for (int i = 0; i < nk; ++i) {
-        const long long q = it + i;
-        const int s = (int)(q % stages);
-        mbar_wait(&full[s], (uint32_t)(q / stages) & 1u);
-        if (q == 0) gstamp(g, 3);  // first stage landed (MMA thread)
-        tc_fence_after();
-        uint8_t* st = smem + (size_t)s * stage_bytes;
-        const uint64_t a0 = sw128_desc(st), b0 = sw128_desc(st + NACC * A_BYTES);
-        const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES) : 0ull;
-        const uint64_t b1 = sw128_desc(st + NACC * A_BYTES + b_bytes);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
-          const uint32_t accf = (i > 0 || k > 0) ? 1u : 0u;
-          mma_bf16(tmem, a0 + 2 * k, b0 + 2 * k, idesc, accf);
-          if (DUAL) mma_bf16(tmem + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
-          if (has_lo) {
-            mma_bf16(tmem, a0 + 2 * k, b1 + 2 * k, idesc, 1u);
-            if (DUAL) mma_bf16(tmem + MP, a1 + 2 * k, b1 + 2 * k, idesc, 1u);
-          }
-        }
-        mma_commit(&empty[s]);  // smem slot free once these MMAs have read it
-      }
-      mma_commit(accum);  // accumulator complete
     }
-    it += nk;
-    __syncwarp();
-    // ---- epilogue (all 128 threads; thread = TMEM lane = weight row of the tile)
-    mbar_wait(accum, (uint32_t)sidx & 1u);
-    if (tid == 0 && sidx == 0) gstamp(g, 4);  // first segment's accumulator complete
-    tc_fence_after();
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-    const int n = t * 128 + tid;
-    const bool complete = (kbeg == 0 && wend == (long long)(t + 1) * g.kb);
-    if (complete) {
-      for (int j0 = 0; j0 < MP; j0 += 16) {
-        float v0[16], v1[16];
-        tmem_ld16(tbase + j0, v0);
-        if (DUAL) tmem_ld16(tbase + MP + j0, v1);
+  } else if (warp == 5) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      long long q = 0;
+      int sidx = 0;
+      for (long long w = w0; w < w1; ++sidx) {
+        const int t = (int)(w / g.kb);
+        const long long wend = min(w1, (long long)(t + 1) * g.kb);
+        const int buf = sidx % NBUF;
+        if (sidx >= NBUF) mbar_wait(&acc_empty[buf], (uint32_t)((sidx / NBUF) - 1) & 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * NACC * MP);
+        for (long long i = 0; w + i < wend; ++i, ++q) {
+          const int s = (int)(q % stages);
+          mbar_wait(&full[s], (uint32_t)(q / stages) & 1u);
+          if (q == 0) gstamp(g, 3);
+          tc_fence_after();
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          const uint64_t a0 = sw128_desc(st), b0 = sw128_desc(st + NACC * A_BYTES);
+          const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES) : 0ull;
+          const uint64_t b1 = sw128_desc(st + NACC * A_BYTES + b_bytes);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, v0[j], DUAL ? v1[j] : 0.f);
-      }
-    } else {
-      const int slot = (w == w0) ? 0 : 1;
-      float* mine = g.part + ((size_t)(c * 2 + slot) * NACC) * 256 * 128;
-      for (int j0 = 0; j0 < MP; j0 += 16) {
-        float v[16];
-        for (int a = 0; a < NACC; ++a) {
-          tmem_ld16(tbase + a * MP + j0, v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) mine[((size_t)a * 256 + j0 + j) * 128 + tid] = v[j];
-        }
-      }
-      const int cf = owner_of((long long)t * g.kb, W, G);
-      const int cl = owner_of(min(W, (long long)(t + 1) * g.kb) - 1, W, G);
-      if (arrive_last(g.counters + t, (unsigned)(cl - cf + 1))) {
-        for (int j0 = 0; j0 < MP; j0 += 16) {
-          float s0[16], s1[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) s0[j] = s1[j] = 0.f;
-          for (int cc = cf; cc <= cl; ++cc) {  // fixed CTA order -> deterministic
-            const long long cw0 = W * cc / G;
-            const int sl = ((int)(cw0 / g.kb) == t) ? 0 : 1;
-            const float* p = g.part + ((size_t)(cc * 2 + sl) * NACC) * 256 * 128;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              s0[j] += __ldcg(p + (size_t)(j0 + j) * 128 + tid);
-              if (DUAL) s1[j] += __ldcg(p + ((size_t)256 + j0 + j) * 128 + tid);
+          for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
+            const uint32_t accf = (i > 0 || k > 0) ? 1u : 0u;
+            mma_bf16(acc, a0 + 2 * k, b0 + 2 * k, idesc, accf);
+            if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
+            if (has_lo) {
+              mma_bf16(acc, a0 + 2 * k, b1 + 2 * k, idesc, 1u);
+              if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b1 + 2 * k, idesc, 1u);
             }
           }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, s0[j], s1[j]);
+          mma_commit(&empty[s]);  // smem slot free once these MMAs have read it
         }
+        mma_commit(&acc_full[buf]);  // this segment's accumulator complete
+        w = wend;
       }
     }
-    tc_fence_before();
-    __syncthreads();  // TMEM drained before the next segment's MMAs overwrite it
-    tc_fence_after();
-    w = wend;
+  } else {  // ---------------- epilogue warps 0-3 (thread = TMEM lane = weight row of the tile)
+    pdl_wait();
+    int sidx = 0;
+    for (long long w = w0; w < w1; ++sidx) {
+      const int t = (int)(w / g.kb);
+      const int kbeg = (int)(w % g.kb);
+      const long long wend = min(w1, (long long)(t + 1) * g.kb);
+      const int buf = sidx % NBUF;
+      mbar_wait(&acc_full[buf], (uint32_t)(sidx / NBUF) & 1u);
+      if (tid == 0 && sidx == 0) gstamp(g, 4);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t)(buf * NACC * MP) + ((uint32_t)(warp * 32) << 16);
+      const int n = t * 128 + tid;
+      const bool complete = (kbeg == 0 && wend == (long long)(t + 1) * g.kb);
+      if (complete) {
+        for (int j0 = 0; j0 < MP; j0 += 16) {
+          float v0[16], v1[16];
+          tmem_ld16(tbase + j0, v0);
+          if (DUAL) tmem_ld16(tbase + MP + j0, v1);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, v0[j], DUAL ? v1[j] : 0.f);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      } else {
+        const int slot = (w == w0) ? 0 : 1;
+        float* mine = g.part + ((size_t)(c * 2 + slot) * NACC) * 256 * 128;
+        for (int j0 = 0; j0 < MP; j0 += 16) {
+          float v[16];
+          for (int a = 0; a < NACC; ++a) {
+            tmem_ld16(tbase + a * MP + j0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) mine[((size_t)a * 256 + j0 + j) * 128 + tid] = v[j];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);  // TMEM drained; the fix-up below reads global memory
+        const int cf = owner_of((long long)t * g.kb, W, G);
+        const int cl = owner_of(min(W, (long long)(t + 1) * g.kb) - 1, W, G);
+        if (epi_arrive_last(g.counters + t, (unsigned)(cl - cf + 1), flag_s)) {
+          for (int j0 = 0; j0 < MP; j0 += 16) {
+            float s0[16], s1[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) s0[j] = s1[j] = 0.f;
+            for (int cc = cf; cc <= cl; ++cc) {  // fixed CTA order -> deterministic
+              const long long cw0 = W * cc / G;
+              const int sl = ((int)(cw0 / g.kb) == t) ? 0 : 1;
+              const float* p = g.part + ((size_t)(cc * 2 + sl) * NACC) * 256 * 128;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                s0[j] += __ldcg(p + (size_t)(j0 + j) * 128 + tid);
+                if (DUAL) s1[j] += __ldcg(p + ((size_t)256 + j0 + j) * 128 + tid);
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, s0[j], s1[j]);
+          }
+        }
+      }
+      w = wend;
+    }
   }
+  tc_fence_before();
   __syncthreads();
   if (tid == 0) gstamp(g, 5);  // all segments (epilogue + fix-up) done
-  if (warp == 2)
+  if (warp == 5) {
+    tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+  }
 }
 
 // ===================================================================== host side
@@ -331,7 +362,7 @@ cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void
   const int NACC = dual ? 2 : 1;
   const int NB = tmBlo ? 2 : 1;
   const size_t stage_bytes = ((size_t)NACC * 16384 + (size_t)NB * MP * 128 + 1023) & ~(size_t)1023;
-  const size_t extra = 1024 + 256;
+  const size_t extra = 1024 + 512;
   int stages = (int)((smem_budget - extra) / stage_bytes);
   if (stages > 8) stages = 8;
   if (stages < 2) return cudaErrorInvalidValue;
@@ -346,12 +377,12 @@ cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void
   if (dual) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return launch_chain(gemm_tc_kernel<true>, dim3(grid), dim3(128), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
+    return launch_chain(gemm_tc_kernel<true>, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
                         has_lo);
   } else {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return launch_chain(gemm_tc_kernel<false>, dim3(grid), dim3(128), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
+    return launch_chain(gemm_tc_kernel<false>, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
                         has_lo);
   }
   return cudaGetLastError();
