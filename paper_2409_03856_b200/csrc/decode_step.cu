@@ -711,6 +711,40 @@ __global__ void __launch_bounds__(kNT, 1) decode_step_kernel(StepArgs a) {
   }
 }
 
+// The attention phase alone, as the per-stage schedule's attention kernel (one (b, kv head, split)
+// item per CTA, RoPE + K/V append + split-K + last-split combine; no co-residency needed).
+template <int B, int HD, int G>
+__global__ void __launch_bounds__(kNT, 1) attn_stage_kernel(StepArgs a, int l) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  StepSmem<B, HD, G>& sm = *reinterpret_cast<StepSmem<B, HD, G>*>(smem_raw);
+  const AttnItem it = attn_item<B>(a);
+  constexpr int NL = kKB * HD / 8 / kNT > 0 ? kKB * HD / 8 / kNT : 1;
+  uint4 kv[NL], vv[NL];
+  if (it.active && it.k0 < it.k1) attn_load_block<HD>(a, l, it, it.k0, kv, vv);
+  attention_phase<B, HD, G>(a, l, sm, it, kv, vv);
+}
+
+template <int B, int HD, int G>
+cudaError_t launch_attn_stage(const StepArgs& a, int l, cudaStream_t st) {
+  auto kern = attn_stage_kernel<B, HD, G>;
+  const size_t smem = (sizeof(StepSmem<B, HD, G>) + 127) / 128 * 128;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<B * a.KVr * a.splits, kNT, smem, st>>>(a, l);
+  return cudaGetLastError();
+}
+
+template <int HD, int G>
+cudaError_t attn_stage_b(const StepArgs& a, int l, int B, cudaStream_t st) {
+  switch (B) {
+    case 1: return launch_attn_stage<1, HD, G>(a, l, st);
+    case 2: return launch_attn_stage<2, HD, G>(a, l, st);
+    case 4: return launch_attn_stage<4, HD, G>(a, l, st);
+    case 8: return launch_attn_stage<8, HD, G>(a, l, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int B, int CPL, int HD, int G>
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
   auto kern = decode_step_kernel<B, CPL, HD, G>;
@@ -755,6 +789,16 @@ bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms) {
 int decode_step_splits(int B, int KV, int num_sms) {
   int s = num_sms / (B * KV);
   return s < 1 ? 1 : (s > kMaxSplits ? kMaxSplits : s);
+}
+
+bool attn_stage_supported(int hd, int G) { return (hd == 128 && (G == 4 || G == 8)) || (hd == 64 && G == 2); }
+
+cudaError_t attn_stage(const StepArgs& a, int l, int B, cudaStream_t st) {
+  const int G = a.Hr / a.KVr;
+  if (a.hd == 128 && G == 4) return attn_stage_b<128, 4>(a, l, B, st);
+  if (a.hd == 128 && G == 8) return attn_stage_b<128, 8>(a, l, B, st);
+  if (a.hd == 64 && G == 2) return attn_stage_b<64, 2>(a, l, B, st);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t decode_step(const StepArgs& a, int B, int grid, cudaStream_t st) {

@@ -29,6 +29,8 @@ cudaError_t attn_decode(const AttnArgs& a, int B, int hd, int group, cudaStream_
 bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms);
 int decode_step_splits(int B, int KV, int num_sms);
 cudaError_t decode_step(const StepArgs& a, int B, int grid, cudaStream_t st);
+bool attn_stage_supported(int hd, int G);
+cudaError_t attn_stage(const StepArgs& a, int l, int B, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius
 
@@ -109,6 +111,8 @@ struct sirius_ctx {
   int num_sms = 148;
   size_t smem_optin = 0;
   int attn_splits = 1;
+  bool attn_stage = false;  // decode attention as the 512-thread item kernel (SIRIUS_ATTN_STAGE=0: old kernel)
+  int attn_stage_splits = 1;
   int accept_splits = 8;
   std::vector<RankState> ranks;
   float *thresholds = nullptr, *rope_cos = nullptr, *rope_sin = nullptr;
@@ -474,6 +478,9 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     return s;
   }
   c->attn_splits = launch::attn_splits(cf.batch, c->KVr, c->num_sms);  // ~one wave of split CTAs
+  c->attn_stage = launch::attn_stage_supported(cf.head_dim, c->G);
+  if (const char* e = getenv("SIRIUS_ATTN_STAGE")) c->attn_stage = c->attn_stage && atoi(e) != 0;
+  c->attn_stage_splits = launch::decode_step_splits(cf.batch, c->KVr, c->num_sms);
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
   auto cleanup_fail = [&](sirius_status s) {
@@ -797,7 +804,30 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       at.out = R.ob;
       at.err = c->err_dev;
       prof_begin(c, P_ATTN);
-      LCU(launch::attn_decode(at, B, hd, c->G, c->stream));
+      if (c->attn_stage) {  // 512-thread item kernel with the last-split combine (decode_step.cu)
+        StepArgs sa = {};
+        sa.d = d;
+        sa.Hr = c->Hr;
+        sa.KVr = c->KVr;
+        sa.hd = hd;
+        sa.max_seq = cf.max_seq;
+        sa.splits = c->attn_stage_splits;
+        sa.attn_scale = 1.0f / sqrtf((float)hd);
+        sa.pos = pos;
+        sa.qkv = R.qkv;
+        sa.o = R.ob;
+        sa.k_cache = R.k_cache;
+        sa.v_cache = R.v_cache;
+        sa.kv_layer = kv_layer;
+        sa.rope_cos = c->rope_cos;
+        sa.rope_sin = c->rope_sin;
+        sa.attn_part = R.attn_part;
+        sa.group_bar = R.attn_bar;
+        sa.err = c->err_dev;
+        LCU(launch::attn_stage(sa, l, B, c->stream));
+      } else {
+        LCU(launch::attn_decode(at, B, hd, c->G, c->stream));
+      }
       prof_end(c);
       GemvArgs o = {};
       o.pro.mode = IN_F32;
