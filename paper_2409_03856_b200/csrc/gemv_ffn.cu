@@ -29,8 +29,12 @@ constexpr int kGemvWarps = 8;   // 2 CTAs per SM
 constexpr int kFfnWarps = 16;   // 1 CTA per SM (cooperative)
 constexpr int kFfnMaxN = 256;   // neurons per CTA
 constexpr int kFfnMaxChunks = kFfnMaxN / 32;
+using dev::after_all;
 using dev::prologue;
 using dev::row_dot;
+using dev::row_finish;
+using dev::row_issue;
+using dev::RowRegs;
 
 // ===================================================================== dense GEMV
 template <int B, int CPL>
@@ -42,16 +46,23 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
   const int K = a.K, CH = K / 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t pol = policy_evict_first();  // weights: read once per step
-  prologue<B>(a.pro, K, h_s, red_s, blockIdx.x == 0);
-  const float4* hp = reinterpret_cast<const float4*>(h_s);
   const int r0 = (int)((long long)a.rows * blockIdx.x / gridDim.x);
   const int r1 = (int)((long long)a.rows * (blockIdx.x + 1) / gridDim.x);
+  // the warp's first weight row is requested before the activation prologue (it does not depend on
+  // it); afterwards each row's loads go out before the previous row's reduction
+  RowRegs<CPL> pf;
+  row_issue<CPL>(pf, a.W + (size_t)(r0 + warp) * K, CH, lane, r0 + warp < r1, pol);
+  constexpr int MG = CPL / 4 > 0 ? CPL / 4 : 1;  // prologue float4 groups per thread (K <= 256 CPL)
+  prologue<B, MG>(a.pro, K, h_s, red_s, blockIdx.x == 0);
+  const float4* hp = reinterpret_cast<const float4*>(h_s);
   unsigned long long best[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) best[b] = 0ull;
   for (int row = r0 + warp; row < r1; row += kGemvWarps) {
     float acc[B];
-    row_dot<B, CPL>(a.W + (size_t)row * K, hp, CH, lane, acc, pol);
+    row_finish<B, CPL>(pf, a.W + (size_t)row * K, hp, CH, lane, acc);
+    row_issue<CPL>(pf, a.W + (size_t)(row + kGemvWarps) * K + after_all<B>(acc), CH, lane, row + kGemvWarps < r1,
+                   pol);
 #pragma unroll
     for (int b = 0; b < B; ++b) acc[b] = warp_sum(acc[b]);
     if (lane == 0) {
@@ -113,14 +124,19 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
   const int nch = (nn + 31) / 32;
 
   const uint64_t pol = policy_evict_first();
-  prologue<B>(a.pro, d, h_s, red_s, cta == 0);
+  RowRegs<CPL> pf;  // first gate row of the warp, requested before the activation prologue
+  row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn, pol);
+  constexpr int MG = CPL / 8 > 0 ? CPL / 8 : 1;  // prologue float4 groups per thread (d <= 512 CPL)
+  prologue<B, MG>(a.pro, d, h_s, red_s, cta == 0);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
   const float t = a.dense ? 0.f : *a.threshold;
 
   // ---- A: dense gate rows: g = h2 . W_gate[n];  a = SiLU(g)
   for (int i = warp; i < nn; i += kFfnWarps) {
     float acc[B];
-    row_dot<B, CPL>(a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc, pol);
+    row_finish<B, CPL>(pf, a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc);
+    row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + i + kFfnWarps) * d + after_all<B>(acc), CH, lane, i + kFfnWarps < nn,
+                   pol);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float g = warp_sum(acc[b]);
