@@ -117,13 +117,16 @@ SIRIUS_DEV bool epi_arrive_last(unsigned* counter, unsigned n, unsigned* flag_s)
 // buffered in TMEM when 2 NACC MP <= 512 columns, so a segment's epilogue / fix-up overlaps the next
 // segment's loads and MMAs (r01 trace: the second segment of a CTA used to wait for the first's
 // epilogue and refill the pipeline, up to 17 us per GEMM).
-template <bool DUAL>
+template <bool DUAL, int KBOX>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo, GemmArgs g,
                    int MP, int stages, int has_lo) {
+  // KBOX: 64-wide K boxes per pipeline stage (one work unit = 64 KBOX of K): each weight row is read
+  // 128 KBOX contiguous bytes at a time
   constexpr int NACC = DUAL ? 2 : 1;
-  constexpr uint32_t A_BYTES = 128 * 64 * 2;  // one 128 x 64 bf16 weight tile
+  constexpr uint32_t BOX_BYTES = 128 * 64 * 2;      // one 128 x 64 bf16 weight box
+  constexpr uint32_t A_BYTES = BOX_BYTES * KBOX;    // one operand's weight tiles of a stage
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int G = gridDim.x, c = blockIdx.x;
   const long long W = (long long)g.n_tiles * g.kb;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(192, 1)
   if (tid == 0) gstamp(g, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t b_bytes = (uint32_t)MP * 128;
+  const uint32_t b_bytes = (uint32_t)MP * 128 * KBOX;  // one activation operand's boxes of a stage
   const int NB = has_lo ? 2 : 1;
   const uint32_t stage_bytes = ((NACC * A_BYTES + NB * b_bytes) + 1023) & ~1023u;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
@@ -187,9 +190,12 @@ __global__ void __launch_bounds__(192, 1)
         const long long w = w0 + i;
         uint8_t* st = smem + (size_t)i * stage_bytes;
         mbar_arrive_expect_tx(&full[i], tx_bytes);
-        const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64;
-        tma_load_2d(st, &tmA0, kc, t * 128, &full[i], pol_w);
-        if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[i], pol_w);
+        const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64 * KBOX;
+#pragma unroll
+        for (int x = 0; x < KBOX; ++x) {
+          tma_load_2d(st + x * BOX_BYTES, &tmA0, kc + 64 * x, t * 128, &full[i], pol_w);
+          if (DUAL) tma_load_2d(st + A_BYTES + x * BOX_BYTES, &tmA1, kc + 64 * x, t * 128, &full[i], pol_w);
+        }
       }
       gstamp(g, 1);
       pdl_wait();
@@ -197,17 +203,24 @@ __global__ void __launch_bounds__(192, 1)
       for (long long q = 0; q < nq; ++q) {
         const long long w = w0 + q;
         const int s = (int)(q % stages);
-        const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64;
+        const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64 * KBOX;
         uint8_t* st = smem + (size_t)s * stage_bytes;
         if (q >= npre) {
           mbar_wait(&empty[s], ((uint32_t)(q / stages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], tx_bytes);
-          tma_load_2d(st, &tmA0, kc, t * 128, &full[s], pol_w);
-          if (DUAL) tma_load_2d(st + A_BYTES, &tmA1, kc, t * 128, &full[s], pol_w);
+#pragma unroll
+          for (int x = 0; x < KBOX; ++x) {
+            tma_load_2d(st + x * BOX_BYTES, &tmA0, kc + 64 * x, t * 128, &full[s], pol_w);
+            if (DUAL) tma_load_2d(st + A_BYTES + x * BOX_BYTES, &tmA1, kc + 64 * x, t * 128, &full[s], pol_w);
+          }
         }
-        for (int r = 0; r < MP / 16; ++r) {
-          tma_load_2d(st + NACC * A_BYTES + r * 2048, &tmB, kc, r * 16, &full[s], pol_x);
-          if (has_lo) tma_load_2d(st + NACC * A_BYTES + b_bytes + r * 2048, &tmBlo, kc, r * 16, &full[s], pol_x);
+#pragma unroll
+        for (int x = 0; x < KBOX; ++x) {
+          uint8_t* bx = st + NACC * A_BYTES + x * (b_bytes / KBOX);
+          for (int r = 0; r < MP / 16; ++r) {
+            tma_load_2d(bx + r * 2048, &tmB, kc + 64 * x, r * 16, &full[s], pol_x);
+            if (has_lo) tma_load_2d(bx + b_bytes + r * 2048, &tmBlo, kc + 64 * x, r * 16, &full[s], pol_x);
+          }
         }
       }
     }
@@ -228,17 +241,21 @@ __global__ void __launch_bounds__(192, 1)
           if (q == 0) gstamp(g, 3);
           tc_fence_after();
           uint8_t* st = smem + (size_t)s * stage_bytes;
-          const uint64_t a0 = sw128_desc(st), b0 = sw128_desc(st + NACC * A_BYTES);
-          const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES) : 0ull;
-          const uint64_t b1 = sw128_desc(st + NACC * A_BYTES + b_bytes);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
-            const uint32_t accf = (i > 0 || k > 0) ? 1u : 0u;
-            mma_bf16(acc, a0 + 2 * k, b0 + 2 * k, idesc, accf);
-            if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
-            if (has_lo) {
-              mma_bf16(acc, a0 + 2 * k, b1 + 2 * k, idesc, 1u);
-              if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b1 + 2 * k, idesc, 1u);
+          for (int x = 0; x < KBOX; ++x) {
+            const uint64_t a0 = sw128_desc(st + x * BOX_BYTES);
+            const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES + x * BOX_BYTES) : 0ull;
+            const uint64_t b0 = sw128_desc(st + NACC * A_BYTES + x * (b_bytes / KBOX));
+            const uint64_t b1 = sw128_desc(st + NACC * A_BYTES + b_bytes + x * (b_bytes / KBOX));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
+              const uint32_t accf = (i > 0 || x > 0 || k > 0) ? 1u : 0u;
+              mma_bf16(acc, a0 + 2 * k, b0 + 2 * k, idesc, accf);
+              if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
+              if (has_lo) {
+                mma_bf16(acc, a0 + 2 * k, b1 + 2 * k, idesc, 1u);
+                if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b1 + 2 * k, idesc, 1u);
+              }
             }
           }
           mma_commit(&empty[s]);  // smem slot free once these MMAs have read it
@@ -355,13 +372,15 @@ bool make_tmap(void* map, const void* base, uint64_t rows, uint64_t K, uint32_t 
 
 size_t gemm_workspace_bytes(int num_sms) { return (size_t)num_sms * 2 * 2 * 256 * 128 * sizeof(float); }
 
-cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void* tmBlo, const GemmArgs& g, int MP,
-                 int num_sms, size_t smem_budget, cudaStream_t st) {
-  if (MP < 16 || MP > 256 || MP % 16) return cudaErrorInvalidValue;
-  const bool dual = tmA1 != nullptr;
-  const int NACC = dual ? 2 : 1;
-  const int NB = tmBlo ? 2 : 1;
-  const size_t stage_bytes = ((size_t)NACC * 16384 + (size_t)NB * MP * 128 + 1023) & ~(size_t)1023;
+int g_gemm_kbox = 2;  // 64-wide K boxes per stage (SIRIUS_GEMM_KBOX)
+
+template <bool DUAL, int KBOX>
+static cudaError_t gemm_k(const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b, const CUtensorMap* blo,
+                          GemmArgs g, int MP, int num_sms, size_t smem_budget, int has_lo, cudaStream_t st) {
+  const int NACC = DUAL ? 2 : 1;
+  const int NB = has_lo ? 2 : 1;
+  g.kb = (g.K + 64 * KBOX - 1) / (64 * KBOX);
+  const size_t stage_bytes = ((size_t)KBOX * (NACC * 16384 + (size_t)NB * MP * 128) + 1023) & ~(size_t)1023;
   const size_t extra = 1024 + 512;
   int stages = (int)((smem_budget - extra) / stage_bytes);
   if (stages > 8) stages = 8;
@@ -369,23 +388,36 @@ cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void
   const size_t smem = (size_t)stages * stage_bytes + extra;
   const long long W = (long long)g.n_tiles * g.kb;
   const int grid = (int)(W < num_sms ? W : num_sms);
+  auto kern = gemm_tc_kernel<DUAL, KBOX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_chain(kern, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, *blo, g, MP, stages, has_lo);
+}
+
+cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void* tmBlo, const GemmArgs& g, int MP,
+                 int num_sms, size_t smem_budget, cudaStream_t st) {
+  if (MP < 16 || MP > 256 || MP % 16) return cudaErrorInvalidValue;
+  const bool dual = tmA1 != nullptr;
   const CUtensorMap* a0 = reinterpret_cast<const CUtensorMap*>(tmA0);
   const CUtensorMap* a1 = reinterpret_cast<const CUtensorMap*>(dual ? tmA1 : tmA0);
   const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmB);
   const CUtensorMap* blo = reinterpret_cast<const CUtensorMap*>(tmBlo ? tmBlo : tmB);
   const int has_lo = tmBlo ? 1 : 0;
+  // KBOX boxes per stage need room for >= 2 stages (dual operands at large MP fall back to fewer)
+  auto fits = [&](int kb) {
+    return (size_t)kb * ((dual ? 2 : 1) * 16384 + (has_lo ? 2 : 1) * MP * 128) * 2 + 1536 <= smem_budget;
+  };
+  int kbox = 1;
+  if (g_gemm_kbox >= 4 && fits(4)) kbox = 4;
+  else if (g_gemm_kbox >= 2 && fits(2)) kbox = 2;
   if (dual) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return launch_chain(gemm_tc_kernel<true>, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
-                        has_lo);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return launch_chain(gemm_tc_kernel<false>, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, *blo, g, MP, stages,
-                        has_lo);
+    if (kbox == 4) return gemm_k<true, 4>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
+    if (kbox == 2) return gemm_k<true, 2>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
+    return gemm_k<true, 1>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
   }
-  return cudaGetLastError();
+  if (kbox == 4) return gemm_k<false, 4>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
+  if (kbox == 2) return gemm_k<false, 2>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
+  return gemm_k<false, 1>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
 }
 
 }  // namespace launch

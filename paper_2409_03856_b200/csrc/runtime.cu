@@ -30,6 +30,7 @@ bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms);
 int decode_step_splits(int B, int KV, int num_sms);
 cudaError_t decode_step(const StepArgs& a, int B, int grid, cudaStream_t st);
 bool attn_stage_supported(int hd, int G);
+extern int g_gemm_kbox;
 cudaError_t attn_stage(const StepArgs& a, int l, int B, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius
@@ -483,6 +484,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   c->attn_stage_splits = launch::decode_step_splits(cf.batch, c->KVr, c->num_sms);
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
+  if (const char* e = getenv("SIRIUS_GEMM_KBOX")) launch::g_gemm_kbox = atoi(e);
   auto cleanup_fail = [&](sirius_status s) {
     sirius_destroy(c);
     return s;
