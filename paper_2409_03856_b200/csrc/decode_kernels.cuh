@@ -39,6 +39,8 @@ struct GemvArgs {
   int finalize;                 // EPI_ARGMAX: last CTA converts amax -> token_out and resets amax
   unsigned* done_counter;       // EPI_ARGMAX + finalize
   int32_t* token_out;           // EPI_ARGMAX + finalize: [B]
+  float* zero_out;              // if non-NULL: the grid zeroes zero_n floats here (the next FFN's accumulator)
+  int zero_n;
 };
 
 // ---- fused CATS FFN (gate GEMV + SiLU + threshold + ballot compaction + up/down gathers)
@@ -56,6 +58,7 @@ struct FfnArgs {
   int n_active_stride;
   float* gate_out;         // [B * gate_stride] (+layer*F) or NULL: a = SiLU(g)
   long long gate_stride;
+  int atomic_out;          // 1: partials added into out (pre-zeroed) with float4 atomics, no grid barrier
 };
 
 // ---- decode attention (RoPE + KV append + split-K flash decode + last-CTA combine)

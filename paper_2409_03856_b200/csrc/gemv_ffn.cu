@@ -52,6 +52,11 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
   // it); afterwards each row's loads go out before the previous row's reduction
   RowRegs<CPL> pf;
   row_issue<CPL>(pf, a.W + (size_t)(r0 + warp) * K, CH, lane, r0 + warp < r1, pol);
+  if (a.zero_out) {  // the next FFN's accumulator (its previous contents were consumed upstream)
+    const int z0 = (int)((long long)a.zero_n * blockIdx.x / gridDim.x);
+    const int z1 = (int)((long long)a.zero_n * (blockIdx.x + 1) / gridDim.x);
+    for (int i = z0 + tid; i < z1; i += blockDim.x) a.zero_out[i] = 0.f;
+  }
   constexpr int MG = CPL / 4 > 0 ? CPL / 4 : 1;  // prologue float4 groups per thread (K <= 256 CPL)
   prologue<B, MG>(a.pro, K, h_s, red_s, blockIdx.x == 0);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
@@ -230,6 +235,26 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
         }
       }
     }
+  }
+  if (a.atomic_out) {  // ---- partials added into out (zeroed by the O-proj GEMV); order varies run to run
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int ch = tid + NT * j;
+      if (ch < CH && nact > 0) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          float4* dst = reinterpret_cast<float4*>(a.out + (size_t)b * d + ch * 8);
+          atomicAdd(dst, make_float4(y[b][j * 8 + 0], y[b][j * 8 + 1], y[b][j * 8 + 2], y[b][j * 8 + 3]));
+          atomicAdd(dst + 1, make_float4(y[b][j * 8 + 4], y[b][j * 8 + 5], y[b][j * 8 + 6], y[b][j * 8 + 7]));
+        }
+      }
+    }
+    if (a.n_active_out && tid < B) {
+      int cnt = 0;
+      for (int c = 0; c < nch; ++c) cnt += __popc(act_s[c][tid]);
+      if (cnt) atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, cnt);
+    }
+    return;
   }
   // ---- per-CTA partials -> grid barrier -> deterministic column reduction
 #pragma unroll

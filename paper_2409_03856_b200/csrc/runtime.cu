@@ -112,6 +112,7 @@ struct sirius_ctx {
   int num_sms = 148;
   size_t smem_optin = 0;
   int attn_splits = 1;
+  bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   bool attn_stage = false;  // decode attention as the 512-thread item kernel (SIRIUS_ATTN_STAGE=0: old kernel)
   int attn_stage_splits = 1;
   int accept_splits = 8;
@@ -481,6 +482,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   c->attn_splits = launch::attn_splits(cf.batch, c->KVr, c->num_sms);  // ~one wave of split CTAs
   c->attn_stage = launch::attn_stage_supported(cf.head_dim, c->G);
   if (const char* e = getenv("SIRIUS_ATTN_STAGE")) c->attn_stage = c->attn_stage && atoi(e) != 0;
+  if (const char* e = getenv("SIRIUS_FFN_ATOMIC")) c->ffn_atomic = atoi(e) != 0;
   c->attn_stage_splits = launch::decode_step_splits(cf.batch, c->KVr, c->num_sms);
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
@@ -840,6 +842,10 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       o.epi = EPI_STORE;
       o.out = R.dA;
       o.ldo = d;
+      if (c->ffn_atomic) {  // zero the FFN accumulator dF (the QKV prologue above consumed it)
+        o.zero_out = R.dF;
+        o.zero_n = B * d;
+      }
       prof_begin(c, P_OPROJ);
       OK(run_gemv(c, o, B));
       prof_end(c);
@@ -866,6 +872,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       f.out = R.dF;
       f.n_active_out = n_active_out ? n_active_out + l : nullptr;
       f.n_active_stride = L;
+      f.atomic_out = c->ffn_atomic ? 1 : 0;
       if (gate_act_out) {  // [B, L, F] (emulated group: rank shards concatenated) or [B, L, F/tp]
         const int F = c->emulated ? cf.ffn_dim : c->Fr;
         f.gate_out = gate_act_out + (size_t)l * F + (c->emulated ? (size_t)R.rank * c->Fr : 0);
