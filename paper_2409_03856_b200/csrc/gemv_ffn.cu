@@ -111,8 +111,12 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
 }
 
 // ===================================================================== fused CATS FFN
-template <int B, int CPL, int CPT>
-__global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
+// NW warps per CTA: 16 with one CTA per SM (deterministic mode: cooperative grid barrier + column
+// reduction), 8 with several small CTAs per SM (atomic mode: the hardware scheduler balances the
+// data-dependent up/down work across SMs and one CTA's prologue overlaps another's weight stream).
+template <int B, int CPL, int CPT, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a) {
+  constexpr int kFfnWarps = NW;
   extern __shared__ __align__(16) float h_s[];  // [B][2][CH] float4
   __shared__ float red_s[32];
   __shared__ float a_s[B][kFfnMaxN];            // a = SiLU(g) of the CTA's neurons
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(kFfnWarps * 32, 1) ffn_kernel(FfnArgs a) {
   const uint64_t pol = policy_evict_first();
   RowRegs<CPL> pf;  // first gate row of the warp, requested before the activation prologue
   row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn, pol);
-  constexpr int MG = CPL / 8 > 0 ? CPL / 8 : 1;  // prologue float4 groups per thread (d <= 512 CPL)
+  constexpr int MG = CPL * 2 / NW > 0 ? CPL * 2 / NW : 1;  // prologue float4 groups per thread (d = 256 CPL)
   prologue<B, MG>(a.pro, d, h_s, red_s, cta == 0);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
   const float t = a.dense ? 0.f : *a.threshold;
@@ -344,35 +348,45 @@ int ffn_grid(int F, int num_sms) {
   return g;
 }
 
-template <int B, int CPL, int CPT>
+template <int B, int CPL, int CPT, int NW>
 static cudaError_t ffn_bc(const FfnArgs& a, int grid, cudaStream_t st) {
-  auto kern = ffn_kernel<B, CPL, CPT>;
+  auto kern = ffn_kernel<B, CPL, CPT, NW>;
   const size_t smem = (size_t)B * a.d * 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kFfnWarps * 32);
+  cfg.blockDim = dim3(NW * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier (deterministic mode)
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.atomic_out ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <int B>
 static cudaError_t ffn_b(const FfnArgs& a, int grid, cudaStream_t st) {
   const int CH = a.d / 8;
-  const int cpl = (CH + 31) / 32, cpt = (CH + kFfnWarps * 32 - 1) / (kFfnWarps * 32);
-  if (cpl <= 1) return ffn_bc<B, 1, 1>(a, grid, st);
-  if (cpl <= 2) return ffn_bc<B, 2, 1>(a, grid, st);
-  if (cpl <= 4) return ffn_bc<B, 4, 1>(a, grid, st);
-  if (cpl <= 8) return ffn_bc<B, 8, 1>(a, grid, st);
-  if (cpl <= 16) return ffn_bc<B, 16, 1>(a, grid, st);  // d = 4096
-  if (cpl <= 32 && cpt <= 2) return ffn_bc<B, 32, 2>(a, grid, st);  // d = 8192
+  const int cpl = (CH + 31) / 32;
+  if (a.atomic_out) {  // 8 warps: CPT = d / 2048 column chunks per thread
+    if (cpl <= 1) return ffn_bc<B, 1, 1, 8>(a, grid, st);
+    if (cpl <= 2) return ffn_bc<B, 2, 1, 8>(a, grid, st);
+    if (cpl <= 4) return ffn_bc<B, 4, 1, 8>(a, grid, st);
+    if (cpl <= 8) return ffn_bc<B, 8, 1, 8>(a, grid, st);
+    if (cpl <= 16) return ffn_bc<B, 16, 2, 8>(a, grid, st);  // d = 4096
+    if (cpl <= 32) return ffn_bc<B, 32, 4, 8>(a, grid, st);  // d = 8192
+    return cudaErrorInvalidValue;
+  }
+  const int cpt = (CH + 16 * 32 - 1) / (16 * 32);
+  if (cpl <= 1) return ffn_bc<B, 1, 1, 16>(a, grid, st);
+  if (cpl <= 2) return ffn_bc<B, 2, 1, 16>(a, grid, st);
+  if (cpl <= 4) return ffn_bc<B, 4, 1, 16>(a, grid, st);
+  if (cpl <= 8) return ffn_bc<B, 8, 1, 16>(a, grid, st);
+  if (cpl <= 16) return ffn_bc<B, 16, 1, 16>(a, grid, st);  // d = 4096
+  if (cpl <= 32 && cpt <= 2) return ffn_bc<B, 32, 2, 16>(a, grid, st);  // d = 8192
   return cudaErrorInvalidValue;
 }
 

@@ -112,7 +112,8 @@ struct sirius_ctx {
   int num_sms = 148;
   size_t smem_optin = 0;
   int attn_splits = 1;
-  bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
+  bool ffn_atomic = true;
+  int ffn_split = 2;  // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   bool attn_stage = false;  // decode attention as the 512-thread item kernel (SIRIUS_ATTN_STAGE=0: old kernel)
   int attn_stage_splits = 1;
   int accept_splits = 8;
@@ -483,6 +484,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   c->attn_stage = launch::attn_stage_supported(cf.head_dim, c->G);
   if (const char* e = getenv("SIRIUS_ATTN_STAGE")) c->attn_stage = c->attn_stage && atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_FFN_ATOMIC")) c->ffn_atomic = atoi(e) != 0;
+  if (const char* e = getenv("SIRIUS_FFN_SPLIT")) c->ffn_split = std::max(1, atoi(e));
   c->attn_stage_splits = launch::decode_step_splits(cf.batch, c->KVr, c->num_sms);
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
@@ -879,7 +881,8 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
         f.gate_stride = (long long)L * F;
       }
       prof_begin(c, P_FFN);
-      LCU(launch::ffn(f, B, ffn_grid, c->stream));
+      LCU(launch::ffn(f, B, c->ffn_atomic ? std::min((c->Fr + 7) / 8, c->ffn_split * c->num_sms) : ffn_grid,
+                      c->stream));
       prof_end(c);
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
