@@ -112,8 +112,8 @@ struct sirius_ctx {
   int num_sms = 148;
   size_t smem_optin = 0;
   int attn_splits = 1;
-  bool ffn_atomic = true;
-  int ffn_split = 2;  // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
+  bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
+  int ffn_split = 2;       // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)
   bool attn_stage = false;  // decode attention as the 512-thread item kernel (SIRIUS_ATTN_STAGE=0: old kernel)
   int attn_stage_splits = 1;
   int accept_splits = 8;
