@@ -32,6 +32,16 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 WORKLOAD = "llama3-8b-shape random-init bf16, batch 1, prompt 900, CATS 50% FFN density, gamma 16, r 0.1"
+METRIC = "decode ms/token (Sirius; dense and CS-only beside it), Llama-3-8B shape"
+
+
+def bench_config(a, world):
+    """The workload description shared by both arms (BASELINE.json configs[1] by default)."""
+    B = a.batch
+    return {"workload": WORKLOAD if B == 1 else WORKLOAD.replace("batch 1", f"batch {B}"), "model": a.model,
+            "batch": B, "prompt": a.prompt, "gamma": a.gamma, "r": a.r, "rho_target": a.rho,
+            "parallelism": f"tp{world}",
+            "l2": "weights (15 GB) >> 126 MB L2: every step streams from HBM, no flush needed"}
 
 
 def parse():
@@ -169,10 +179,10 @@ def run_reference(a):
     sample = (f"per step: one gamma={a.gamma} Sirius kernel ({a.gamma - 1} CATS-sparse rows + {a.gamma} dense verify "
               f"rows) of the {a.model} shape, oracle timed on its 2-layer truncation + head-only model and "
               f"scaled to {cfg.n_layers} layers; advance taken as gamma (upper bound)")
-    out = {"metric": "decode ms/token (Sirius, Llama-3-8B shape)", "value": v, "unit": "ms/token",
+    out = {"metric": METRIC, "value": v, "unit": "ms/token",
            "impl": "reference", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": v * a.gamma,
            "higher_is_better": False, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "model": a.model},
+           "config": bench_config(a, int(os.environ.get("WORLD_SIZE", "1"))),
            "cpu_baseline": {"value": v, "unit": "ms/token", "cores": s["threads"], "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "wall_s": time.perf_counter() - t_start}
@@ -351,14 +361,11 @@ def main():
                "row_sparse_s": s["row_sparse_s"], "row_dense_s": s["row_dense_s"]}
     if rank == 0:
         out = {
-            "metric": "decode ms/token (Sirius; dense and CS-only beside it), Llama-3-8B shape",
+            "metric": METRIC,
             "value": sirius_ms_tok, "unit": "ms/token", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": t_ms / a.steps, "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD if B == 1 else WORKLOAD.replace("batch 1", f"batch {B}"), "model": a.model,
-                       "batch": B, "prompt": a.prompt, "gamma": a.gamma,
-                       "r": a.r, "rho_target": a.rho, "parallelism": f"tp{world}",
-                       "l2": "weights (15 GB) >> 126 MB L2: every step streams from HBM, no flush needed"},
+            "config": bench_config(a, world),
             "sirius": {"ms_per_token": sirius_ms_tok, "aal": aal,
                        "advances": advances if B > 1 else [v[0] for v in advances],
                        "tokens_per_s": 1e3 / sirius_ms_tok, "tokens_per_s_aggregate": B * 1e3 / sirius_ms_tok,

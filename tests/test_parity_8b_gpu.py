@@ -261,3 +261,21 @@ def test_tiny_batch8_per_sequence_sets():
     refs = [oracle_script(cfg, wh, thr, p, 2, 8, 256) for p in prompts]
     ctx = make_ctx(cfg, sg.device_weights(cfg), thr, 8, 256)
     gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
+
+
+# ------------------------------------------------------------------ Llama-3-70B per-layer shapes
+@pytest.mark.parametrize("tp", [1, 8])
+def test_70b_1l_decode_verify(tp):
+    """Llama-3-70B per-layer shapes (d 8192, ffn 28672, GQA group 8): the d = 8192 kernel variants
+    (two-chunk row loads, 8-head attention groups), TP 1 and the per-rank shapes of BASELINE
+    configs[3] (TP 8: 8 q heads, 1 kv head, 3584 neurons, 16032 vocab rows per rank) emulated."""
+    from synth import gpu as sg
+    cfg = synth.LLAMA3_70B.with_layers(1)
+    wh = synth.host_weights(cfg)
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 4, 37)]
+    refs = [oracle_script(cfg, wh, thr, prompts[0], 2, 8, 128)]
+    del wh
+    w = sg.device_weights(cfg) if tp == 1 else [sg.device_weights(cfg, tp, r) for r in range(tp)]
+    ctx = make_ctx(cfg, w, thr, 1, 128, tp=tp)
+    gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
