@@ -40,13 +40,16 @@ using namespace sirius;
 // ----------------------------------------------------------------------------- NCCL (dlopen'd)
 namespace {
 typedef int ncclResult_t_;
+struct NcclUid {  // ncclUniqueId: passed BY VALUE to ncclCommInitRank (a 128-byte struct, not a pointer)
+  char internal[128];
+};
 struct NcclApi {
   bool loaded = false;
   ncclResult_t_ (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   ncclResult_t_ (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t_) = nullptr;
   ncclResult_t_ (*getUniqueId)(void*) = nullptr;
-  ncclResult_t_ (*commInitRank)(void**, int, char[128], int) = nullptr;
+  ncclResult_t_ (*commInitRank)(void**, int, NcclUid, int) = nullptr;
   ncclResult_t_ (*commDestroy)(void*) = nullptr;
 };
 // nccl.h enum values (stable ABI): ncclUint8 = 1... ncclUint64 = 5, ncclFloat32 = 7; ncclSum = 0, ncclMax = 2
@@ -1066,8 +1069,8 @@ int sirius_nccl_unique_id(void* out128) {
 int sirius_nccl_comm_init(int nranks, const void* id128, int rank, void** comm_out) {
   NcclApi& api = nccl();
   if (!api.loaded) return -1;
-  char id[128];
-  memcpy(id, id128, 128);
+  NcclUid id;
+  memcpy(id.internal, id128, 128);
   return api.commInitRank(comm_out, nranks, id, rank);
 }
 int sirius_nccl_comm_destroy(void* comm) {

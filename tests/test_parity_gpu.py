@@ -225,3 +225,19 @@ def test_r_zero_accepts_all_on_gpu(tiny_models):
     d = driver.Driver(make_ctx(cfg, wd, thr))
     out = d.sirius([synth.eval_prompt(cfg, 7, 32)], 24, 5, 0.0)
     assert all(a == 5 for a in out.advances(0))
+
+
+def test_nccl_bootstrap_single_rank():
+    """The TP > 1 bootstrap through the library (paper_2409_03856_b200/tp.py): ncclGetUniqueId and
+    ncclCommInitRank (whose 128-byte id is passed by value) on a 1-rank communicator."""
+    import ctypes
+    from paper_2409_03856_b200 import sirius as S
+    lib = S.load()
+    if lib.sirius_nccl_available() != 1:
+        pytest.skip("libnccl.so.2 not loadable")
+    uid = (ctypes.c_char * 128)()
+    assert lib.sirius_nccl_unique_id(uid) == 0
+    comm = ctypes.c_void_p()
+    assert lib.sirius_nccl_comm_init(1, uid, 0, ctypes.byref(comm)) == 0
+    assert comm.value
+    assert lib.sirius_nccl_comm_destroy(comm) == 0
