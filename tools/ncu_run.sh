@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${TAG}.csv python tools/profile_step.py --kernels 2 > /dev/null 2>&1
 # full sections for the top decode kernels (a few launches each, after the prefill + warm-up launches)
-for K in ffn_kernel gemv_kernel attn_decode_kernel; do
+for K in ffn_kernel gemv_kernel attn_stage_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:${K} -s 200 -c 2 \
     -o gpurun_out/prof_${TAG}_${K} python tools/profile_step.py --kernels 1 > gpurun_out/ncu_${K}.log 2>&1
 done
