@@ -22,7 +22,8 @@ UNIT = {"duration": {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "nsecond": 1e-9, "
 
 
 def short(name):
-    n = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("sirius::", "").replace("void ", "")
+    n = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
+    n = n.replace("sirius::", "").replace("void ", "")
     return n.split("<")[0].split("(")[0]
 
 
