@@ -114,6 +114,7 @@ struct sirius_ctx {
   int Hr = 0, KVr = 0, Fr = 0, Vr = 0, Nqkv = 0, G = 0, MAXM = 0;
   int num_sms = 148;
   size_t smem_optin = 0;
+  size_t gemm_smem = 0;
   int attn_splits = 1;
   bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   int ffn_split = 2;       // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)
@@ -322,7 +323,7 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
   g.part = R.gemm_part;
   g.counters = R.gemm_cnt;
   const int MP = round_up(M, 16);
-  LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms, c->smem_optin, c->stream));
+  LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms, c->gemm_smem, c->stream));
   return SIRIUS_OK;
 }
 
@@ -476,6 +477,8 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   c->smem_optin = (size_t)optin - 1024;  // keep room for static shared memory
+  c->gemm_smem = c->smem_optin;            // verify GEMM pipeline budget (SIRIUS_GEMM_SMEM_KB caps it)
+  if (const char* e = getenv("SIRIUS_GEMM_SMEM_KB")) c->gemm_smem = std::min(c->smem_optin, (size_t)atoi(e) * 1024);
   int major = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   if (major != 10) {
