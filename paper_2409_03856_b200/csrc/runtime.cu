@@ -323,7 +323,8 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
   g.part = R.gemm_part;
   g.counters = R.gemm_cnt;
   const int MP = round_up(M, 16);
-  LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms, c->gemm_smem, c->stream));
+  LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms,
+                   MP <= 64 ? c->gemm_smem : c->smem_optin, c->stream));
   return SIRIUS_OK;
 }
 
