@@ -190,10 +190,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   __syncthreads();
   const int nact = off_s[nch];
   // ---- C: active up rows only: u = h2 . W_up[n];  m = a * u  (inactive (b, n) pairs contribute 0)
+  // (each warp's next up row requested before the current row's reduction, as for the gate rows)
+  row_issue<CPL>(pf, a.w_up + (size_t)(n0 + list_s[warp < nact ? warp : 0]) * d, CH, lane, warp < nact, pol);
   for (int k = warp; k < nact; k += kFfnWarps) {
     const int i = list_s[k];
     float acc[B];
-    row_dot<B, CPL>(a.w_up + (size_t)(n0 + i) * d, hp, CH, lane, acc, pol);
+    row_finish<B, CPL>(pf, a.w_up + (size_t)(n0 + i) * d, hp, CH, lane, acc);
+    const int kn = k + kFfnWarps < nact ? k + kFfnWarps : k;
+    row_issue<CPL>(pf, a.w_up + (size_t)(n0 + list_s[kn]) * d + after_all<B>(acc), CH, lane, k + kFfnWarps < nact,
+                   pol);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float u = warp_sum(acc[b]);
