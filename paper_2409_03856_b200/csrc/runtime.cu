@@ -493,6 +493,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   if (const char* e = getenv("SIRIUS_FFN_ATOMIC")) c->ffn_atomic = atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_FFN_SPLIT")) c->ffn_split = std::max(1, atoi(e));
   c->attn_stage_splits = launch::decode_step_splits(cf.batch, c->KVr, c->num_sms);
+  if (const char* e = getenv("SIRIUS_ATTN_SPLITS")) c->attn_stage_splits = std::max(1, std::min(64, atoi(e)));
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_GEMM_KBOX")) launch::g_gemm_kbox = atoi(e);
