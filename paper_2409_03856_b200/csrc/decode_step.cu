@@ -200,7 +200,10 @@ SIRIUS_DEV void attn_load_block(const StepArgs& a, int l, const AttnItem& it, in
   }
 }
 
-template <int B, int HD, int G>
+// L1OK: the combine may read the (M_s, L_s) partials through L1 — only in the one-launch-per-layer
+// item kernel (L1 does not survive kernel boundaries); the persistent step kernel reuses the
+// partial buffer every layer within one launch, so it bypasses L1.
+template <int B, int HD, int G, bool L1OK>
 SIRIUS_DEV void attention_phase(const StepArgs& a, int l, StepSmem<B, HD, G>& sm, const AttnItem& it, uint4* kv,
                                 uint4* vv) {
   constexpr int ROWB = HD * 2 + 16;  // padded K row (bytes): conflict-free row reads
@@ -368,8 +371,9 @@ SIRIUS_DEV void attention_phase(const StepArgs& a, int l, StepSmem<B, HD, G>& sm
       for (int u = 0; u < 32; ++u) {
         const float* ps = pb + ((size_t)(sp0 + u) * G + g) * (HD + 2);
         const bool ok = sp0 + u < s_active;
-        mv[u] = ok ? __ldcg(ps) : -INFINITY;
-        lv[u] = ok ? __ldcg(ps + 1) : 0.f;
+        // (M_s, L_s) are shared by the HD threads of a head (L1-cached where that is safe)
+        mv[u] = ok ? (L1OK ? __ldca(ps) : __ldcg(ps)) : -INFINITY;
+        lv[u] = ok ? (L1OK ? __ldca(ps + 1) : __ldcg(ps + 1)) : 0.f;
         av[u] = ok ? __ldcg(ps + 2 + dd) : 0.f;
       }
       float Mb = M;
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(kNT, 1) decode_step_kernel(StepArgs a) {
     grid_sync(a.grid_bar, Gd);
     stamp(a, l * kTraceSlots + 2);
     // ---------------- P2: attention (RoPE, K/V append, split-K, last-split combine)
-    attention_phase<B, HD, G>(a, l, sm, it, kv, vv);
+    attention_phase<B, HD, G, false>(a, l, sm, it, kv, vv);
     rs_start<CPL, RING>(st, no, o_row(l), CH, lane);
     stamp(a, l * kTraceSlots + 6);
     grid_sync(a.grid_bar, Gd);
@@ -721,7 +725,7 @@ __global__ void __launch_bounds__(kNT, 1) attn_stage_kernel(StepArgs a, int l) {
   constexpr int NL = kKB * HD / 8 / kNT > 0 ? kKB * HD / 8 / kNT : 1;
   uint4 kv[NL], vv[NL];
   if (it.active && it.k0 < it.k1) attn_load_block<HD>(a, l, it, it.k0, kv, vv);
-  attention_phase<B, HD, G>(a, l, sm, it, kv, vv);
+  attention_phase<B, HD, G, true>(a, l, sm, it, kv, vv);
 }
 
 template <int B, int HD, int G>
