@@ -77,7 +77,11 @@ template <bool DUAL>
 SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
   if (j >= g.M || n >= g.N) return;
   if (DUAL) {
-    const float m = v0 / (1.0f + expf(-v0)) * v1;  // SiLU(gate) * up
+    const float av = v0 / (1.0f + expf(-v0));  // a = SiLU(gate)
+    const bool on = !g.thr || fabsf(av) >= *g.thr;
+    const float m = on ? av * v1 : 0.f;        // a * up, CATS-masked (inactive pairs contribute exact 0)
+    if (g.gate_out) g.gate_out[(size_t)j * g.gate_stride + n] = av;
+    if (g.n_active && on) atomicAdd(g.n_active + (size_t)j * g.n_active_stride, 1);
     const uint16_t hi = f2bf_bits(m);
     reinterpret_cast<uint16_t*>(g.out)[(size_t)j * g.ldc + n] = hi;
     reinterpret_cast<uint16_t*>(g.out2)[(size_t)j * g.ldc + n] = f2bf_bits(m - __uint_as_float((uint32_t)hi << 16));

@@ -15,6 +15,13 @@ struct GemmArgs {
   float* part;          // stream-K partials [num_sms, 2, NACC, 256, 128]
   unsigned* counters;   // [n_tiles] (self-resetting)
   unsigned long long* trace;  // debug: [8][grid] %globaltimer stamps of thread 0 / the MMA thread, or NULL
+  // dual (SwiGLU) epilogue only: CATS mask of the batched sparse decode — m = 0 unless
+  // |SiLU(g)| >= *thr (thr NULL: dense); optional per-row active counts and a = SiLU(g) export
+  const float* thr;
+  int* n_active;           // [M rows] stride n_active_stride, or NULL
+  int n_active_stride;
+  float* gate_out;         // [M rows] stride gate_stride, or NULL
+  long long gate_stride;
 };
 
 namespace launch {

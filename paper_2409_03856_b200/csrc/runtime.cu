@@ -118,6 +118,8 @@ struct sirius_ctx {
   int attn_splits = 1;
   bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   int ffn_split = 2;       // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)
+  bool decode_rows = false;  // batched decode through the tensor-core row path (batch >= 8; SIRIUS_DECODE_ROWS)
+  int32_t* dec_nacc = nullptr;
   bool attn_stage = false;  // decode attention as the 512-thread item kernel (SIRIUS_ATTN_STAGE=0: old kernel)
   int attn_stage_splits = 1;
   int accept_splits = 8;
@@ -307,11 +309,26 @@ sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
   return SIRIUS_OK;
 }
 
+struct GemmMask {  // CATS mask of the dual (SwiGLU) GEMM in the batched sparse decode
+  const float* thr = nullptr;
+  int* n_active = nullptr;
+  int n_active_stride = 0;
+  float* gate_out = nullptr;
+  long long gate_stride = 0;
+};
+
 sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x_hi,
                        const TmapBuf& x_lo, int N, int K, int M, void* out, int ldc, void* out2 = nullptr,
-                       unsigned long long* trace = nullptr) {
+                       unsigned long long* trace = nullptr, const GemmMask* mask = nullptr) {
   GemmArgs g = {};
   g.trace = trace;
+  if (mask) {
+    g.thr = mask->thr;
+    g.n_active = mask->n_active;
+    g.n_active_stride = mask->n_active_stride;
+    g.gate_out = mask->gate_out;
+    g.gate_stride = mask->gate_stride;
+  }
   g.N = N;
   g.K = K;
   g.M = M;
@@ -331,9 +348,11 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
 // ---- the dense / verify / prefill forward over M token rows (chunk).  Rows are ordered
 // (sequence, i); rows_per_seq rows per sequence, sequences b_base .. b_base + nseq - 1.
 // to_cache: prefill (K/V -> cache at start[b] + i, attention reads the cache only).
+// sparse: CATS mask on the FFN (batched sparse decode, rows_per_seq = 1); n_active_out [rows, L] and
+// gate_act_out [rows, L, ffn] (emulated TP: rank shards concatenated) optional.
 sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* start, int b_base, int nseq,
-                           int rows_per_seq, bool to_cache, int l_dummy = 0) {
-  (void)l_dummy;
+                           int rows_per_seq, bool to_cache, bool sparse = false, int32_t* n_active_out = nullptr,
+                           float* gate_act_out = nullptr) {
   const sirius_config& cf = c->cfg;
   const int M = nseq * rows_per_seq, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   for (int l = 0; l < L; ++l) {
@@ -418,8 +437,19 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.out_lo = R.xn_lo;
       LCU(launch::norm_rows(na, M, c->stream));
       unsigned long long* gtr2 = (!to_cache && l == c->trace_layer && c->trace) ? c->trace + 3 * 8 * 1024 : nullptr;
+      GemmMask mk;
+      if (sparse) mk.thr = c->thresholds + l;
+      if (n_active_out) {
+        mk.n_active = n_active_out + l;
+        mk.n_active_stride = L;
+      }
+      if (gate_act_out) {
+        const int Ff = c->emulated ? cf.ffn_dim : c->Fr;
+        mk.gate_out = gate_act_out + (size_t)l * Ff + (c->emulated ? (size_t)R.rank * c->Fr : 0);
+        mk.gate_stride = (long long)L * Ff;
+      }
       OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn_hi, R.tm_xn_lo, c->Fr, d, M, R.mb_hi, c->Fr, R.mb_lo,
-                  gtr2));
+                  gtr2, &mk));
       OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb_hi, R.tm_mb_lo, d, c->Fr, M, R.dF, d, nullptr,
                   gtr2 ? gtr2 + 8 * 1024 : nullptr));
     }
@@ -453,7 +483,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   if (cf.d_model % 256 || ((cf.n_heads / cf.tp_size) * cf.head_dim) % 64 || (cf.ffn_dim / cf.tp_size) % 8)
     return SIRIUS_ERR_UNSUPPORTED;
   if (cf.max_gamma > 64 || (long)cf.batch * cf.max_gamma > 256) return SIRIUS_ERR_UNSUPPORTED;
-  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4 && cf.batch != 8) return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4 && cf.batch != 8 && cf.batch != 16) return SIRIUS_ERR_UNSUPPORTED;
   for (int l = 0; l < cf.n_layers; ++l)
     if (!(cats_threshold[l] >= 0.f)) return SIRIUS_ERR_INVALID_ARG;
   const bool emulate = cf.tp_size > 1 && nccl_comm == nullptr;
@@ -491,6 +521,9 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   c->attn_stage = launch::attn_stage_supported(cf.head_dim, c->G);
   if (const char* e = getenv("SIRIUS_ATTN_STAGE")) c->attn_stage = c->attn_stage && atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_FFN_ATOMIC")) c->ffn_atomic = atoi(e) != 0;
+  c->decode_rows = cf.batch >= 8;
+  if (const char* e = getenv("SIRIUS_DECODE_ROWS")) c->decode_rows = atoi(e) != 0;
+  if (cf.batch > 8) c->decode_rows = true;  // the per-stage decode kernels are instantiated up to batch 8
   if (const char* e = getenv("SIRIUS_FFN_SPLIT")) c->ffn_split = std::max(1, atoi(e));
   c->attn_stage_splits = launch::decode_step_splits(cf.batch, c->KVr, c->num_sms);
   if (const char* e = getenv("SIRIUS_ATTN_SPLITS")) c->attn_stage_splits = std::max(1, std::min(64, atoi(e)));
@@ -508,6 +541,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       alloc(c, &c->stats, (size_t)c->nranks * c->MAXM * c->accept_splits) ||
       alloc(c, &c->stats_gather, (size_t)cf.tp_size * c->MAXM * c->accept_splits) ||
       alloc(c, &c->dA_ptrs, 64) || alloc(c, &c->dF_ptrs, 64) || alloc(c, &c->pre_start, B) ||
+      alloc(c, &c->dec_nacc, B) ||
       alloc(c, &c->scratch_tok, 64))
     return cleanup_fail(SIRIUS_ERR_CUDA);
   if (cudaHostAlloc(&c->err_host, 64, cudaHostAllocDefault) != cudaSuccess ||
@@ -708,12 +742,34 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
   return SIRIUS_OK;
 }
 
+static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* tokens, int gamma, int M, float* logits_out,
+                                         int32_t* n_accept_out, int32_t* next_token_out, float* q_out,
+                                         float accept_threshold, int32_t accept_mode);
+
+// Batched decode (batch >= 8) through the tensor-core row path: one row per sequence at pos[b] (K/V
+// straight into the cache), CATS mask in the SwiGLU epilogue (sparse) — at these batch sizes the
+// union of the per-sequence active sets covers ~all neurons (SURVEY.md §7 hard part 7), so every
+// W_up / W_down row is read anyway and inactive (b, n) pairs contribute exact zeros (reading D19) —
+// then final norm + head GEMM + argmax (accept machinery with gamma = 1: next = argmax row 0).
+static sirius_status enqueue_decode_rows(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, bool dense,
+                                         int32_t* token_out, float* logits_out, int32_t* n_active_out,
+                                         float* gate_act_out) {
+  const int B = c->cfg.batch;
+  if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * c->cfg.n_layers, c->stream));
+  OK(forward_rows(c, token_in, pos, 0, B, 1, true, !dense, n_active_out, gate_act_out));
+  OK(enqueue_head_argmax(c, token_in, 1, B, logits_out, c->dec_nacc, token_out, nullptr, 0.f, 0));
+  CU(cudaGetLastError());
+  return SIRIUS_OK;
+}
+
 static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
                                     int32_t* token_out, float* logits_out, int32_t* n_active_out,
                                     float* gate_act_out) {
   const sirius_config& cf = c->cfg;
   const int B = cf.batch, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   const bool dense = flags & SIRIUS_DENSE;
+  if (c->decode_rows) return enqueue_decode_rows(c, token_in, pos, dense, token_out, logits_out, n_active_out,
+                                                 gate_act_out);
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
   if (c->use_step) {  // the whole step in one persistent launch (decode_step.cu)
     RankState& R = c->ranks[0];
@@ -949,6 +1005,21 @@ static sirius_status enqueue_correct(sirius_ctx* c, const int32_t* kernel_tokens
   const int B = cf.batch, d = cf.d_model, M = B * gamma;
   prof_begin(c, P_VERIFY);
   OK(forward_rows(c, kernel_tokens, start_pos, 0, B, gamma, false));
+  OK(enqueue_head_argmax(c, kernel_tokens, gamma, M, logits_out, n_accept_out, next_token_out, q_out,
+                         accept_threshold, accept_mode));
+  prof_end(c);
+  mirror_err(c);
+  CU(cudaGetLastError());
+  return SIRIUS_OK;
+}
+
+// final RMSNorm of the M rows + head GEMM + per-row softmax statistics (+ TP all-gather) + the accept
+// scan / interleave (gamma = 1: next = argmax of the row)
+static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* kernel_tokens, int gamma, int M,
+                                         float* logits_out, int32_t* n_accept_out, int32_t* next_token_out,
+                                         float* q_out, float accept_threshold, int32_t accept_mode) {
+  const sirius_config& cf = c->cfg;
+  const int B = cf.batch, d = cf.d_model;
   for (auto& R : c->ranks) {
     NormRowsArgs na = {};
     na.base = R.resB;
@@ -998,9 +1069,6 @@ static sirius_status enqueue_correct(sirius_ctx* c, const int32_t* kernel_tokens
   fa.next_token = next_token_out;
   fa.q_out = q_out;
   LCU(launch::accept_finalize(fa, B, c->stream));
-  prof_end(c);
-  mirror_err(c);
-  CU(cudaGetLastError());
   return SIRIUS_OK;
 }
 

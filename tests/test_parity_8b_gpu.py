@@ -279,3 +279,16 @@ def test_70b_1l_decode_verify(tp):
     w = sg.device_weights(cfg) if tp == 1 else [sg.device_weights(cfg, tp, r) for r in range(tp)]
     ctx = make_ctx(cfg, w, thr, 1, 128, tp=tp)
     gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
+
+
+@pytest.mark.parametrize("batch", [16])
+def test_8b2l_batched_decode_rows_path(l2, batch):
+    """Batched decode (batch >= 8) runs the tensor-core row path with the CATS mask in the SwiGLU
+    epilogue: per-sequence logits, active sets and decisions against the oracle at 8B shapes."""
+    from synth import gpu as sg
+    cfg, wh = l2
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 20 + b, 5 + b) for b in range(batch)]
+    refs = [oracle_script(cfg, wh, thr, p, 1, 4, 128) for p in prompts]
+    ctx = make_ctx(cfg, sg.device_weights(cfg), thr, batch, 128)
+    gpu_script(ctx, cfg, thr, prompts, refs, 1, 4)
