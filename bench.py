@@ -321,8 +321,9 @@ def main():
             traffic = summ["kernels"]["decode_step_kernel"]["dram_bytes_per_launch"]
         except Exception:
             pass
-        roof = {"bound": "hbm", "kernel": "decode_step_kernel (persistent CATS-sparse decode step: QKV, attention, "
-                "O-proj, gate+SiLU+threshold+ballot, active up/down gathers, head+argmax)",
+        roof = {"bound": "hbm", "kernel": ("decode_step_kernel (persistent CATS-sparse decode step: QKV, attention, "
+                "O-proj, gate+SiLU+threshold+ballot, active up/down gathers, head+argmax)") if B < 8 else
+                "batched decode step (row path: tcgen05 GEMMs with the CATS-masked SwiGLU epilogue, attention, head)",
                 "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                 "traffic": traffic, "algorithmic_bytes_per_launch": st_bytes, "avg_launch_us": avg_s * 1e6,
                 "launches_timed": st_n,

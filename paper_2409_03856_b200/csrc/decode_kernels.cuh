@@ -103,6 +103,7 @@ struct StepArgs {
   const float *rope_cos, *rope_sin;
   // workspace
   float *x, *x1, *qkv, *o, *attn_part, *ffn_part;
+  uint16_t *o_hi, *o_lo;  // if set: attention output as a bf16 hi/lo pair (tcgen05 operand) instead of o
   int* part_cnt;
   unsigned* group_bar;
   unsigned long long* grid_bar;  // dedicated monotone counter (nblocks = grid)

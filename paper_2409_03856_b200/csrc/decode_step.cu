@@ -390,7 +390,15 @@ SIRIUS_DEV void attention_phase(const StepArgs& a, int l, StepSmem<B, HD, G>& sm
       }
       M = Mb;
     }
-    a.o[(size_t)b * Hr * HD + (kvh * G + g) * HD + dd] = Ls > 0.f ? o / Ls : 0.f;
+    const float val = Ls > 0.f ? o / Ls : 0.f;
+    const size_t off = (size_t)b * Hr * HD + (kvh * G + g) * HD + dd;
+    if (a.o_hi) {  // the row path's O-proj GEMM operand: val = hi + lo to 2^-17
+      const uint16_t hi = f2bf_bits(val);
+      a.o_hi[off] = hi;
+      a.o_lo[off] = f2bf_bits(val - __uint_as_float((uint32_t)hi << 16));
+    } else {
+      a.o[off] = val;
+    }
   }
 }
 
@@ -745,6 +753,7 @@ cudaError_t attn_stage_b(const StepArgs& a, int l, int B, cudaStream_t st) {
     case 2: return launch_attn_stage<2, HD, G>(a, l, st);
     case 4: return launch_attn_stage<4, HD, G>(a, l, st);
     case 8: return launch_attn_stage<8, HD, G>(a, l, st);
+    case 16: return launch_attn_stage<16, HD, G>(a, l, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -377,6 +377,33 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Nqkv, d, M, R.qkv, c->Nqkv, nullptr, gtr));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
+      if (rows_per_seq == 1 && to_cache && c->attn_stage && c->decode_rows) {
+        // one query row per sequence (batched decode): the decode-attention item kernel does RoPE,
+        // the K/V append at pos and split-K attention, writing the O-proj operand as a hi/lo pair
+        StepArgs sa = {};
+        sa.d = d;
+        sa.Hr = c->Hr;
+        sa.KVr = c->KVr;
+        sa.hd = hd;
+        sa.max_seq = cf.max_seq;
+        sa.splits = c->attn_stage_splits;
+        sa.attn_scale = 1.0f / sqrtf((float)hd);
+        sa.pos = start;
+        sa.qkv = R.qkv;
+        sa.o_hi = R.ob_hi;
+        sa.o_lo = R.ob_lo;
+        sa.k_cache = R.k_cache;
+        sa.v_cache = R.v_cache;
+        sa.kv_layer = kv_layer;
+        sa.rope_cos = c->rope_cos;
+        sa.rope_sin = c->rope_sin;
+        sa.attn_part = R.attn_part;
+        sa.group_bar = R.attn_bar;
+        sa.err = c->err_dev;
+        LCU(launch::attn_stage(sa, l, cf.batch, c->stream));
+        OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d));
+        continue;
+      }
       RopeStoreArgs ra = {};
       ra.qkv = R.qkv;
       ra.start = start;
@@ -756,8 +783,10 @@ static sirius_status enqueue_decode_rows(sirius_ctx* c, const int32_t* token_in,
                                          float* gate_act_out) {
   const int B = c->cfg.batch;
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * c->cfg.n_layers, c->stream));
+  prof_begin(c, P_STEP);
   OK(forward_rows(c, token_in, pos, 0, B, 1, true, !dense, n_active_out, gate_act_out));
   OK(enqueue_head_argmax(c, token_in, 1, B, logits_out, c->dec_nacc, token_out, nullptr, 0.f, 0));
+  prof_end(c);
   CU(cudaGetLastError());
   return SIRIUS_OK;
 }
