@@ -59,6 +59,7 @@ struct FfnArgs {
   float* gate_out;         // [B * gate_stride] (+layer*F) or NULL: a = SiLU(g)
   long long gate_stride;
   int atomic_out;          // 1: partials added into out (pre-zeroed) with float4 atomics, no grid barrier
+  unsigned long long* trace;  // debug: [8][1024] %globaltimer stamps per CTA (phase boundaries), or NULL
 };
 
 // ---- decode attention (RoPE + KV append + split-K flash decode + last-CTA combine)

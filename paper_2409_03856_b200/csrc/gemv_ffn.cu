@@ -111,12 +111,23 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
 }
 
 // ===================================================================== fused CATS FFN
+SIRIUS_DEV void fstamp(const FfnArgs& a, int slot) {  // debug phase stamps (a.trace != NULL)
+  if (!a.trace) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(size_t)slot * 1024 + blockIdx.x] = t;
+  }
+}
+
 // NW warps per CTA: 16 with one CTA per SM (deterministic mode: cooperative grid barrier + column
 // reduction), 8 with several small CTAs per SM (atomic mode: the hardware scheduler balances the
 // data-dependent up/down work across SMs and one CTA's prologue overlaps another's weight stream).
 template <int B, int CPL, int CPT, int NW>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a) {
   constexpr int kFfnWarps = NW;
+  fstamp(a, 0);
   extern __shared__ __align__(16) float h_s[];  // [B][2][CH] float4
   __shared__ float red_s[32];
   __shared__ float a_s[B][kFfnMaxN];            // a = SiLU(g) of the CTA's neurons
@@ -137,6 +148,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn, pol);
   constexpr int MG = CPL * 2 / NW > 0 ? CPL * 2 / NW : 1;  // prologue float4 groups per thread (d = 256 CPL)
   prologue<B, MG>(a.pro, d, h_s, red_s, cta == 0);
+  fstamp(a, 1);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
   const float t = a.dense ? 0.f : *a.threshold;
 
@@ -153,6 +165,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
     }
   }
   __syncthreads();
+  fstamp(a, 2);
   // ---- B: CATS threshold |a| >= t and warp-ballot compaction (warp c <-> 32-neuron chunk c)
   unsigned um = 0u;
   if (warp < nch) {
@@ -189,6 +202,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   }
   __syncthreads();
   const int nact = off_s[nch];
+  fstamp(a, 3);
   // ---- C: active up rows only: u = h2 . W_up[n];  m = a * u  (inactive (b, n) pairs contribute 0)
   // (each warp's next up row requested before the current row's reduction, as for the gate rows)
   row_issue<CPL>(pf, a.w_up + (size_t)(n0 + list_s[warp < nact ? warp : 0]) * d, CH, lane, warp < nact, pol);
@@ -206,6 +220,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
     }
   }
   __syncthreads();
+  fstamp(a, 4);
   // ---- D: active down rows only: y += m * W_down[n]; thread owns column chunks tid + NT j
   // rows in flight per thread (fewer for B = 8: the y[B][.] accumulators share the registers)
   constexpr int RU = (CPT == 1 ? 16 : (CPT == 2 ? 8 : 4)) / (B >= 8 ? 2 : 1);
@@ -245,6 +260,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
       }
     }
   }
+  fstamp(a, 5);
   if (a.atomic_out) {  // ---- partials added into out (zeroed by the O-proj GEMV); order varies run to run
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
@@ -263,6 +279,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
       for (int c = 0; c < nch; ++c) cnt += __popc(act_s[c][tid]);
       if (cnt) atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, cnt);
     }
+    fstamp(a, 6);
     return;
   }
   // ---- per-CTA partials -> grid barrier -> deterministic column reduction

@@ -153,7 +153,8 @@ struct sirius_ctx {
   const uint16_t** step_w = nullptr;  // device [7][L]: attn_norm, w_qkv, w_o, ffn_norm, w_gate, w_up, w_down
   float *step_x = nullptr, *step_x1 = nullptr, *step_o = nullptr;
   unsigned long long* step_bar = nullptr;
-  int trace_layer = -1;                  // debug: attn_rows trace of this verify layer (sirius_debug_trace_verify)
+  int trace_layer = -1;
+  bool trace_ffn = false;  // debug: the trace buffer records the decode FFN of trace_layer                  // debug: attn_rows trace of this verify layer (sirius_debug_trace_verify)
   int step_tune = 1;                     // SIRIUS_STEP_TUNE (bit 0: evict-first weight loads)
   unsigned long long* trace = nullptr;  // debug: decode-step phase stamps (sirius_debug_trace)
   // CUDA graphs: every ABI call is captured once per distinct argument set and replayed
@@ -968,6 +969,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       f.n_active_out = n_active_out ? n_active_out + l : nullptr;
       f.n_active_stride = L;
       f.atomic_out = c->ffn_atomic ? 1 : 0;
+      f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
       if (gate_act_out) {  // [B, L, F] (emulated group: rank shards concatenated) or [B, L, F/tp]
         const int F = c->emulated ? cf.ffn_dim : c->Fr;
         f.gate_out = gate_act_out + (size_t)l * F + (c->emulated ? (size_t)R.rank * c->Fr : 0);
@@ -1199,6 +1201,16 @@ int sirius_debug_trace_verify(sirius_ctx* c, void* buf, int layer) {
   if (!c) return -1;
   c->trace = static_cast<unsigned long long*>(buf);
   c->trace_layer = layer;
+  c->trace_ffn = false;
+  return 0;
+}
+
+// Debug: %globaltimer phase stamps of the decode CATS FFN of `layer` (DEV u64 [8][1024]); graphs off.
+int sirius_debug_trace_ffn(sirius_ctx* c, void* buf, int layer) {
+  if (!c) return -1;
+  c->trace = static_cast<unsigned long long*>(buf);
+  c->trace_layer = layer;
+  c->trace_ffn = buf != nullptr;
   return 0;
 }
 

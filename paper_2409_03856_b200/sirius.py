@@ -83,6 +83,8 @@ def load():
         lib.sirius_debug_buffer.restype = I
         lib.sirius_debug_launches.argtypes = [P]
         lib.sirius_debug_launches.restype = ctypes.c_ulonglong
+        lib.sirius_debug_trace_ffn.argtypes = [P, P, I]
+        lib.sirius_debug_trace_ffn.restype = I
         lib.sirius_debug_trace_verify.argtypes = [P, P, I]
         lib.sirius_debug_trace_verify.restype = I
         lib.sirius_debug_trace.argtypes = [P, P]
