@@ -49,10 +49,12 @@ def test_weights_on_device_equal_host(tiny_models):
         np.testing.assert_array_equal(wd[k].view(torch.int16).cpu().numpy().view(np.uint16).reshape(wh[k].shape), wh[k])
 
 
-@pytest.fixture(params=["per_stage", "step_kernel"])
+@pytest.fixture(params=["per_stage", "step_kernel", "per_stage_deterministic_ffn"])
 def schedule(request, monkeypatch):
-    """Decode schedule: one kernel per stage (default) or the persistent step kernel (opt-in)."""
+    """Decode schedule: one kernel per stage (default: CATS FFN partials added with atomics), the
+    persistent step kernel (opt-in), or per stage with the deterministic FFN reduction."""
     monkeypatch.setenv("SIRIUS_STEP_KERNEL", "1" if request.param == "step_kernel" else "0")
+    monkeypatch.setenv("SIRIUS_FFN_ATOMIC", "0" if request.param == "per_stage_deterministic_ffn" else "1")
     return request.param
 
 
