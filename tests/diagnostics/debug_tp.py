@@ -1,6 +1,6 @@
 """Diagnostic: TP-emulated decode (tp = 2, 8) against TP 1 on the GPU and the oracle, per stage."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import synth
 from synth import gpu as sg
