@@ -15,6 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsirius.so")
 
 SIRIUS_OK = 0
+SIRIUS_ERR_INVALID_ARG, SIRIUS_ERR_CAPACITY, SIRIUS_ERR_STATE = -1, -2, -3
+SIRIUS_ERR_CUDA, SIRIUS_ERR_NCCL, SIRIUS_ERR_UNSUPPORTED = -4, -5, -6
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "CAPACITY", -3: "STATE", -4: "CUDA", -5: "NCCL", -6: "UNSUPPORTED"}
 SIRIUS_DENSE = 1
 ACCEPT_THRESHOLD = 0

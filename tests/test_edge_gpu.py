@@ -1,0 +1,114 @@
+"""Edge cases of the C ABI on the GPU (tiny config): the degenerate cases of the method and the
+documented error behaviour of include/sirius.h.
+
+  * gamma = 1: the correction kernel verifies only the pending token — no draft to accept,
+    n_accept = 0 and the next token is the full model's argmax of that row (Alg. 1 with kernel size 1);
+  * no neuron active (t_l above every |a|): the CATS FFN contributes exactly nothing — the oracle with
+    the same thresholds is the reference (PAPER.md:121 applied at density 0);
+  * gamma > max_gamma -> SIRIUS_ERR_CAPACITY, gamma < 1 / NULL buffers -> SIRIUS_ERR_INVALID_ARG,
+    a decode position outside [0, max_seq) -> sticky device-side capacity error reported by the next
+    call, kv_rewrite with n_rows outside [1, gamma] -> likewise.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import sirius_oracle as so
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ABS, REL = 2e-2, 1e-2
+
+
+def i32(x):
+    return torch.tensor(np.asarray(x, dtype=np.int32), device="cuda")
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from synth import gpu as sg
+    cfg = synth.TINY
+    return cfg, synth.host_weights(cfg), sg.device_weights(cfg)
+
+
+def make_ctx(cfg, wd, thr, max_seq=128, max_gamma=8):
+    from paper_2409_03856_b200 import sirius as S
+    return S.Sirius(cfg, wd, thr, batch=1, max_seq=max_seq, max_gamma=max_gamma)
+
+
+def test_gamma_one_is_a_dense_step(tiny):
+    cfg, wh, wd = tiny
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 11, 30)
+    om = so.OracleModel(cfg, wh, max_seq=128, max_gamma=8)
+    first = so.argmax_lowest(om.prefill_last(prompt))
+    ctx = make_ctx(cfg, wd, thr)
+    f = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [len(prompt)], f)
+    lf = om.verify([first], len(prompt))
+    na, nx = torch.zeros(1, dtype=torch.int32, device="cuda"), torch.zeros(1, dtype=torch.int32, device="cuda")
+    q = torch.zeros((1, 1), dtype=torch.float32, device="cuda")
+    lo = torch.zeros((1, 1, cfg.vocab), dtype=torch.float32, device="cuda")
+    ctx.correct_kernel(i32([[first]]), i32([len(prompt)]), 1, 0.5, 0, na, nx, q, lo)
+    torch.cuda.synchronize()
+    assert int(na.item()) == 0
+    err = np.abs(lo.cpu().numpy()[0, 0] - lf[0])
+    assert np.all(err <= ABS + REL * np.abs(lf[0]))
+    s = np.sort(lf[0])
+    if s[-1] - s[-2] > 2 * err.max():
+        assert int(nx.item()) == so.argmax_lowest(lf[0])
+    # q of the last (bonus) row is the probability of its argmax
+    p = np.exp(lf[0] - lf[0].max())
+    np.testing.assert_allclose(float(q.item()), p.max() / p.sum(), rtol=1e-3)
+
+
+def test_no_active_neuron(tiny):
+    """Thresholds above every |SiLU(g)|: the sparse model's FFN output is exactly zero."""
+    from paper_2409_03856_b200 import sirius as S
+    cfg, wh, wd = tiny
+    thr = np.full(cfg.n_layers, 1e30, dtype=np.float32)
+    prompt = synth.eval_prompt(cfg, 12, 20)
+    om = so.OracleModel(cfg, wh, max_seq=128, max_gamma=8)
+    tok = so.argmax_lowest(om.prefill_last(prompt))
+    ref = om.decode(tok, len(prompt), True, thr, want_mask=True)
+    assert ref.mask.sum() == 0
+    ctx = make_ctx(cfg, wd, thr)
+    f = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [len(prompt)], f)
+    to = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lo = torch.zeros((1, cfg.vocab), dtype=torch.float32, device="cuda")
+    na = torch.zeros((1, cfg.n_layers), dtype=torch.int32, device="cuda")
+    ctx.sparse_decode_step(i32([tok]), i32([len(prompt)]), 0, to, lo, na)
+    torch.cuda.synchronize()
+    assert np.all(na.cpu().numpy() == 0)
+    err = np.abs(lo.cpu().numpy()[0] - ref.logits)
+    assert np.all(err <= ABS + REL * np.abs(ref.logits))
+
+
+def test_error_behaviour(tiny):
+    from paper_2409_03856_b200 import sirius as S
+    cfg, wh, wd = tiny
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 13, 16)
+    ctx = make_ctx(cfg, wd, thr, max_seq=64, max_gamma=4)
+    f = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [len(prompt)], f)
+    na, nx = torch.zeros(1, dtype=torch.int32, device="cuda"), torch.zeros(1, dtype=torch.int32, device="cuda")
+    kt = i32([[int(f.item())] * 8])
+    with pytest.raises(S.SiriusError) as e:  # gamma > max_gamma
+        ctx.correct_kernel(kt, i32([16]), 8, 0.1, 0, na, nx)
+    assert e.value.status == S.SIRIUS_ERR_CAPACITY
+    with pytest.raises(S.SiriusError) as e:  # gamma < 1
+        ctx.correct_kernel(kt, i32([16]), 0, 0.1, 0, na, nx)
+    assert e.value.status == S.SIRIUS_ERR_INVALID_ARG
+    lib = S.load()  # NULL token buffer
+    assert lib.sparse_decode_step(ctx.h, None, i32([16]).data_ptr(), 0, nx.data_ptr(), None, None, None) == \
+        S.SIRIUS_ERR_INVALID_ARG
+    # a decode position outside [0, max_seq): suppressed on the device, reported by a later call
+    ctx.sparse_decode_step(i32([int(f.item())]), i32([64]), 0, nx)
+    ctx.correct_kernel(i32([[int(f.item())] * 2]), i32([16]), 2, 0.1, 0, na, nx)
+    torch.cuda.synchronize()
+    with pytest.raises(S.SiriusError) as e:
+        ctx.sparse_decode_step(i32([int(f.item())]), i32([17]), 0, nx)
+    assert e.value.status == S.SIRIUS_ERR_CAPACITY
