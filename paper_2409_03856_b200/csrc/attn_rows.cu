@@ -258,9 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
     const float val = Ls > 0.f ? o / Ls : 0.f;
     const int rr = r_base + r, i = rr / G, g = rr % G;
     const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + d;
-    const uint16_t hi = f2bf_bits(val);
-    a.out_hi[off] = hi;
-    a.out_lo[off] = f2bf_bits(val - __uint_as_float((uint32_t)hi << 16));
+    store_split3(a.out3, a.plane, off, val);
   }
   rstamp(a, 7);
 }

@@ -122,6 +122,23 @@ SIRIUS_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); 
 SIRIUS_DEV uint16_t f2bf_bits(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
 SIRIUS_DEV float round_bf16(float f) { return __bfloat162float(__float2bfloat16_rn(f)); }
 SIRIUS_DEV uint32_t pack_bf16(float lo, float hi) { return (uint32_t)f2bf_bits(lo) | ((uint32_t)f2bf_bits(hi) << 16); }
+// fp32 value as three bf16 terms x = t0 + t1 + t2 (exact for normal x: each residual is exact in fp32
+// and the last one has <= 8 significant bits) — the tensor-core B operand of the verify / prefill
+// GEMMs ("x3" operand planes, D15a).  t[0] = bf16(x), t[1] = bf16(x - t0), t[2] = bf16(x - t0 - t1).
+SIRIUS_DEV void split3(float x, uint16_t* t) {
+  t[0] = f2bf_bits(x);
+  const float r1 = x - __uint_as_float((uint32_t)t[0] << 16);
+  t[1] = f2bf_bits(r1);
+  t[2] = f2bf_bits(r1 - __uint_as_float((uint32_t)t[1] << 16));
+}
+// store x at element off of the three planes (plane stride in elements)
+SIRIUS_DEV void store_split3(uint16_t* x3, size_t plane, size_t off, float x) {
+  uint16_t t[3];
+  split3(x, t);
+  x3[off] = t[0];
+  x3[plane + off] = t[1];
+  x3[2 * plane + off] = t[2];
+}
 
 // dot of 8 bf16 (packed in a uint4) with 8 floats
 SIRIUS_DEV float dot8(const uint4 w, const float* x) {

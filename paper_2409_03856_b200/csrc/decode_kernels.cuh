@@ -104,7 +104,8 @@ struct StepArgs {
   const float *rope_cos, *rope_sin;
   // workspace
   float *x, *x1, *qkv, *o, *attn_part, *ffn_part;
-  uint16_t *o_hi, *o_lo;  // if set: attention output as a bf16 hi/lo pair (tcgen05 operand) instead of o
+  uint16_t* o3;           // if set: attention output as three bf16 terms (tcgen05 operand planes) instead of o
+  size_t o3_plane;
   int* part_cnt;
   unsigned* group_bar;
   unsigned long long* grid_bar;  // dedicated monotone counter (nblocks = grid)

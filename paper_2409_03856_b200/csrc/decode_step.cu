@@ -392,10 +392,8 @@ SIRIUS_DEV void attention_phase(const StepArgs& a, int l, StepSmem<B, HD, G>& sm
     }
     const float val = Ls > 0.f ? o / Ls : 0.f;
     const size_t off = (size_t)b * Hr * HD + (kvh * G + g) * HD + dd;
-    if (a.o_hi) {  // the row path's O-proj GEMM operand: val = hi + lo to 2^-17
-      const uint16_t hi = f2bf_bits(val);
-      a.o_hi[off] = hi;
-      a.o_lo[off] = f2bf_bits(val - __uint_as_float((uint32_t)hi << 16));
+    if (a.o3) {  // the row path's O-proj GEMM operand: val as three bf16 terms (exact)
+      store_split3(a.o3, a.o3_plane, off, val);
     } else {
       a.o[off] = val;
     }

@@ -14,9 +14,9 @@
 //
 // Roles (128 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer, warp 2 = TMEM
 // allocator; all four warps run the epilogue (TMEM lane = weight row = threadIdx.x).
-// Epilogues: fp32 store, or SwiGLU m = SiLU(g) * u from two accumulators (gate, up), written as a bf16
-// hi/lo pair.  Activations enter as bf16 hi/lo pairs of fp32 values (x = hi + lo to 2^-17): two MMAs
-// per k-step, free while the pass is HBM-bound.
+// Epilogues: fp32 store, or SwiGLU m = SiLU(g) * u from two accumulators (gate, up), written as three
+// bf16 terms.  Activations enter as three bf16 terms of fp32 values (split3: x = t0 + t1 + t2 exactly):
+// three MMAs per k-step into one accumulator, free while the pass is HBM-bound (D15a).
 #include <cuda.h>
 
 #include "common.cuh"
@@ -82,9 +82,7 @@ SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
     const float m = on ? av * v1 : 0.f;        // a * up, CATS-masked (inactive pairs contribute exact 0)
     if (g.gate_out) g.gate_out[(size_t)j * g.gate_stride + n] = av;
     if (g.n_active && on) atomicAdd(g.n_active + (size_t)j * g.n_active_stride, 1);
-    const uint16_t hi = f2bf_bits(m);
-    reinterpret_cast<uint16_t*>(g.out)[(size_t)j * g.ldc + n] = hi;
-    reinterpret_cast<uint16_t*>(g.out2)[(size_t)j * g.ldc + n] = f2bf_bits(m - __uint_as_float((uint32_t)hi << 16));
+    store_split3(reinterpret_cast<uint16_t*>(g.out), g.out_plane, (size_t)j * g.ldc + n, m);
   } else {
     reinterpret_cast<float*>(g.out)[(size_t)j * g.ldc + n] = v0;
   }
@@ -124,8 +122,7 @@ SIRIUS_DEV bool epi_arrive_last(unsigned* counter, unsigned n, unsigned* flag_s)
 template <bool DUAL, int KBOX>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
-                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo, GemmArgs g,
-                   int MP, int stages, int has_lo) {
+                   const __grid_constant__ CUtensorMap tmB, GemmArgs g, int MP, int stages) {
   // KBOX: 64-wide K boxes per pipeline stage (one work unit = 64 KBOX of K): each weight row is read
   // 128 KBOX contiguous bytes at a time
   constexpr int NACC = DUAL ? 2 : 1;
@@ -140,8 +137,8 @@ __global__ void __launch_bounds__(192, 1)
   if (tid == 0) gstamp(g, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t b_bytes = (uint32_t)MP * 128 * KBOX;  // one activation operand's boxes of a stage
-  const int NB = has_lo ? 2 : 1;
+  const uint32_t b_bytes = (uint32_t)MP * 128 * KBOX;  // one activation term's boxes of a stage
+  const int NB = g.nterms;
   const uint32_t stage_bytes = ((NACC * A_BYTES + NB * b_bytes) + 1023) & ~1023u;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
@@ -166,7 +163,6 @@ __global__ void __launch_bounds__(192, 1)
     prefetch_tmap(&tmA0);
     if (DUAL) prefetch_tmap(&tmA1);
     prefetch_tmap(&tmB);
-    if (has_lo) prefetch_tmap(&tmBlo);
   }
   if (warp == 5) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_ptr_s)),
@@ -221,10 +217,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int x = 0; x < KBOX; ++x) {
           uint8_t* bx = st + NACC * A_BYTES + x * (b_bytes / KBOX);
-          for (int r = 0; r < MP / 16; ++r) {
-            tma_load_2d(bx + r * 2048, &tmB, kc + 64 * x, r * 16, &full[s], pol_x);
-            if (has_lo) tma_load_2d(bx + b_bytes + r * 2048, &tmBlo, kc + 64 * x, r * 16, &full[s], pol_x);
-          }
+          for (int p = 0; p < NB; ++p)
+            for (int r = 0; r < MP / 16; ++r)
+              tma_load_2d(bx + p * b_bytes + r * 2048, &tmB, kc + 64 * x, p * g.plane_rows + g.row0 + r * 16, &full[s], pol_x);
         }
       }
     }
@@ -249,16 +244,13 @@ __global__ void __launch_bounds__(192, 1)
           for (int x = 0; x < KBOX; ++x) {
             const uint64_t a0 = sw128_desc(st + x * BOX_BYTES);
             const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES + x * BOX_BYTES) : 0ull;
-            const uint64_t b0 = sw128_desc(st + NACC * A_BYTES + x * (b_bytes / KBOX));
-            const uint64_t b1 = sw128_desc(st + NACC * A_BYTES + b_bytes + x * (b_bytes / KBOX));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
-              const uint32_t accf = (i > 0 || x > 0 || k > 0) ? 1u : 0u;
-              mma_bf16(acc, a0 + 2 * k, b0 + 2 * k, idesc, accf);
-              if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b0 + 2 * k, idesc, accf);
-              if (has_lo) {
-                mma_bf16(acc, a0 + 2 * k, b1 + 2 * k, idesc, 1u);
-                if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, b1 + 2 * k, idesc, 1u);
+              for (int p = 0; p < NB; ++p) {  // the activation's bf16 terms, all into one accumulator
+                const uint64_t bp = sw128_desc(st + NACC * A_BYTES + p * b_bytes + x * (b_bytes / KBOX));
+                const uint32_t accf = (i > 0 || x > 0 || k > 0 || p > 0) ? 1u : 0u;
+                mma_bf16(acc, a0 + 2 * k, bp + 2 * k, idesc, accf);
+                if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, bp + 2 * k, idesc, accf);
               }
             }
           }
@@ -379,10 +371,10 @@ size_t gemm_workspace_bytes(int num_sms) { return (size_t)num_sms * 2 * 2 * 256 
 int g_gemm_kbox = 2;  // 64-wide K boxes per stage (SIRIUS_GEMM_KBOX)
 
 template <bool DUAL, int KBOX>
-static cudaError_t gemm_k(const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b, const CUtensorMap* blo,
-                          GemmArgs g, int MP, int num_sms, size_t smem_budget, int has_lo, cudaStream_t st) {
+static cudaError_t gemm_k(const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b, GemmArgs g, int MP,
+                          int num_sms, size_t smem_budget, cudaStream_t st) {
   const int NACC = DUAL ? 2 : 1;
-  const int NB = has_lo ? 2 : 1;
+  const int NB = g.nterms;
   g.kb = (g.K + 64 * KBOX - 1) / (64 * KBOX);
   const size_t stage_bytes = ((size_t)KBOX * (NACC * 16384 + (size_t)NB * MP * 128) + 1023) & ~(size_t)1023;
   const size_t extra = 1024 + 512;
@@ -395,33 +387,31 @@ static cudaError_t gemm_k(const CUtensorMap* a0, const CUtensorMap* a1, const CU
   auto kern = gemm_tc_kernel<DUAL, KBOX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_chain(kern, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, *blo, g, MP, stages, has_lo);
+  return launch_chain(kern, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, g, MP, stages);
 }
 
-cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void* tmBlo, const GemmArgs& g, int MP,
-                 int num_sms, size_t smem_budget, cudaStream_t st) {
-  if (MP < 16 || MP > 256 || MP % 16) return cudaErrorInvalidValue;
+cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const GemmArgs& g, int MP, int num_sms,
+                 size_t smem_budget, cudaStream_t st) {
+  if (MP < 16 || MP > 256 || MP % 16 || g.nterms < 1 || g.nterms > 3) return cudaErrorInvalidValue;
   const bool dual = tmA1 != nullptr;
   const CUtensorMap* a0 = reinterpret_cast<const CUtensorMap*>(tmA0);
   const CUtensorMap* a1 = reinterpret_cast<const CUtensorMap*>(dual ? tmA1 : tmA0);
   const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmB);
-  const CUtensorMap* blo = reinterpret_cast<const CUtensorMap*>(tmBlo ? tmBlo : tmB);
-  const int has_lo = tmBlo ? 1 : 0;
   // KBOX boxes per stage need room for >= 2 stages (dual operands at large MP fall back to fewer)
   auto fits = [&](int kb) {
-    return (size_t)kb * ((dual ? 2 : 1) * 16384 + (has_lo ? 2 : 1) * MP * 128) * 2 + 1536 <= smem_budget;
+    return (size_t)kb * ((dual ? 2 : 1) * 16384 + (size_t)g.nterms * MP * 128) * 2 + 1536 <= smem_budget;
   };
   int kbox = 1;
   if (g_gemm_kbox >= 4 && fits(4)) kbox = 4;
   else if (g_gemm_kbox >= 2 && fits(2)) kbox = 2;
   if (dual) {
-    if (kbox == 4) return gemm_k<true, 4>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
-    if (kbox == 2) return gemm_k<true, 2>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
-    return gemm_k<true, 1>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
+    if (kbox == 4) return gemm_k<true, 4>(a0, a1, b, g, MP, num_sms, smem_budget, st);
+    if (kbox == 2) return gemm_k<true, 2>(a0, a1, b, g, MP, num_sms, smem_budget, st);
+    return gemm_k<true, 1>(a0, a1, b, g, MP, num_sms, smem_budget, st);
   }
-  if (kbox == 4) return gemm_k<false, 4>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
-  if (kbox == 2) return gemm_k<false, 2>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
-  return gemm_k<false, 1>(a0, a1, b, blo, g, MP, num_sms, smem_budget, has_lo, st);
+  if (kbox == 4) return gemm_k<false, 4>(a0, a1, b, g, MP, num_sms, smem_budget, st);
+  if (kbox == 2) return gemm_k<false, 2>(a0, a1, b, g, MP, num_sms, smem_budget, st);
+  return gemm_k<false, 1>(a0, a1, b, g, MP, num_sms, smem_budget, st);
 }
 
 }  // namespace launch

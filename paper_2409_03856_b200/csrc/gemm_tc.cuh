@@ -9,9 +9,12 @@ namespace sirius {
 struct GemmArgs {
   int N, K, M;          // weight rows, reduction length, valid token rows (<= MP)
   int n_tiles, kb;      // ceil(N / 128), ceil(K / 64)
-  void* out;            // fp32 [M, ldc] (single) or bf16 hi part [M, ldc] (dual, SwiGLU)
-  void* out2;           // dual: bf16 lo part [M, ldc] (m = hi + lo, |m - hi - lo| <= 2^-17 |m|)
+  void* out;            // fp32 [M, ldc] (single) or bf16 [3][out_plane] (dual, SwiGLU: m as three
+  size_t out_plane;     //   bf16 terms, split3 — the next GEMM's B operand planes)
   int ldc;
+  int nterms;           // B operand terms (1: plain bf16 activations; 3: fp32 activations split3)
+  int plane_rows;       // rows between the B operand's term planes in its tensor map
+  int row0;             // first B operand row of this launch (row chunks of large M)
   float* part;          // stream-K partials [num_sms, 2, NACC, 256, 128]
   unsigned* counters;   // [n_tiles] (self-resetting)
   unsigned long long* trace;  // debug: [8][grid] %globaltimer stamps of thread 0 / the MMA thread, or NULL
@@ -28,10 +31,11 @@ namespace launch {
 constexpr size_t kTmapBytes = 128;  // sizeof(CUtensorMap)
 bool make_tmap(void* map, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows);
 size_t gemm_workspace_bytes(int num_sms);
-// tmA1 == nullptr: single GEMM (fp32 out); else dual gate/up GEMM with SwiGLU bf16 hi/lo epilogue.
-// tmBlo != nullptr: the activation operand is the bf16 pair (hi, lo) of an fp32 tensor; both are
-// multiplied and accumulated (fp32-grade activations on the bf16 tensor cores).
-cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const void* tmBlo, const GemmArgs& g, int MP,
-                 int num_sms, size_t smem_budget, cudaStream_t st);
+// tmA1 == nullptr: single GEMM (fp32 out); else dual gate/up GEMM with the SwiGLU epilogue.
+// tmB: the activation operand, g.nterms planes of g.plane_rows rows each ([nterms * plane_rows, K]);
+// with 3 terms (split3 of an fp32 tensor) every term is multiplied and accumulated: fp32 activations
+// on the bf16 tensor cores, exactly represented.
+cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const GemmArgs& g, int MP, int num_sms,
+                 size_t smem_budget, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius

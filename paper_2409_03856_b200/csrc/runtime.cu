@@ -92,8 +92,8 @@ struct RankState {
   // activations (MAXM rows)
   float *resA = nullptr, *resB = nullptr, *dA = nullptr, *dF = nullptr, *qkv = nullptr, *logits = nullptr;
   float *qb = nullptr, *ob = nullptr;                      // post-RoPE q (verify), attention out (decode)
-  uint16_t *xn_hi = nullptr, *xn_lo = nullptr;            // tensor-core operands: bf16 hi/lo pairs of fp32
-  uint16_t *ob_hi = nullptr, *ob_lo = nullptr, *mb_hi = nullptr, *mb_lo = nullptr;
+  // tensor-core B operands: fp32 activations as three bf16 terms, [3][MAXM][K] (split3, exact)
+  uint16_t *xn3 = nullptr, *ob3 = nullptr, *mb3 = nullptr;
   // workspaces
   float *ffn_part = nullptr, *attn_part = nullptr, *gemm_part = nullptr;
   int* ffn_cnt = nullptr;
@@ -102,7 +102,7 @@ struct RankState {
   unsigned *attn_cnt = nullptr, *gemm_cnt = nullptr, *head_cnt = nullptr;
   // tensor maps
   std::vector<TmapBuf> tm_qkv, tm_o, tm_gate, tm_up, tm_down;
-  TmapBuf tm_head, tm_xn_hi, tm_xn_lo, tm_ob_hi, tm_ob_lo, tm_mb_hi, tm_mb_lo;
+  TmapBuf tm_head, tm_xn, tm_ob, tm_mb;  // activation maps: [3 * MAXM, K], box 16 rows
 };
 
 struct sirius_ctx {
@@ -318,9 +318,11 @@ struct GemmMask {  // CATS mask of the dual (SwiGLU) GEMM in the batched sparse 
   long long gate_stride = 0;
 };
 
-sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x_hi,
-                       const TmapBuf& x_lo, int N, int K, int M, void* out, int ldc, void* out2 = nullptr,
-                       unsigned long long* trace = nullptr, const GemmMask* mask = nullptr) {
+// out: fp32 [M, ldc] (single) or, dual (wb != NULL), the SwiGLU product's three bf16 term planes
+// (plane stride MAXM * ldc).  x: the activation's three term planes ([3 * MAXM, K] map).
+sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x, int N,
+                       int K, int M, void* out, int ldc, unsigned long long* trace = nullptr,
+                       const GemmMask* mask = nullptr) {
   GemmArgs g = {};
   g.trace = trace;
   if (mask) {
@@ -332,28 +334,46 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
   }
   g.N = N;
   g.K = K;
-  g.M = M;
   g.n_tiles = (N + 127) / 128;
   g.kb = (K + 63) / 64;
-  g.out = out;
-  g.out2 = out2;
+  g.out_plane = (size_t)c->MAXM * ldc;
   g.ldc = ldc;
+  g.nterms = 3;
+  g.plane_rows = c->MAXM;
   g.part = R.gemm_part;
   g.counters = R.gemm_cnt;
-  const int MP = round_up(M, 16);
-  LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x_hi.b, x_lo.b, g, MP, c->num_sms,
-                   MP <= 64 ? c->gemm_smem : c->smem_optin, c->stream));
+  // more than 128 token rows (prefill chunks, batched verify): launches of <= 128 rows, so that the
+  // three activation terms of >= 2 pipeline stages fit in shared memory next to the weight boxes
+  const int chunk = M > 128 ? 128 : M;
+  for (int r0 = 0; r0 < M; r0 += chunk) {
+    const int Mc = M - r0 < chunk ? M - r0 : chunk;
+    GemmArgs gc = g;
+    gc.M = Mc;
+    gc.row0 = r0;
+    gc.out = wb ? (void*)((uint16_t*)out + (size_t)r0 * ldc) : (void*)((float*)out + (size_t)r0 * ldc);
+    if (gc.n_active) gc.n_active += (size_t)r0 * gc.n_active_stride;
+    if (gc.gate_out) gc.gate_out += (size_t)r0 * gc.gate_stride;
+    if (r0) gc.trace = nullptr;
+    const int MP = round_up(Mc, 16);
+    LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x.b, gc, MP, c->num_sms,
+                     MP <= 64 ? c->gemm_smem : c->smem_optin, c->stream));
+  }
   return SIRIUS_OK;
 }
 
 // ---- the dense / verify / prefill forward over M token rows (chunk).  Rows are ordered
 // (sequence, i); rows_per_seq rows per sequence, sequences b_base .. b_base + nseq - 1.
-// to_cache: prefill (K/V -> cache at start[b] + i, attention reads the cache only).
+//   ROWS_PREFILL: K/V -> cache at start[b] + i, attention reads the cache only (one sequence per call);
+//   ROWS_VERIFY : K/V -> staging rows i, attention reads cache [0, start[b]) + staging [0, i];
+//   ROWS_DECODE : batched decode, one row per sequence of the whole batch (b_base 0, nseq = batch),
+//                 K/V -> cache at start[b] through the decode-attention item kernel.
 // sparse: CATS mask on the FFN (batched sparse decode, rows_per_seq = 1); n_active_out [rows, L] and
 // gate_act_out [rows, L, ffn] (emulated TP: rank shards concatenated) optional.
+enum RowsMode { ROWS_PREFILL = 0, ROWS_VERIFY = 1, ROWS_DECODE = 2 };
 sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* start, int b_base, int nseq,
-                           int rows_per_seq, bool to_cache, bool sparse = false, int32_t* n_active_out = nullptr,
+                           int rows_per_seq, RowsMode mode, bool sparse = false, int32_t* n_active_out = nullptr,
                            float* gate_act_out = nullptr) {
+  const bool to_cache = mode != ROWS_VERIFY;
   const sirius_config& cf = c->cfg;
   const int M = nseq * rows_per_seq, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   for (int l = 0; l < L; ++l) {
@@ -371,14 +391,14 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.norm_w = R.attn_norm[l];
       na.eps = cf.rms_eps;
       na.res_out = R.resA;
-      na.out_hi = R.xn_hi;
-      na.out_lo = R.xn_lo;
+      na.out3 = R.xn3;
+      na.plane = (size_t)c->MAXM * d;
       LCU(launch::norm_rows(na, M, c->stream));
       unsigned long long* gtr = (!to_cache && l == c->trace_layer && c->trace) ? c->trace + 8 * 1024 : nullptr;
-      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Nqkv, d, M, R.qkv, c->Nqkv, nullptr, gtr));
+      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn, c->Nqkv, d, M, R.qkv, c->Nqkv, gtr));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
-      if (rows_per_seq == 1 && to_cache && c->attn_stage && c->decode_rows) {
+      if (mode == ROWS_DECODE && c->attn_stage) {
         // one query row per sequence (batched decode): the decode-attention item kernel does RoPE,
         // the K/V append at pos and split-K attention, writing the O-proj operand as a hi/lo pair
         StepArgs sa = {};
@@ -391,8 +411,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         sa.attn_scale = 1.0f / sqrtf((float)hd);
         sa.pos = start;
         sa.qkv = R.qkv;
-        sa.o_hi = R.ob_hi;
-        sa.o_lo = R.ob_lo;
+        sa.o3 = R.ob3;
+        sa.o3_plane = (size_t)c->MAXM * c->Hr * hd;
         sa.k_cache = R.k_cache;
         sa.v_cache = R.v_cache;
         sa.kv_layer = kv_layer;
@@ -402,7 +422,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         sa.group_bar = R.attn_bar;
         sa.err = c->err_dev;
         LCU(launch::attn_stage(sa, l, cf.batch, c->stream));
-        OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d));
+        OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob, d, c->Hr * hd, M, R.dA, d));
         continue;
       }
       RopeStoreArgs ra = {};
@@ -441,15 +461,14 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       aa.part = R.attn_part;
       aa.counters = R.attn_cnt;
       aa.group_bar = R.attn_bar;
-      aa.out_hi = R.ob_hi;
-      aa.out_lo = R.ob_lo;
+      aa.out3 = R.ob3;
+      aa.plane = (size_t)c->MAXM * c->Hr * hd;
       aa.trace = (!to_cache && l == c->trace_layer) ? c->trace : nullptr;
       const int row_blocks = (rows_per_seq * c->G + 63) / 64;
       int splits = launch::attn_rows_splits(nseq, c->KVr, row_blocks, cf.max_seq, c->num_sms);
       while (splits > 1 && nseq * c->KVr * row_blocks * splits > kAttnRowUnits) --splits;  // workspace bound
       LCU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
-      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob_hi, R.tm_ob_lo, d, c->Hr * hd, M, R.dA, d, nullptr,
-                  gtr ? gtr + 8 * 1024 : nullptr));
+      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob, d, c->Hr * hd, M, R.dA, d, gtr ? gtr + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
     for (auto& R : c->ranks) {
@@ -461,8 +480,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.norm_w = R.ffn_norm[l];
       na.eps = cf.rms_eps;
       na.res_out = R.resB;
-      na.out_hi = R.xn_hi;
-      na.out_lo = R.xn_lo;
+      na.out3 = R.xn3;
+      na.plane = (size_t)c->MAXM * d;
       LCU(launch::norm_rows(na, M, c->stream));
       unsigned long long* gtr2 = (!to_cache && l == c->trace_layer && c->trace) ? c->trace + 3 * 8 * 1024 : nullptr;
       GemmMask mk;
@@ -476,10 +495,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         mk.gate_out = gate_act_out + (size_t)l * Ff + (c->emulated ? (size_t)R.rank * c->Fr : 0);
         mk.gate_stride = (long long)L * Ff;
       }
-      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn_hi, R.tm_xn_lo, c->Fr, d, M, R.mb_hi, c->Fr, R.mb_lo,
-                  gtr2, &mk));
-      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb_hi, R.tm_mb_lo, d, c->Fr, M, R.dF, d, nullptr,
-                  gtr2 ? gtr2 + 8 * 1024 : nullptr));
+      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn, c->Fr, d, M, R.mb3, c->Fr, gtr2, &mk));
+      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb, d, c->Fr, M, R.dF, d, gtr2 ? gtr2 + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
   }
@@ -622,11 +639,9 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     if (alloc(c, &R.k_cache, kv) || alloc(c, &R.v_cache, kv) || alloc(c, &R.stage_k, stg) ||
         alloc(c, &R.stage_v, stg) || alloc(c, &R.resA, (size_t)M * d) || alloc(c, &R.resB, (size_t)M * d) ||
         alloc(c, &R.dA, (size_t)M * d) || alloc(c, &R.dF, (size_t)M * d) || alloc(c, &R.qkv, (size_t)M * c->Nqkv) ||
-        alloc(c, &R.logits, (size_t)M * c->Vr) || alloc(c, &R.xn_hi, (size_t)M * d) ||
-        alloc(c, &R.xn_lo, (size_t)M * d) || alloc(c, &R.qb, (size_t)M * c->Hr * hd) ||
-        alloc(c, &R.ob, (size_t)M * c->Hr * hd) || alloc(c, &R.ob_hi, (size_t)M * c->Hr * hd) ||
-        alloc(c, &R.ob_lo, (size_t)M * c->Hr * hd) || alloc(c, &R.mb_hi, (size_t)M * c->Fr) ||
-        alloc(c, &R.mb_lo, (size_t)M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * std::max(4, B) * d) ||
+        alloc(c, &R.logits, (size_t)M * c->Vr) || alloc(c, &R.xn3, (size_t)3 * M * d) ||
+        alloc(c, &R.qb, (size_t)M * c->Hr * hd) || alloc(c, &R.ob, (size_t)M * c->Hr * hd) ||
+        alloc(c, &R.ob3, (size_t)3 * M * c->Hr * hd) || alloc(c, &R.mb3, (size_t)3 * M * c->Fr) || alloc(c, &R.ffn_part, (size_t)c->num_sms * std::max(4, B) * d) ||
         alloc(c, &R.ffn_cnt, (size_t)c->num_sms * std::max(4, B)) || alloc(c, &R.ffn_barrier, 8) ||
         alloc(c, &R.attn_part, (size_t)kAttnRowUnits * 64 * (hd + 2) + (size_t)B * c->KVr * 64 * 8 * (hd + 2)) ||
         alloc(c, &R.attn_cnt, (size_t)(B + 1) * c->KVr * (row_blocks_max + 1) * 4 + 4096) || alloc(c, &R.attn_bar, 8192) ||
@@ -657,12 +672,9 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       ok &= launch::make_tmap(R.tm_down[l].b, R.w_down_t[l], d, c->Fr, 128);
     }
     ok &= launch::make_tmap(R.tm_head.b, R.lm_head, c->Vr, d, 128);
-    ok &= launch::make_tmap(R.tm_xn_hi.b, R.xn_hi, M, d, 16);
-    ok &= launch::make_tmap(R.tm_xn_lo.b, R.xn_lo, M, d, 16);
-    ok &= launch::make_tmap(R.tm_ob_hi.b, R.ob_hi, M, c->Hr * hd, 16);
-    ok &= launch::make_tmap(R.tm_ob_lo.b, R.ob_lo, M, c->Hr * hd, 16);
-    ok &= launch::make_tmap(R.tm_mb_hi.b, R.mb_hi, M, c->Fr, 16);
-    ok &= launch::make_tmap(R.tm_mb_lo.b, R.mb_lo, M, c->Fr, 16);
+    ok &= launch::make_tmap(R.tm_xn.b, R.xn3, 3 * M, d, 16);
+    ok &= launch::make_tmap(R.tm_ob.b, R.ob3, 3 * M, c->Hr * hd, 16);
+    ok &= launch::make_tmap(R.tm_mb.b, R.mb3, 3 * M, c->Fr, 16);
     if (!ok) {
       c->last_error = "cuTensorMapEncodeTiled failed";
       return cleanup_fail(SIRIUS_ERR_CUDA);
@@ -729,7 +741,7 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
       const int rows = P - s < c->MAXM ? P - s : c->MAXM;
       c->pre_start_host[b] = s;
       CU(cudaMemcpyAsync(c->pre_start + b, c->pre_start_host + b, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-      OK(forward_rows(c, tokens + off + s, c->pre_start, b, 1, rows, true));
+      OK(forward_rows(c, tokens + off + s, c->pre_start, b, 1, rows, ROWS_PREFILL));
       CU(cudaStreamSynchronize(c->stream));  // pre_start_host reuse
       if (s + rows == P) {  // dense greedy next token from the last prompt row (reading D17)
         for (auto& R : c->ranks) {
@@ -785,7 +797,7 @@ static sirius_status enqueue_decode_rows(sirius_ctx* c, const int32_t* token_in,
   const int B = c->cfg.batch;
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * c->cfg.n_layers, c->stream));
   prof_begin(c, P_STEP);
-  OK(forward_rows(c, token_in, pos, 0, B, 1, true, !dense, n_active_out, gate_act_out));
+  OK(forward_rows(c, token_in, pos, 0, B, 1, ROWS_DECODE, !dense, n_active_out, gate_act_out));
   OK(enqueue_head_argmax(c, token_in, 1, B, logits_out, c->dec_nacc, token_out, nullptr, 0.f, 0));
   prof_end(c);
   CU(cudaGetLastError());
@@ -1024,7 +1036,9 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
   GraphKey key = {0xDEC0u, flags, (uintptr_t)token_in, (uintptr_t)pos, (uintptr_t)token_out, (uintptr_t)logits_out,
                   (uintptr_t)n_active_out, (uintptr_t)gate_act_out};
   return run_graphed(c, key, [&] {
-    return enqueue_decode(c, token_in, pos, flags, token_out, logits_out, n_active_out, gate_act_out);
+    OK(enqueue_decode(c, token_in, pos, flags, token_out, logits_out, n_active_out, gate_act_out));
+    mirror_err(c);  // a position outside [0, max_seq) is reported by the NEXT call (include/sirius.h)
+    return SIRIUS_OK;
   });
 }
 
@@ -1035,7 +1049,7 @@ static sirius_status enqueue_correct(sirius_ctx* c, const int32_t* kernel_tokens
   const sirius_config& cf = c->cfg;
   const int B = cf.batch, d = cf.d_model, M = B * gamma;
   prof_begin(c, P_VERIFY);
-  OK(forward_rows(c, kernel_tokens, start_pos, 0, B, gamma, false));
+  OK(forward_rows(c, kernel_tokens, start_pos, 0, B, gamma, ROWS_VERIFY));
   OK(enqueue_head_argmax(c, kernel_tokens, gamma, M, logits_out, n_accept_out, next_token_out, q_out,
                          accept_threshold, accept_mode));
   prof_end(c);
@@ -1059,12 +1073,12 @@ static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* kernel_to
     na.d = d;
     na.norm_w = R.final_norm;
     na.eps = cf.rms_eps;
-    na.out_hi = R.xn_hi;
-    na.out_lo = R.xn_lo;
+    na.out3 = R.xn3;
+    na.plane = (size_t)c->MAXM * d;
     LCU(launch::norm_rows(na, M, c->stream));
     float* lo = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : R.logits;
     const int ldl = logits_out ? (c->emulated ? cf.vocab : c->Vr) : c->Vr;
-    OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn_hi, R.tm_xn_lo, c->Vr, d, M, lo, ldl));
+    OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn, c->Vr, d, M, lo, ldl));
     AcceptStatsArgs as = {};
     as.logits = lo;
     as.ldl = ldl;
@@ -1245,24 +1259,24 @@ int sirius_debug_profile_read(sirius_ctx* c, float* totals_ms, int* counts) {
 }
 
 // ---------------------------------------------------------------- test-only: copy an internal buffer
-// which: 0 resA, 1 resB, 2 dA, 3 dF, 4 qkv, 5 ob (fp32), 6 xn_hi (bf16), 7 k_cache, 8 v_cache, 9 stage_k,
-// 10 stage_v, 11 mb_hi (bf16), 12 qb (fp32).  Synchronous D2D copy of `bytes` bytes into dst.
+// which: 0 resA, 1 resB, 2 dA, 3 dF, 4 qkv, 5 ob (fp32), 6 xn3 (bf16 term planes), 7 k_cache, 8 v_cache,
+// 9 stage_k, 10 stage_v, 11 mb3 (bf16 term planes), 12 qb (fp32).  Synchronous D2D copy of `bytes` bytes into dst.
 int sirius_debug_buffer(sirius_ctx* c, int rank, int which, void* dst, size_t bytes) {
   if (!c || rank < 0 || rank >= c->nranks) return -1;
   RankState& R = c->ranks[rank];
-  const void* src[13] = {R.resA, R.resB, R.dA, R.dF, R.qkv, R.ob, R.xn_hi, R.k_cache, R.v_cache,
-                         R.stage_k, R.stage_v, R.mb_hi, R.qb};
+  const void* src[13] = {R.resA, R.resB, R.dA, R.dF, R.qkv, R.ob, R.xn3, R.k_cache, R.v_cache,
+                         R.stage_k, R.stage_v, R.mb3, R.qb};
   if (which < 0 || which > 12) return -1;
   cudaStreamSynchronize(c->stream);
   return (int)cudaMemcpy(dst, src[which], bytes, cudaMemcpyDeviceToDevice);
 }
 
 // ---------------------------------------------------------------- test-only entry: the tcgen05 GEMM
-// out[m, n] = sum_k (X + Xlo)[m, k] W[n, k] (fp32), or (W2 != NULL) m = SiLU(X W^T) * (X W2^T) as bf16
-// hi (out) / lo (out2).  X, Xlo (nullable): DEV bf16 [x_rows >= M, K]; W, W2: DEV bf16 [N, K].
-// Synchronous.  Returns cudaError_t.
-int sirius_debug_gemm(const void* X, const void* Xlo, int x_rows, const void* Wt, const void* W2, void* out,
-                      void* out2, int M, int N, int K) {
+// out[m, n] = sum_k sum_p X[p][m, k] W[n, k] (fp32), or (W2 != NULL) m = SiLU(x W^T) * (x W2^T) as three
+// bf16 term planes out[3][M][N] (x = sum of the terms).  X: DEV bf16 [nterms][x_rows >= M][K] (term
+// planes); W, W2: DEV bf16 [N, K].  Synchronous.  Returns cudaError_t.
+int sirius_debug_gemm(const void* X, int nterms, int x_rows, const void* Wt, const void* W2, void* out, int M, int N,
+                      int K) {
   static float* part = nullptr;
   static unsigned* cnt = nullptr;
   int dev = 0, sms = 0, optin = 0;
@@ -1274,9 +1288,8 @@ int sirius_debug_gemm(const void* X, const void* Xlo, int x_rows, const void* Wt
     if (cudaMalloc(&cnt, 65536 * sizeof(unsigned))) return -1;
     cudaMemset(cnt, 0, 65536 * sizeof(unsigned));
   }
-  TmapBuf ta, tb, tx, txl;
-  if (!launch::make_tmap(ta.b, Wt, N, K, 128) || !launch::make_tmap(tx.b, X, x_rows, K, 16)) return -2;
-  if (Xlo && !launch::make_tmap(txl.b, Xlo, x_rows, K, 16)) return -2;
+  TmapBuf ta, tb, tx;
+  if (!launch::make_tmap(ta.b, Wt, N, K, 128) || !launch::make_tmap(tx.b, X, (uint64_t)nterms * x_rows, K, 16)) return -2;
   if (W2 && !launch::make_tmap(tb.b, W2, N, K, 128)) return -2;
   GemmArgs g = {};
   g.N = N;
@@ -1285,12 +1298,13 @@ int sirius_debug_gemm(const void* X, const void* Xlo, int x_rows, const void* Wt
   g.n_tiles = (N + 127) / 128;
   g.kb = (K + 63) / 64;
   g.out = out;
-  g.out2 = out2;
+  g.out_plane = (size_t)M * N;
   g.ldc = N;
+  g.nterms = nterms;
+  g.plane_rows = x_rows;
   g.part = part;
   g.counters = cnt;
-  cudaError_t e = launch::gemm(ta.b, W2 ? tb.b : nullptr, tx.b, Xlo ? txl.b : nullptr, g, round_up(M, 16), sms,
-                               (size_t)optin - 1024, 0);
+  cudaError_t e = launch::gemm(ta.b, W2 ? tb.b : nullptr, tx.b, g, round_up(M, 16), sms, (size_t)optin - 1024, 0);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaDeviceSynchronize();
 }

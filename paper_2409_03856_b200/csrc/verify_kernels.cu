@@ -76,16 +76,13 @@ __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
     if (g < NG) {
       const float h[4] = {(x[j].x * r) * bf16_lo(wn[j].x), (x[j].y * r) * bf16_hi(wn[j].x),
                           (x[j].z * r) * bf16_lo(wn[j].y), (x[j].w * r) * bf16_hi(wn[j].y)};
-      uint16_t hi[4], lo[4];
+      uint16_t t[4][3];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        hi[e] = f2bf_bits(h[e]);
-        lo[e] = f2bf_bits(h[e] - __uint_as_float((uint32_t)hi[e] << 16));
-      }
-      reinterpret_cast<uint2*>(a.out_hi + (size_t)m * d)[g] =
-          make_uint2(hi[0] | ((uint32_t)hi[1] << 16), hi[2] | ((uint32_t)hi[3] << 16));
-      reinterpret_cast<uint2*>(a.out_lo + (size_t)m * d)[g] =
-          make_uint2(lo[0] | ((uint32_t)lo[1] << 16), lo[2] | ((uint32_t)lo[3] << 16));
+      for (int e = 0; e < 4; ++e) split3(h[e], t[e]);
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        reinterpret_cast<uint2*>(a.out3 + p * a.plane + (size_t)m * d)[g] =
+            make_uint2(t[0][p] | ((uint32_t)t[1][p] << 16), t[2][p] | ((uint32_t)t[3][p] << 16));
     }
   }
 }

@@ -15,8 +15,8 @@ struct NormRowsArgs {
   const uint16_t* norm_w;  // [d]
   float eps;
   float* res_out;          // [M, d] or NULL
-  uint16_t* out_hi;        // [M, d] bf16: hi = bf16(h), lo = bf16(h - hi)  (fp32 h as a bf16 pair for
-  uint16_t* out_lo;        //          the tensor-core B operand; |h - hi - lo| <= 2^-17 |h|)
+  uint16_t* out3;          // [3][plane] bf16: h = t0 + t1 + t2 (split3: fp32 h exactly, as three bf16
+  size_t plane;            //          terms for the tensor-core B operand); row m at m * d of each plane
 };
 
 struct RopeStoreArgs {
@@ -45,8 +45,8 @@ struct AttnRowsArgs {
   float* part;              // workspace
   unsigned* counters;       // unused (kept for ABI-internal layout)
   unsigned* group_bar;      // [nseq * KVr * row_blocks][2] barrier (count, generation) of the split groups
-  uint16_t* out_hi;         // [nseq * rows, Hr * hd] attention output as a bf16 hi/lo pair
-  uint16_t* out_lo;
+  uint16_t* out3;           // [3][plane]: attention output [nseq * rows, Hr * hd] as three bf16 terms
+  size_t plane;
   unsigned long long* trace;  // debug: [8][grid CTAs] %globaltimer stamps, or NULL
 };
 

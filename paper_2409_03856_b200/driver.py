@@ -62,6 +62,7 @@ class Driver:
         self.d_in = torch.zeros(2 * B + (gm + 1) * B, dtype=i32, device=dev)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        self._h_out_ev = None  # recorded after the last H2D copy out of h_out
 
     # ------------------------------------------------------------------ session state
     def begin(self, prompts: Sequence[Sequence[int]]) -> None:
@@ -82,6 +83,11 @@ class Driver:
     def _upload(self, gamma: int, T=None) -> None:
         B = self.B
         T = self.T if T is None else T
+        # the previous non-blocking copy out of the pinned h_out may still be queued behind earlier
+        # steps: wait for it before overwriting h_out (it runs ahead of the steps enqueued after it,
+        # so the stream keeps those queued meanwhile)
+        if self._h_out_ev is not None:
+            self._h_out_ev.synchronize()
         h = self.h_out.numpy()
         h[0:B] = self.n_rows_h
         h[B:2 * B] = T
@@ -90,6 +96,8 @@ class Driver:
         h[3 * B:3 * B + gamma * B] = pos.reshape(-1)
         n = 3 * B + gamma * B
         self.d_out[:n].copy_(self.h_out[:n], non_blocking=True)
+        self._h_out_ev = self.torch.cuda.Event()
+        self._h_out_ev.record()
         self.h2d_bytes += 4 * n
 
     def flush(self) -> None:

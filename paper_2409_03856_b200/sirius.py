@@ -80,7 +80,7 @@ def load():
         lib.sirius_last_error.restype = ctypes.c_char_p
         lib.sirius_version.argtypes = []
         lib.sirius_version.restype = ctypes.c_char_p
-        lib.sirius_debug_gemm.argtypes = [P, P, I, P, P, P, P, I, I, I]
+        lib.sirius_debug_gemm.argtypes = [P, I, I, P, P, P, I, I, I]
         lib.sirius_debug_buffer.argtypes = [P, I, I, P, ctypes.c_size_t]
         lib.sirius_debug_buffer.restype = I
         lib.sirius_debug_launches.argtypes = [P]
@@ -213,12 +213,13 @@ class Sirius:
             pass
 
 
-def debug_gemm(X, W, out, M: int, W2=None, Xlo=None, out2=None) -> None:
-    """Test-only: out = (X + Xlo)[:M] @ W.T (fp32), or with W2 the SwiGLU m = SiLU(X W^T) * (X W2^T)
-    as a bf16 hi (out) / lo (out2) pair, via the tcgen05 kernel."""
+def debug_gemm(X, W, out, M: int, W2=None) -> None:
+    """Test-only, via the tcgen05 kernel: X is bf16 [rows, K] (one term) or [nterms, rows, K] (term
+    planes, x = their sum).  out = x[:M] @ W.T (fp32 [M, N]), or with W2 the SwiGLU
+    m = SiLU(x W^T) * (x W2^T) as three bf16 term planes (out: bf16 [3, M, N])."""
     lib = load()
     N, K = W.shape
-    r = lib.sirius_debug_gemm(X.data_ptr(), _ptr(Xlo), X.shape[0], W.data_ptr(), _ptr(W2), out.data_ptr(),
-                              _ptr(out2), M, N, K)
+    nterms, rows = (1, X.shape[0]) if X.dim() == 2 else (X.shape[0], X.shape[1])
+    r = lib.sirius_debug_gemm(X.data_ptr(), nterms, rows, W.data_ptr(), _ptr(W2), out.data_ptr(), M, N, K)
     if r != 0:
         raise RuntimeError(f"sirius_debug_gemm failed: {r}")

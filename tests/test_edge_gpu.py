@@ -106,9 +106,62 @@ def test_error_behaviour(tiny):
     assert lib.sparse_decode_step(ctx.h, None, i32([16]).data_ptr(), 0, nx.data_ptr(), None, None, None) == \
         S.SIRIUS_ERR_INVALID_ARG
     # a decode position outside [0, max_seq): suppressed on the device, reported by a later call
+    # (once the stream has run the call that set it)
     ctx.sparse_decode_step(i32([int(f.item())]), i32([64]), 0, nx)
-    ctx.correct_kernel(i32([[int(f.item())] * 2]), i32([16]), 2, 0.1, 0, na, nx)
+    torch.cuda.synchronize()
+    with pytest.raises(S.SiriusError) as e:
+        ctx.correct_kernel(i32([[int(f.item())] * 2]), i32([16]), 2, 0.1, 0, na, nx)
+    assert e.value.status == S.SIRIUS_ERR_CAPACITY
+    with pytest.raises(S.SiriusError) as e:  # sticky
+        ctx.sparse_decode_step(i32([int(f.item())]), i32([17]), 0, nx)
+    assert e.value.status == S.SIRIUS_ERR_CAPACITY
+
+
+def test_decode_capacity_error_reported_by_next_decode(tiny):
+    """A greedy-only loop (no correct_kernel in between) still sees a device-side capacity error: the
+    decode step mirrors the device error word, so the NEXT decode call returns CAPACITY."""
+    from paper_2409_03856_b200 import sirius as S
+    cfg, wh, wd = tiny
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 14, 16)
+    ctx = make_ctx(cfg, wd, thr, max_seq=64, max_gamma=4)
+    f = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [len(prompt)], f)
+    nx = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sparse_decode_step(i32([int(f.item())]), i32([64]), 0, nx)  # pos == max_seq: suppressed
     torch.cuda.synchronize()
     with pytest.raises(S.SiriusError) as e:
         ctx.sparse_decode_step(i32([int(f.item())]), i32([17]), 0, nx)
     assert e.value.status == S.SIRIUS_ERR_CAPACITY
+
+
+@pytest.mark.parametrize("lens", [[1, 9, 1, 33, 2, 1, 17, 5], [257, 1, 300, 3, 260, 1, 4, 258]])
+def test_batch8_prefill_single_row_chunks(tiny, lens):
+    """Batch 8 (the batched decode row path) with prompts whose last prefill chunk is ONE row (length
+    1, or 257 = 256 + 1): that chunk is a prefill of one sequence, not a batched decode step — every
+    sequence's first token, its cache and the next decode row match the oracle."""
+    from paper_2409_03856_b200 import sirius as S
+    cfg, wh, wd = tiny
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 40 + b, n) for b, n in enumerate(lens)]
+    ctx = S.Sirius(cfg, wd, thr, batch=8, max_seq=384, max_gamma=8)
+    f = torch.zeros(8, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(np.concatenate(prompts)), lens, f)
+    torch.cuda.synchronize()
+    oms, toks = [], []
+    for b, p in enumerate(prompts):
+        om = so.OracleModel(cfg, wh, max_seq=384, max_gamma=8)
+        last = om.prefill_last(p)
+        s = np.sort(last)
+        if s[-1] - s[-2] > 0.1:
+            assert int(f[b].item()) == so.argmax_lowest(last), b
+        oms.append(om)
+        toks.append(so.argmax_lowest(last))
+    to = torch.zeros(8, dtype=torch.int32, device="cuda")
+    lo = torch.zeros((8, cfg.vocab), dtype=torch.float32, device="cuda")
+    ctx.sparse_decode_step(i32(toks), i32(lens), S.SIRIUS_DENSE, to, lo)
+    torch.cuda.synchronize()
+    for b in range(8):
+        ref = oms[b].decode(toks[b], lens[b], False)
+        err = np.abs(lo.cpu().numpy()[b] - ref.logits)
+        assert np.all(err <= ABS + REL * np.abs(ref.logits)), (b, float(err.max()))

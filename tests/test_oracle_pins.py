@@ -19,13 +19,10 @@ def _f64(bits: np.ndarray) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ dense decoder vs HuggingFace
-def test_dense_decoder_matches_hf_llama_fp64(tiny):
-    """The dense decoder (embed, RMSNorm, RoPE rotate-half, GQA kv=h//(H/KV), SiLU-gated MLP, head)
-    equals transformers.LlamaForCausalLM in fp64 with the same weights (oracle with no activation
-    rounding of the KV cache).  Residual ~3e-6 comes from HF's fp32 RoPE table."""
+def _hf_llama(cfg, w):
+    """transformers.LlamaForCausalLM in fp64 carrying the synthetic weights."""
     torch = pytest.importorskip("torch")
     tr = pytest.importorskip("transformers")
-    cfg, w = tiny
     hc = tr.LlamaConfig(vocab_size=cfg.vocab, hidden_size=cfg.d_model, intermediate_size=cfg.ffn_dim,
                         num_hidden_layers=cfg.n_layers, num_attention_heads=cfg.n_heads,
                         num_key_value_heads=cfg.n_kv_heads, head_dim=cfg.head_dim, rope_theta=cfg.rope_theta,
@@ -51,13 +48,117 @@ def test_dense_decoder_matches_hf_llama_fp64(tiny):
         sd[p + "post_attention_layernorm.weight"] = t(w[f"layers.{l}.ffn_norm"])
     res = m.load_state_dict(sd, strict=False)
     assert not res.missing_keys and not res.unexpected_keys
+    return m
+
+
+def test_dense_decoder_matches_hf_llama_fp64(tiny, monkeypatch):
+    """The dense decoder (embed, RMSNorm, RoPE rotate-half, GQA kv=h//(H/KV), SiLU-gated MLP, head)
+    equals transformers.LlamaForCausalLM in fp64 with the same weights (oracle with no activation
+    rounding of the KV cache): to fp64 summation-order error once HF's fp32 RMSNorm / softmax / RoPE
+    table are made fp64 (and D16's table); with HF's stock fp32 pieces, to ~1e-5."""
+    torch = pytest.importorskip("torch")
+    cfg, w = tiny
+    m = _hf_llama(cfg, w)
+    prompt = synth.eval_prompt(cfg, 0, 48)
+    with torch.no_grad():
+        stock = m(torch.tensor(prompt[None].astype(np.int64))).logits[0].numpy()
+    _hf_full_fp64(monkeypatch, m, cfg)
     prompt = synth.eval_prompt(cfg, 0, 48)
     with torch.no_grad():
         ref = m(torch.tensor(prompt[None].astype(np.int64))).logits[0].numpy()
     om = so.OracleModel(cfg, w, max_seq=64, round_kv=False)
     mine = om.prefill(prompt)
     assert np.abs(ref).max() > 5.0  # logits are not degenerate
-    assert np.abs(mine - ref).max() < 2e-5, np.abs(mine - ref).max()
+    assert np.abs(mine - ref).max() < 1e-9, np.abs(mine - ref).max()
+    assert np.abs(mine - stock).max() < 5e-5, np.abs(mine - stock).max()
+
+
+def _hf_full_fp64(monkeypatch, m, cfg):
+    """HF computes RMSNorm, the attention softmax and the RoPE table in fp32 even for an fp64 model;
+    make the first two fp64 and the table that of reading D16 (angles in fp64, cos/sin rounded to
+    fp32) — precision conventions of the library, not part of the method — and select eager
+    attention."""
+    import torch
+    from transformers.models.llama import modeling_llama as ml
+    hd, half = cfg.head_dim, cfg.head_dim // 2
+
+    def rope_d16(x, position_ids):
+        inv = cfg.rope_theta ** (-2.0 * torch.arange(half, dtype=torch.float64) / hd)
+        ang = position_ids[0].to(torch.float64)[:, None] * inv[None, :]
+        c = torch.cos(ang).to(torch.float32).to(torch.float64)
+        s = torch.sin(ang).to(torch.float32).to(torch.float64)
+        return torch.cat([c, c], -1)[None], torch.cat([s, s], -1)[None]
+    monkeypatch.setattr(m.model.rotary_emb, "forward", rope_d16)
+
+    def rms_fp64(self, x):
+        return self.weight * (x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + self.variance_epsilon))
+
+    def eager_fp64(module, query, key, value, attention_mask, scaling, dropout=0.0, **kw):
+        k = ml.repeat_kv(key, module.num_key_value_groups)
+        v = ml.repeat_kv(value, module.num_key_value_groups)
+        s = torch.matmul(query, k.transpose(2, 3)) * scaling
+        if attention_mask is not None:
+            s = s + attention_mask
+        p = torch.softmax(s, dim=-1)
+        return torch.matmul(p, v).transpose(1, 2).contiguous(), p
+    monkeypatch.setattr(ml.LlamaRMSNorm, "forward", rms_fp64)
+    monkeypatch.setattr(ml, "eager_attention_forward", eager_fp64)
+    m.config._attn_implementation = "eager"
+    for layer in m.model.layers:
+        layer.self_attn.config._attn_implementation = "eager"
+
+
+def _rne_bf16(t):
+    """fp64 tensor -> nearest bf16 value (ties to even), computed in fp64 (no fp32 double rounding)."""
+    import torch
+    m, e = torch.frexp(t)
+    return torch.ldexp(torch.round(torch.ldexp(m, torch.full_like(e, 8))), e - 8)
+
+
+@pytest.mark.parametrize("variant", ["oracle_reading", "k_rounded_before_rope", "q_rounded_too", "no_rounding"])
+def test_kv_bf16_rounding_placement_against_hf(tiny, monkeypatch, variant):
+    """Pins WHERE the oracle rounds to bf16 (D15: the stored K after RoPE and V, nothing
+    else) against HuggingFace LlamaForCausalLM in fp64, with a KV cache whose update() stores bf16
+    values of the post-RoPE K and V, and the RoPE table of reading D16 (angles in fp64, cos/sin
+    rounded to fp32).  The oracle (round_kv) must equal that model to fp64 summation-order error;
+    the three mis-placed variants (K rounded before RoPE; q rounded as well; nothing rounded) must
+    all differ from the oracle by far more — so a misplaced rounding in the oracle fails this test."""
+    torch = pytest.importorskip("torch")
+    from transformers import DynamicCache
+    from transformers.models.llama import modeling_llama as ml
+    cfg, w = tiny
+    m = _hf_llama(cfg, w)
+    _hf_full_fp64(monkeypatch, m, cfg)
+    orig_rope = ml.apply_rotary_pos_emb
+
+    class RoundingCache(DynamicCache):
+        def update(self, k, v, layer_idx, *a, **kw):
+            if variant in ("oracle_reading", "q_rounded_too"):
+                k, v = _rne_bf16(k), _rne_bf16(v)
+            return super().update(k, v, layer_idx, *a, **kw)
+
+    def rope_variant(q, k, cos, sin, *a, **kw):
+        if variant == "k_rounded_before_rope":
+            k = _rne_bf16(k)
+        q2, k2 = orig_rope(q, k, cos, sin, *a, **kw)
+        if variant == "q_rounded_too":
+            q2 = _rne_bf16(q2)
+        return q2, k2
+    monkeypatch.setattr(ml, "apply_rotary_pos_emb", rope_variant)
+    if variant == "k_rounded_before_rope":  # V is not rotated: round it where it is produced
+        for layer in m.model.layers:
+            layer.self_attn.v_proj.register_forward_hook(lambda mod, inp, out: _rne_bf16(out))
+    prompt = synth.eval_prompt(cfg, 0, 48)
+    with torch.no_grad():
+        ref = m(torch.tensor(prompt[None].astype(np.int64)), past_key_values=RoundingCache(),
+                use_cache=True).logits[0].numpy()
+    mine = so.OracleModel(cfg, w, max_seq=64, round_kv=True).prefill(prompt)
+    diff = float(np.abs(mine - ref).max())
+    print(f"{variant}: max |oracle - HF| = {diff:.3e}")
+    if variant == "oracle_reading":
+        assert diff < 1e-9, diff
+    else:
+        assert diff > 1e-4, (variant, diff)
 
 
 def test_round_bf16_is_rne():

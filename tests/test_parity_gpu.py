@@ -243,3 +243,21 @@ def test_nccl_bootstrap_single_rank():
     assert lib.sirius_nccl_comm_init(1, uid, 0, ctypes.byref(comm)) == 0
     assert comm.value
     assert lib.sirius_nccl_comm_destroy(comm) == 0
+
+
+def test_greedy_run_chunked_positions(tiny_models):
+    """driver.greedy_run (the bench's dense / CS-only baseline): chunks of max_gamma steps over fixed
+    buffer slots with one H2D of positions per chunk, no host sync between chunks — every chunk must
+    decode at its own positions (the pinned staging buffer is not overwritten before its copy ran)."""
+    from paper_2409_03856_b200 import driver
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.1)
+    prompt = synth.eval_prompt(cfg, 8, 40)
+    for dense in (True, False):
+        ref = so.greedy_decode(so.OracleModel(cfg, wh, max_seq=256), prompt, 51, not dense, None if dense else thr)
+        d = driver.Driver(make_ctx(cfg, wd, thr, max_gamma=8))
+        d.begin([prompt])
+        assert d.pending[0] == ref[0]
+        d.greedy_run(d.pending, d.T, 50, dense)  # 7 chunks of 8 steps
+        torch.cuda.synchronize()
+        assert int(d.drafts[0, 0].item()) == ref[50]
