@@ -162,6 +162,13 @@ sirius_status correct_kernel(sirius_ctx* ctx, const int32_t* kernel_tokens, cons
  * Errors: STATE if no correct_kernel preceded it. */
 sirius_status kv_rewrite(sirius_ctx* ctx, const int32_t* start_pos, const int32_t* n_rows);
 
+/* The full model's greedy token (argmax, lowest id on ties) of EVERY verify row of the last
+ * correct_kernel call — the interleaving candidates of the component ablation without rollback
+ * (Table 4: "only letting the LLM correct the token it is evaluating"; reading
+ * D27).  out: DEV int32 [batch, gamma of that call]; enqueued on the stream (async copy).
+ * Errors: STATE if no correct_kernel preceded it. */
+sirius_status sirius_verify_row_argmax(sirius_ctx* ctx, int32_t* out);
+
 sirius_status sirius_destroy(sirius_ctx* ctx);
 
 /* Human-readable description of the last error on ctx (static storage inside ctx; never NULL). */

@@ -176,6 +176,12 @@ class OracleModel:
         return np.stack([self.forward_row(t, T + i, False, None, i).logits for i, t in enumerate(kernel_tokens)])
 
 
+def top2_margin(l: np.ndarray) -> float:
+    """Largest minus second-largest logit (0 on an exact tie): how far the argmax is from flipping."""
+    s = np.partition(l, -2)[-2:]
+    return float(s[1] - s[0])
+
+
 def argmax_lowest(l: np.ndarray) -> int:
     """argmax with the lowest token id on exact ties (reading D13)."""
     return int(np.flatnonzero(l == l.max())[0])
@@ -213,6 +219,9 @@ class KernelRecord:
     q: np.ndarray  # full-model likelihoods
     next_token: int  # interleaved / bonus token = argmax of verify row j
     n_active: np.ndarray  # [g-1, L] active neurons per sparse step
+    draft_margin: np.ndarray = None   # [g-1] top-2 logit margin of each sparse drafting row
+    verify_margin: np.ndarray = None  # [g] top-2 logit margin of each verify row
+    advance: int = 0                  # tokens committed by this kernel (j + 1 with rollback, else g)
 
 
 @dataclass
@@ -223,11 +232,17 @@ class GenerateResult:
 
     @property
     def advances(self) -> List[int]:
-        return [k.j + 1 for k in self.kernels]
+        return [k.advance for k in self.kernels]
+
+    def rejection_positions(self) -> List[int]:
+        """Index i (0-based draft position within the kernel) of every rejected draft: the data of the
+        paper's rejection-position histogram (Appendix)."""
+        return [k.j for k in self.kernels if k.j < len(k.tokens) - 1]
 
 
 def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: int, r: float,
-             thresholds: np.ndarray, accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True) -> GenerateResult:
+             thresholds: np.ndarray, accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True,
+             interleave: bool = True, rollback: bool = True) -> GenerateResult:
     """The Sirius loop, Algorithm 1, readings D5-D18:
       * dense prefill of the prompt; the first generated token is the dense argmax (D17);
       * kernel size n = gamma: the sparse model drafts gamma-1 tokens after the pending token,
@@ -236,28 +251,53 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
       * accept scan with threshold r (lines 12-16); rollback to T+j+1 (line 'cache_pos <- j+1');
       * KV rewrite of the committed span [T, T+j] with the full model's K/V (PAPER.md:257, :294);
       * interleave the full model's argmax of row j (line 'Interleaving Key Token', reading D10/D11).
-    Generates exactly n_tokens tokens (D18); the final kernel's surplus is truncated."""
+    Generates exactly n_tokens tokens (D18); the final kernel's surplus is truncated.
+
+    Component ablation (Table 4, §5.3; reading D27): `rewrite`
+    (KV Rewrite), `interleave`, `rollback` switch the three correction components independently
+    (rollback needs interleave: Table 4 has no rollback without it).  Without rollback every kernel
+    commits all gamma positions: the drafts d_1..d_{g-1}, where `interleave` replaces each REJECTED
+    draft d_{i+1} (q_i < r) by the full model's argmax of verify row i ("only letting the LLM correct
+    the token it is evaluating"), then the full model's token of the last row; with `rewrite` the
+    full model's K/V of the g verified rows overwrite the cache rows [T, T+g).  KernelRecord.j stays
+    the first rejection (the statistic), the advance is then g."""
+    assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
     P = len(prompt)
     assert P + n_tokens + gamma <= model.max_seq and gamma >= 1
-    logits = model.prefill(prompt)
-    out = [argmax_lowest(logits[-1])]  # out[-1] is the pending token at position T
+    # dense prefill; only the last row's logits are needed (prefill_last: same cache, pinned bitwise
+    # against prefill() in tests/test_oracle_pins.py)
+    out = [argmax_lowest(model.prefill_last(prompt))]  # out[-1] is the pending token at position T
     T = P
     res = GenerateResult(out)
     while len(out) < n_tokens:
         ins = [out[-1]]
-        nact = []
+        nact, dmarg = [], []
         for i in range(gamma - 1):  # sparse drafting, greedy (D13)
             row = model.decode(ins[i], T + i, True, thresholds)
             nact.append(row.n_active)
+            dmarg.append(top2_margin(row.logits))
             ins.append(argmax_lowest(row.logits))
         lf = model.verify(ins, T)  # full model over the kernel, K/V -> staging
         j, q = accept_scan(lf, ins, r, accept_mode)
+        if rollback:
+            adv = j + 1
+            nxt = argmax_lowest(lf[j])
+            committed = ins[1:j + 1] + [nxt]
+        else:  # no rollback: every position is committed; rejected drafts interleaved (or kept)
+            adv = gamma
+            committed = []
+            for i in range(gamma - 1):
+                ok = (q[i] >= r) if accept_mode == ACCEPT_THRESHOLD else (ins[i + 1] == argmax_lowest(lf[i]))
+                committed.append(ins[i + 1] if (ok or not interleave) else argmax_lowest(lf[i]))
+            nxt = argmax_lowest(lf[gamma - 1])
+            committed.append(nxt)
         if rewrite:
-            model.kv_rewrite(T, j + 1)  # commit + rollback: len = T + j + 1
-        nxt = argmax_lowest(lf[j])
-        out += ins[1:j + 1] + [nxt]
-        res.kernels.append(KernelRecord(T, list(ins), j, q, nxt, np.array(nact, dtype=np.int32).reshape(-1, model.cfg.n_layers)))
-        T += j + 1
+            model.kv_rewrite(T, adv)  # commit (+ rollback): len = T + adv
+        out += committed
+        res.kernels.append(KernelRecord(T, list(ins), j, q, nxt,
+                                        np.array(nact, dtype=np.int32).reshape(-1, model.cfg.n_layers),
+                                        np.array(dmarg), np.array([top2_margin(l) for l in lf]), adv))
+        T += adv
     res.all_tokens = list(out)
     res.tokens = out[:n_tokens]
     return res

@@ -134,6 +134,7 @@ struct sirius_ctx {
   int32_t* pre_start = nullptr;  // [batch] chunk start positions (prefill)
   int32_t* pre_start_host = nullptr;
   int32_t* scratch_tok = nullptr;
+  int32_t* row_argmax = nullptr;  // [MAXM] full-model argmax of every row of the last verify
   int last_gamma = 0;
   bool have_correct = false;
   bool prefilled = false;
@@ -146,6 +147,12 @@ struct sirius_ctx {
   };
   std::vector<ProfEv> prof;
   size_t prof_used = 0;
+  // profiling with CUDA graphs on: the events are captured into the graph as external event-record
+  // nodes around the profiled launches; after each replay the call synchronises and accumulates
+  bool capturing = false;
+  std::vector<ProfEv> cap_evs;
+  double prof_tot[16] = {0};
+  int prof_cnt[16] = {0};
   // persistent decode step (decode_step.cu): TP 1 on supported shapes, opt-in (SIRIUS_STEP_KERNEL=1);
   // the default is the one-kernel-per-stage schedule (which TP > 1 needs between its all-reduces)
   bool use_step = false;
@@ -164,6 +171,7 @@ struct sirius_ctx {
     std::vector<uintptr_t> key;
     cudaGraphExec_t exec;
     unsigned long long kernels;
+    std::vector<ProfEv> evs;  // profiled graph: (class, start, end) event-record nodes
   };
   std::vector<GraphEntry> graphs;
   std::vector<void*> allocations;
@@ -196,6 +204,15 @@ sirius_status fail(sirius_ctx* c, sirius_status s, const std::string& msg) {
 enum ProfId { P_QKV = 0, P_ATTN = 1, P_OPROJ = 2, P_FFN = 3, P_HEAD = 4, P_VERIFY = 5, P_REWRITE = 6, P_STEP = 7, P_NUM = 8 };
 void prof_begin(sirius_ctx* c, int id) {
   if (!c->prof_on) return;
+  if (c->capturing) {  // event-record nodes inside the graph being captured
+    sirius_ctx::ProfEv e;
+    e.id = id;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    cudaEventRecordWithFlags(e.a, c->stream, cudaEventRecordExternal);
+    c->cap_evs.push_back(e);
+    return;
+  }
   if (c->prof_used == c->prof.size()) {
     sirius_ctx::ProfEv e;
     e.id = id;
@@ -208,6 +225,10 @@ void prof_begin(sirius_ctx* c, int id) {
 }
 void prof_end(sirius_ctx* c) {
   if (!c->prof_on) return;
+  if (c->capturing) {
+    cudaEventRecordWithFlags(c->cap_evs.back().b, c->stream, cudaEventRecordExternal);
+    return;
+  }
   cudaEventRecord(c->prof[c->prof_used].b, c->stream);
   ++c->prof_used;
 }
@@ -248,14 +269,30 @@ typedef std::vector<uintptr_t> GraphKey;
 // Capture `enqueue` (which only enqueues work on c->stream) into a CUDA graph the first time a key
 // is seen, then replay the instantiated graph: one launch per ABI call instead of ~130 kernels.
 // Bypassed while per-kernel profiling is on.
+// after a profiled graph's replay: wait for it and add its event pairs to the per-class totals
+sirius_status prof_collect(sirius_ctx* c, const std::vector<sirius_ctx::ProfEv>& evs) {
+  if (evs.empty()) return SIRIUS_OK;
+  CU(cudaStreamSynchronize(c->stream));
+  for (const auto& e : evs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) {
+      c->prof_tot[e.id] += ms;
+      c->prof_cnt[e.id] += 1;
+    }
+  }
+  return SIRIUS_OK;
+}
+
 template <class F>
-sirius_status run_graphed(sirius_ctx* c, const GraphKey& key, F enqueue) {
-  if (!c->use_graphs || c->prof_on) return enqueue();
+sirius_status run_graphed(sirius_ctx* c, const GraphKey& key0, F enqueue) {
+  if (!c->use_graphs) return enqueue();
+  GraphKey key = key0;
+  key.push_back(c->prof_on ? 1u : 0u);  // profiled graphs carry event-record nodes
   for (auto& g : c->graphs)
     if (g.key == key) {
       c->launches += g.kernels;
       CU(cudaGraphLaunch(g.exec, c->stream));
-      return SIRIUS_OK;
+      return prof_collect(c, g.evs);
     }
   // capture on a private stream (the caller's stream may be the legacy default stream, which cannot
   // be captured); the instantiated graph is then launched on the caller's stream
@@ -264,7 +301,10 @@ sirius_status run_graphed(sirius_ctx* c, const GraphKey& key, F enqueue) {
   cudaStream_t user = c->stream;
   CU(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
   c->stream = c->cap_stream;
+  c->capturing = true;
+  c->cap_evs.clear();
   sirius_status s = enqueue();
+  c->capturing = false;
   c->stream = user;
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
@@ -277,15 +317,25 @@ sirius_status run_graphed(sirius_ctx* c, const GraphKey& key, F enqueue) {
     c->use_graphs = false;
     c->sticky = SIRIUS_OK;
     c->launches = before;
+    for (auto& e : c->cap_evs) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    c->cap_evs.clear();
     return enqueue();
   }
   if (c->graphs.size() >= 256) {
     cudaGraphExecDestroy(c->graphs.front().exec);
+    for (auto& e : c->graphs.front().evs) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
     c->graphs.erase(c->graphs.begin());
   }
-  c->graphs.push_back({key, exec, c->launches - before});
+  c->graphs.push_back({key, exec, c->launches - before, c->cap_evs});
+  c->cap_evs.clear();
   CU(cudaGraphLaunch(exec, c->stream));
-  return SIRIUS_OK;
+  return prof_collect(c, c->graphs.back().evs);
 }
 
 // enqueue a copy of the device error word into the pinned host mirror (read by the next call)
@@ -301,6 +351,41 @@ sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev,
     int r = api.allReduce(p, p, n, kNcclFloat32, kNcclSum, c->comm, c->stream);
     if (r != 0) return fail(c, SIRIUS_ERR_NCCL, std::string("ncclAllReduce: ") + api.getErrorString(r));
   }
+  return SIRIUS_OK;
+}
+
+// ---- the decode CATS FFN of layer l (S4-S6) on residual rows base (+ delta): out = the FFN's
+// contribution to the residual (accumulated into out, which the O-proj GEMV zeroed, in atomic mode)
+sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float* base, const float* delta,
+                                float* res_out, float* out, bool dense, int32_t* n_active_out, int n_active_stride,
+                                float* gate_out, long long gate_stride) {
+  const sirius_config& cf = c->cfg;
+  FfnArgs f = {};
+  f.pro.mode = IN_RESID;
+  f.pro.base = base;
+  f.pro.delta = delta;
+  f.pro.norm_w = R.ffn_norm[l];
+  f.pro.eps = cf.rms_eps;
+  f.pro.res_out = res_out;
+  f.w_gate = R.w_gate[l];
+  f.w_up = R.w_up[l];
+  f.w_down = R.w_down[l];
+  f.F = c->Fr;
+  f.d = cf.d_model;
+  f.threshold = c->thresholds + l;
+  f.dense = dense ? 1 : 0;
+  f.part = R.ffn_part;
+  f.part_cnt = R.ffn_cnt;
+  f.barrier = R.ffn_barrier;
+  f.out = out;
+  f.n_active_out = n_active_out;
+  f.n_active_stride = n_active_stride;
+  f.atomic_out = c->ffn_atomic ? 1 : 0;
+  f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
+  f.gate_out = gate_out;
+  f.gate_stride = gate_stride;
+  const int grid = c->ffn_atomic ? std::min((c->Fr + 7) / 8, c->ffn_split * c->num_sms) : launch::ffn_grid(c->Fr, c->num_sms);
+  LCU(launch::ffn(f, cf.batch, grid, c->stream));
   return SIRIUS_OK;
 }
 
@@ -586,7 +671,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       alloc(c, &c->stats, (size_t)c->nranks * c->MAXM * c->accept_splits) ||
       alloc(c, &c->stats_gather, (size_t)cf.tp_size * c->MAXM * c->accept_splits) ||
       alloc(c, &c->dA_ptrs, 64) || alloc(c, &c->dF_ptrs, 64) || alloc(c, &c->pre_start, B) ||
-      alloc(c, &c->dec_nacc, B) ||
+      alloc(c, &c->dec_nacc, B) || alloc(c, &c->row_argmax, 256) ||
       alloc(c, &c->scratch_tok, 64))
     return cleanup_fail(SIRIUS_ERR_CUDA);
   if (cudaHostAlloc(&c->err_host, 64, cudaHostAllocDefault) != cudaSuccess ||
@@ -716,7 +801,13 @@ sirius_status sirius_destroy(sirius_ctx* c) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
-  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto& g : c->graphs) {
+    cudaGraphExecDestroy(g.exec);
+    for (auto& e : g.evs) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+  }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocations) cudaFree(p);
   if (c->err_host) cudaFreeHost(c->err_host);
@@ -872,7 +963,6 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     CU(cudaGetLastError());
     return SIRIUS_OK;
   }
-  const int ffn_grid = launch::ffn_grid(c->Fr, c->num_sms);
   for (int l = 0; l < L; ++l) {
     for (auto& R : c->ranks) {
       GemvArgs a = {};
@@ -960,36 +1050,16 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, B));
     for (auto& R : c->ranks) {
-      FfnArgs f = {};
-      f.pro.mode = IN_RESID;
-      f.pro.base = R.resA;
-      f.pro.delta = R.dA;
-      f.pro.norm_w = R.ffn_norm[l];
-      f.pro.eps = cf.rms_eps;
-      f.pro.res_out = R.resB;
-      f.w_gate = R.w_gate[l];
-      f.w_up = R.w_up[l];
-      f.w_down = R.w_down[l];
-      f.F = c->Fr;
-      f.d = d;
-      f.threshold = c->thresholds + l;
-      f.dense = dense ? 1 : 0;
-      f.part = R.ffn_part;
-      f.part_cnt = R.ffn_cnt;
-      f.barrier = R.ffn_barrier;
-      f.out = R.dF;
-      f.n_active_out = n_active_out ? n_active_out + l : nullptr;
-      f.n_active_stride = L;
-      f.atomic_out = c->ffn_atomic ? 1 : 0;
-      f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
+      float* g_out = nullptr;
+      long long g_stride = 0;
       if (gate_act_out) {  // [B, L, F] (emulated group: rank shards concatenated) or [B, L, F/tp]
         const int F = c->emulated ? cf.ffn_dim : c->Fr;
-        f.gate_out = gate_act_out + (size_t)l * F + (c->emulated ? (size_t)R.rank * c->Fr : 0);
-        f.gate_stride = (long long)L * F;
+        g_out = gate_act_out + (size_t)l * F + (c->emulated ? (size_t)R.rank * c->Fr : 0);
+        g_stride = (long long)L * F;
       }
       prof_begin(c, P_FFN);
-      LCU(launch::ffn(f, B, c->ffn_atomic ? std::min((c->Fr + 7) / 8, c->ffn_split * c->num_sms) : ffn_grid,
-                      c->stream));
+      OK(launch_decode_ffn(c, R, l, R.resA, R.dA, R.resB, R.dF, dense, n_active_out ? n_active_out + l : nullptr, L,
+                           g_out, g_stride));
       prof_end(c);
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
@@ -1113,6 +1183,7 @@ static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* kernel_to
   fa.n_accept = n_accept_out;
   fa.next_token = next_token_out;
   fa.q_out = q_out;
+  fa.row_argmax = n_accept_out == c->dec_nacc ? nullptr : c->row_argmax;  // verify rows only
   LCU(launch::accept_finalize(fa, B, c->stream));
   return SIRIUS_OK;
 }
@@ -1177,6 +1248,15 @@ sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t*
   return SIRIUS_OK;
 }
 
+sirius_status sirius_verify_row_argmax(sirius_ctx* c, int32_t* out) {
+  if (!c || !out) return SIRIUS_ERR_INVALID_ARG;
+  if (c->last_gamma < 1) return fail(c, SIRIUS_ERR_STATE, "no correct_kernel call yet");
+  OK(check_sticky(c));
+  CU(cudaMemcpyAsync(out, c->row_argmax, sizeof(int32_t) * c->cfg.batch * c->last_gamma, cudaMemcpyDeviceToDevice,
+                     c->stream));
+  return SIRIUS_OK;
+}
+
 // ---------------------------------------------------------------- NCCL bootstrap helpers (X4)
 int sirius_nccl_available(void) { return nccl().loaded ? 1 : 0; }
 int sirius_nccl_unique_id(void* out128) {
@@ -1238,6 +1318,10 @@ int sirius_debug_profile(sirius_ctx* c, int on) {
   if (!c) return -1;
   c->prof_on = on != 0;
   c->prof_used = 0;
+  for (int i = 0; i < 16; ++i) {
+    c->prof_tot[i] = 0.0;
+    c->prof_cnt[i] = 0;
+  }
   return 0;
 }
 // totals_ms[P_NUM], counts[P_NUM]: summed device time per kernel class since enabling (synchronises).
@@ -1246,8 +1330,8 @@ int sirius_debug_profile_read(sirius_ctx* c, float* totals_ms, int* counts) {
   if (!c) return -1;
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < P_NUM; ++i) {
-    totals_ms[i] = 0.f;
-    counts[i] = 0;
+    totals_ms[i] = (float)c->prof_tot[i];
+    counts[i] = c->prof_cnt[i];
   }
   for (size_t i = 0; i < c->prof_used; ++i) {
     float ms = 0.f;
@@ -1269,6 +1353,23 @@ int sirius_debug_buffer(sirius_ctx* c, int rank, int which, void* dst, size_t by
   if (which < 0 || which > 12) return -1;
   cudaStreamSynchronize(c->stream);
   return (int)cudaMemcpy(dst, src[which], bytes, cudaMemcpyDeviceToDevice);
+}
+
+// ---------------------------------------------------------------- test-only entry: the decode CATS FFN
+// Runs layer `layer`'s decode FFN kernel (exactly the launch sparse_decode_step makes; rank 0's shard)
+// on the residual rows x (DEV fp32 [batch, d]): h2 = RMSNorm(x), a = SiLU(h2 W_gate^T), CATS mask,
+// out (DEV fp32 [batch, d]) = sum over active neurons of a_i (h2 . W_up[i]) W_down[i]; gate_out (DEV
+// fp32 [batch, ffn/tp] or NULL) = a; n_active (DEV int32 [batch] or NULL).  Synchronous; returns a
+// sirius_status.
+int sirius_debug_ffn(sirius_ctx* c, int layer, const float* x, int dense, float* out, float* gate_out,
+                     int32_t* n_active) {
+  if (!c || !x || !out || layer < 0 || layer >= c->cfg.n_layers) return SIRIUS_ERR_INVALID_ARG;
+  const int B = c->cfg.batch, d = c->cfg.d_model;
+  CU(cudaMemsetAsync(out, 0, sizeof(float) * B * d, c->stream));
+  if (n_active) CU(cudaMemsetAsync(n_active, 0, sizeof(int32_t) * B, c->stream));
+  OK(launch_decode_ffn(c, c->ranks[0], layer, x, nullptr, nullptr, out, dense != 0, n_active, 1, gate_out, c->Fr));
+  CU(cudaStreamSynchronize(c->stream));
+  return SIRIUS_OK;
 }
 
 // ---------------------------------------------------------------- test-only entry: the tcgen05 GEMM

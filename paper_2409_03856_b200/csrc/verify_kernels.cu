@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(64) accept_finalize_kernel(AcceptFinalArgs a) 
     const float q = (i < gam - 1) ? expf(ld - lse) : expf(M - lse);
     q_s[i] = q;
     am_s[i] = (int)argmax_key_index(K);
+    if (a.row_argmax) a.row_argmax[(size_t)b * gam + i] = am_s[i];
     if (a.q_out) a.q_out[(size_t)b * gam + i] = q;
   }
   __syncthreads();

@@ -70,6 +70,7 @@ struct AcceptFinalArgs {
   int32_t* n_accept;
   int32_t* next_token;
   float* q_out;
+  int32_t* row_argmax;  // [B, gamma]: the full model's argmax of every verify row (ablation modes)
 };
 
 struct KvRewriteArgs {

@@ -9,6 +9,11 @@ Modes (the three rows of the north-star metric):
   "dense"  : greedy decode with the full model M_F every token
   "sparse" : greedy decode with the CATS-sparse model M_S only (CS-only)
   "sirius" : M_S drafts gamma-1 tokens, M_F verifies the kernel, accept/reject, rewrite, interleave
+
+Component ablation (Table 4; reading D27): Driver(..., rewrite, interleave,
+rollback) switches KV Rewrite / Interleave / Rollback independently (rollback needs interleave).
+Without rollback every kernel commits all gamma positions, a rejected draft replaced by the full
+model's argmax of its verify row when interleaving (sirius_verify_row_argmax).
 """
 from __future__ import annotations
 
@@ -27,6 +32,7 @@ class KernelLog:
     j: np.ndarray       # [B]
     next_token: np.ndarray
     q: Optional[np.ndarray] = None
+    advance: Optional[List[int]] = None  # per sequence, when not j + 1 (ablation without rollback)
 
 
 @dataclass
@@ -36,12 +42,18 @@ class GenOut:
     steps: int = 0  # decode steps launched
 
     def advances(self, b: int = 0) -> List[int]:
-        return [int(k.j[b]) + 1 for k in self.kernels]
+        return [int(k.j[b]) + 1 if k.advance is None else int(k.advance[b]) for k in self.kernels]
+
+    def rejection_positions(self, b: int = 0) -> List[int]:
+        """0-based draft index of every rejection (PAPER.md:678-685 histogram data)."""
+        return [int(k.j[b]) for k in self.kernels if int(k.j[b]) < k.tokens.shape[1] - 1]
 
 
 class Driver:
-    def __init__(self, ctx: S.Sirius):
+    def __init__(self, ctx: S.Sirius, rewrite: bool = True, interleave: bool = True, rollback: bool = True):
         import torch
+        assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
+        self.rewrite, self.interleave, self.rollback = rewrite, interleave, rollback
         self.ctx, self.torch = ctx, torch
         B, gm = ctx.batch, ctx.max_gamma
         dev = "cuda"
@@ -55,6 +67,7 @@ class Driver:
         self.n_accept = torch.zeros(B, dtype=i32, device=dev)
         self.next_tok = torch.zeros(B, dtype=i32, device=dev)
         self.q = torch.zeros((B, gm), dtype=torch.float32, device=dev)
+        self.row_am = torch.zeros((B, gm), dtype=torch.int32, device=dev)
         # pinned staging: out = [n_rows(B) | start(B) | pending(B) | pos(gm*B)], in = [n_accept | next | drafts]
         self.h_out = torch.zeros(3 * B + gm * B, dtype=i32).pin_memory()
         self.h_in = torch.zeros(2 * B + (gm + 1) * B, dtype=i32).pin_memory()
@@ -132,8 +145,11 @@ class Driver:
         else:
             self.kbuf[:, :gamma].copy_(self.drafts[:gamma].t())
             kt = self.kbuf[:, :gamma].contiguous()
+        ablate = not self.rollback
         self.ctx.correct_kernel(kt, cur, gamma, r, accept_mode, self.n_accept, self.next_tok,
-                                self.q if keep_q else None)
+                                self.q if (keep_q or ablate) else None)
+        if ablate:
+            self.ctx.sirius_verify_row_argmax(self.row_am)
         # D2H: accepted count, interleaved token, drafts (the one sync per kernel)
         n = 2 * B + gamma * B
         self.d_in[0:B].copy_(self.n_accept)
@@ -146,17 +162,30 @@ class Driver:
         j = h[0:B].copy()
         nxt = h[B:2 * B].copy()
         dr = h[2 * B:n].reshape(gamma, B)
-        self.log.append(KernelLog(list(self.T), dr.T.copy(), j, nxt,
-                                  self.q[:, :gamma].cpu().numpy() if keep_q else None))
+        qh = self.q[:, :gamma].cpu().numpy() if (keep_q or ablate) else None
+        self.log.append(KernelLog(list(self.T), dr.T.copy(), j, nxt, qh))
+        am = self.row_am[:, :gamma].cpu().numpy() if ablate else None
+        advs = []
         for b in range(B):
             jb = int(j[b])
-            self.out[b] += [int(x) for x in dr[1:jb + 1, b]] + [int(nxt[b])]
-            self.n_rows_h[b] = jb + 1
-            self.T[b] += jb + 1
-            self.pending[b] = int(nxt[b])
-        self.need_rewrite = True
+            if self.rollback:  # commit + rollback to the first rejection; interleave the full model's token
+                committed = [int(x) for x in dr[1:jb + 1, b]] + [int(nxt[b])]
+            else:  # no rollback: all gamma positions; rejected drafts interleaved (or kept)
+                committed = []
+                for i in range(gamma - 1):
+                    d_i = int(dr[i + 1, b])
+                    ok = (qh[b, i] >= r) if accept_mode == S.ACCEPT_THRESHOLD else (d_i == int(am[b, i]))
+                    committed.append(d_i if (ok or not self.interleave) else int(am[b, i]))
+                committed.append(int(am[b, gamma - 1]))
+            self.out[b] += committed
+            advs.append(len(committed))
+            self.n_rows_h[b] = len(committed)
+            self.T[b] += len(committed)
+            self.pending[b] = committed[-1]
+        self.log[-1].advance = None if self.rollback else advs
+        self.need_rewrite = self.rewrite
         self.kidx += 1
-        return int(j[0]) + 1
+        return advs[0]
 
     # ------------------------------------------------------------------ whole generations
     def sirius(self, prompts, n_tokens: int, gamma: int, r: float, accept_mode: int = S.ACCEPT_THRESHOLD,

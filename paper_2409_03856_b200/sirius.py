@@ -24,7 +24,7 @@ ACCEPT_EXACT_ARGMAX = 1
 
 # every symbol include/sirius.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
-               "sirius_destroy", "sirius_last_error", "sirius_version")
+               "sirius_verify_row_argmax", "sirius_destroy", "sirius_last_error", "sirius_version")
 
 
 class SiriusError(RuntimeError):
@@ -74,6 +74,8 @@ def load():
         lib.correct_kernel.restype = I
         lib.kv_rewrite.argtypes = [P, P, P]
         lib.kv_rewrite.restype = I
+        lib.sirius_verify_row_argmax.argtypes = [P, P]
+        lib.sirius_verify_row_argmax.restype = I
         lib.sirius_destroy.argtypes = [P]
         lib.sirius_destroy.restype = I
         lib.sirius_last_error.argtypes = [P]
@@ -81,6 +83,8 @@ def load():
         lib.sirius_version.argtypes = []
         lib.sirius_version.restype = ctypes.c_char_p
         lib.sirius_debug_gemm.argtypes = [P, I, I, P, P, P, I, I, I]
+        lib.sirius_debug_ffn.argtypes = [P, I, P, I, P, P, P]
+        lib.sirius_debug_ffn.restype = I
         lib.sirius_debug_buffer.argtypes = [P, I, I, P, ctypes.c_size_t]
         lib.sirius_debug_buffer.restype = I
         lib.sirius_debug_launches.argtypes = [P]
@@ -178,7 +182,15 @@ class Sirius:
     def kv_rewrite(self, start_pos, n_rows):
         self._check(self.lib.kv_rewrite(self.h, _ptr(start_pos), _ptr(n_rows)))
 
+    def sirius_verify_row_argmax(self, out):
+        self._check(self.lib.sirius_verify_row_argmax(self.h, _ptr(out)))
+
     # ---- instrumentation (bench / tests) ------------------------------------------------
+    def debug_ffn(self, layer: int, x, dense: bool, out, gate_out=None, n_active=None) -> None:
+        """Test-only: the decode CATS FFN kernel of `layer` on residual rows x [batch, d] (fp32 CUDA)."""
+        self._check(self.lib.sirius_debug_ffn(self.h, layer, _ptr(x), 1 if dense else 0, _ptr(out), _ptr(gate_out),
+                                              _ptr(n_active)))
+
     PROF_NAMES = ("qkv_gemv", "attn_decode", "oproj_gemv", "cats_ffn", "lm_head", "correct_kernel", "kv_rewrite",
                   "decode_step")
 

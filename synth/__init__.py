@@ -281,3 +281,14 @@ def layer_thresholds(cfg: ModelConfig, rho, seed: int = WEIGHT_SEED) -> np.ndarr
         # unique gains with multiplicities: mean over neurons == weighted mean over distinct gains
         out.append(cats_threshold(r, gains, float(np.mean(w * w))))
     return np.array(out, dtype=np.float32)
+
+
+def residual_rows(seed: int, n: int, d: int) -> np.ndarray:
+    """Seeded synthetic residual-stream rows (fp32 [n, d]) for kernel-isolated tests of one layer:
+    unit-RMS Gaussian rows with a few heavy channels (x8 on 1% of the coordinates), the shape of a
+    Llama residual stream.  Handed to both sides as the same array."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, d))
+    x[:, rng.choice(d, max(1, d // 100), replace=False)] *= 8.0
+    x *= rng.uniform(0.5, 3.0, (n, 1))
+    return x.astype(np.float32)

@@ -165,3 +165,63 @@ def test_batch8_prefill_single_row_chunks(tiny, lens):
         ref = oms[b].decode(toks[b], lens[b], False)
         err = np.abs(lo.cpu().numpy()[b] - ref.logits)
         assert np.all(err <= ABS + REL * np.abs(ref.logits)), (b, float(err.max()))
+
+
+def _tie_models(tiny, src_offset):
+    """Copy the LM-head row of the dense argmax token i of a decode row into row c = i + src_offset
+    (same 128-row tile): logits l_i == l_c exactly on both sides."""
+    cfg, wh, wd = tiny
+    prompt = synth.eval_prompt(cfg, 21, 30)
+    om = so.OracleModel(cfg, wh, max_seq=128, max_gamma=8)
+    pend = so.argmax_lowest(om.prefill_last(prompt))
+    row = om.decode(pend, len(prompt), False).logits
+    i = so.argmax_lowest(row)
+    c = i + src_offset
+    if c < 0 or c >= cfg.vocab or c // 128 != i // 128:
+        c = i - src_offset
+    wh2 = dict(wh)
+    wh2["lm_head"] = wh["lm_head"].copy()
+    wh2["lm_head"][c] = wh["lm_head"][i]
+    wd2 = dict(wd)
+    wd2["lm_head"] = wd["lm_head"].clone()
+    wd2["lm_head"][c] = wd["lm_head"][i]
+    om2 = so.OracleModel(cfg, wh2, max_seq=128, max_gamma=8)
+    om2.prefill_last(prompt)
+    ref = om2.decode(pend, len(prompt), False).logits
+    assert ref[i] == ref[c] and ref[i] == ref.max()
+    return cfg, wh2, wd2, prompt, pend, min(i, c), max(i, c)
+
+
+@pytest.mark.parametrize("src_offset", [1, -1])
+def test_forced_tie_lowest_index(tiny, src_offset):
+    """Reading D13 (lowest token id on exact ties) on both GPU paths: two identical LM-head rows give
+    an exact logit tie; the decode argmax (GEMV + packed-key atomics), the verify argmax (tcgen05
+    GEMM + accept kernel) and the EXACT_ARGMAX accept rule must all pick the LOWER index."""
+    from paper_2409_03856_b200 import sirius as S
+    cfg, wh2, wd2, prompt, pend, lo_id, hi_id = _tie_models(tiny, src_offset)
+    T = len(prompt)
+    thr = synth.layer_thresholds(cfg, 0.5)
+    ctx = make_ctx(cfg, wd2, thr)
+    f = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [T], f)
+    to = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lo = torch.zeros((1, cfg.vocab), dtype=torch.float32, device="cuda")
+    ctx.sparse_decode_step(i32([pend]), i32([T]), S.SIRIUS_DENSE, to, lo)
+    torch.cuda.synchronize()
+    lg = lo.cpu().numpy()[0]
+    assert lg[lo_id] == lg[hi_id] and lg[lo_id] == lg.max()  # exact tie on the GPU too
+    assert int(to.item()) == lo_id
+    na, nx = torch.zeros(1, dtype=torch.int32, device="cuda"), torch.zeros(1, dtype=torch.int32, device="cuda")
+    q = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+    lv = torch.zeros((1, 2, cfg.vocab), dtype=torch.float32, device="cuda")
+    for draft, j_expect in ((hi_id, 0), (lo_id, 1)):  # EXACT_ARGMAX: only the lowest tied id is "the argmax"
+        ctx.correct_kernel(i32([[pend, draft]]), i32([T]), 2, 0.0, S.ACCEPT_EXACT_ARGMAX, na, nx, q, lv)
+        torch.cuda.synchronize()
+        v0 = lv.cpu().numpy()[0, 0]
+        assert v0[lo_id] == v0[hi_id] and v0[lo_id] == v0.max()
+        assert int(na.item()) == j_expect
+        if j_expect == 0:
+            assert int(nx.item()) == lo_id  # interleaved token = lowest-index argmax of row 0
+    ctx.correct_kernel(i32([[pend]]), i32([T]), 1, 0.5, 0, na, nx, q[:, :1].contiguous())
+    torch.cuda.synchronize()
+    assert int(na.item()) == 0 and int(nx.item()) == lo_id

@@ -424,3 +424,8 @@ def test_paper_worked_numbers():
     assert abs(so.global_density(synth.LLAMA3_8B, 0.5, "fsparse") - g["fsparse_density_8b"]["printed"]) < 0.01
     assert abs(so.global_density(synth.LLAMA3_8B, 0.5, "csparse") - g["csparse_density_8b"]["printed"]) < 0.01
     assert abs(so.global_density(synth.LLAMA3_70B, 0.5, "csparse") - g["csparse_apu_70b"]["printed"]) < 0.01
+
+
+def test_top2_margin():
+    assert so.top2_margin(np.array([1.0, 3.0, 2.5])) == 0.5
+    assert so.top2_margin(np.array([3.0, 1.0, 3.0])) == 0.0

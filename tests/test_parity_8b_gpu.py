@@ -60,37 +60,66 @@ def gpu_decode(ctx, cfg, toks, pos, dense, tp_full=True):
     return to.cpu().numpy(), lo.cpu().numpy(), na.cpu().numpy(), ga.cpu().numpy()
 
 
+# End-to-end tolerance of a = SiLU(g) (D25): every kernel on the path is fp32-exact to
+# ~1e-7 relative (tests/test_ffn_kernel_gpu.py bounds the FFN a priori, with no exemption;
+# tests/diagnostics/stage_err.py per stage), but the two sides store K/V as bf16 rounded from fp32
+# (GPU) vs fp64 (oracle) values: ~0.25% of the stored elements differ by one bf16 ulp (2^-8
+# relative), which moves the attention output by up to ~6e-4 and a by up to ~3e-3 (measured,
+# 8B-2L, prompt 128).  That error of h2 = RMSNorm(x) (relative eps_h, ~1e-4) reaches g_i = s_i w'_i . h2
+# scaled by the neuron's gain s_i (w'_i the unit-scale row), so the bound carries an A_GAIN s_i term.
+# A neuron whose |a_ref| lies within that distance of t_l may then be kept on
+# one side and dropped on the other (an explained active-set difference): the two sides then run
+# different sparse models from that layer on — by up to |m_i W_down[i]| ~ 0.2 per residual element
+# for the heavy-gain neurons — so the strict tolerances apply to a layer's gate only while no
+# earlier layer of the row differed, and to the logits only when no layer differed; after a
+# difference the coarse ones catch gross errors.
+A_ABS, A_REL, A_GAIN = 2e-3, 1e-3, 2e-3
+A_ABS_AFTER_FLIP = 5e-2
+L_ABS_AFTER_FLIP, L_REL_AFTER_FLIP = 1e-1, 2e-2
+FLIP_STATS = {"rows": 0, "rows_with_difference": 0}
+_GAINS = {}
+
+
+def layer_gains(cfg, l):
+    """Per-neuron gain s_i of layer l's W_gate rows (the synthetic recipe, synth/)."""
+    key = (cfg.ffn_dim, l)
+    if key not in _GAINS:
+        spec = {s.name: s for s in synth.tensor_specs(cfg)}[f"layers.{l}.w_gate"]
+        _GAINS[key] = synth.GAIN_TABLE[synth.row_gain_k(spec.gain_id, cfg.ffn_dim).astype(int) + 24].astype(np.float64)
+    return _GAINS[key]
+
+
 def check_decode_row(cfg, thr, ref, tok_gpu, lg, na, ga, sparse):
-    """One sequence's decode row against the oracle's: logits, a = SiLU(g), active set (every
-    mismatch explained by the float error of a), count, argmax (pinned by the top-2 margin).
-    A neuron whose |a| lies within the float error of t_l may be kept on one side and dropped on
-    the other (an explained active-set flip); the two then compute different sparse models, so the
-    logit tolerance is only asserted for rows without a flip."""
-    flips = 0
-    if sparse:
-        flips = int(((np.abs(ga) >= thr[:, None]) != ref.mask.astype(bool)).sum())
-    if flips == 0:
+    """One sequence's decode row against the oracle's: a = SiLU(g) per layer, active set (every
+    difference explained by the float error of a, at most 8 per row), counts, logits, argmax (pinned
+    by the top-2 margin).  Returns the number of active-set differences."""
+    flips, clean = 0, True
+    for l in range(cfg.n_layers):
+        tol = (A_ABS if clean else A_ABS_AFTER_FLIP) + A_REL * np.abs(ref.gate[l]) + A_GAIN * layer_gains(cfg, l)
+        bad = np.abs(ga[l] - ref.gate[l]) > tol
+        assert not bad.any(), ("gate", l, clean, np.argwhere(bad)[:8].tolist(), ga[l][bad][:8], ref.gate[l][bad][:8])
+        if sparse:
+            act = np.abs(ga[l]) >= thr[l]
+            mism = act != ref.mask[l].astype(bool)
+            assert np.all(np.abs(np.abs(ref.gate[l][mism]) - thr[l]) <= np.abs(ga[l][mism] - ref.gate[l][mism]) + 1e-7)
+            assert int(na[l]) == int(act.sum())
+            flips += int(mism.sum())
+            clean = clean and not mism.any()
+        else:
+            assert int(na[l]) == cfg.ffn_dim
+    assert flips <= 8
+    FLIP_STATS["rows"] += 1
+    FLIP_STATS["rows_with_difference"] += int(not clean)
+    if clean:
         eps = check_logits(lg, ref.logits)
     else:
-        eps = float(np.abs(lg - ref.logits).max())
-    # a = SiLU(g) is an fp32 activation: the north star's float tolerance applies.  At 8B shapes a
-    # few K/V cache elements round to the neighbouring bf16 value (fp32 vs fp64 producer, 1 bf16
-    # ulp = 2^-8 relative), which moves later activations by ~1e-3 (DESIGN.md §2, parity rules);
-    # the active set stays pinned by the explained-mismatch rule below.
-    bad = np.abs(ga - ref.gate) > ABS + REL * np.abs(ref.gate)
-    assert not bad.any(), ("gate activations", np.argwhere(bad)[:8].tolist(), ga[bad][:8], ref.gate[bad][:8])
-    if sparse:
-        act = np.abs(ga) >= thr[:, None]
-        mism = act != ref.mask.astype(bool)
-        tt = np.repeat(thr[:, None], cfg.ffn_dim, 1)
-        assert np.all(np.abs(np.abs(ref.gate[mism]) - tt[mism]) <= np.abs(ga[mism] - ref.gate[mism]) + 1e-7)
-        assert np.array_equal(na, act.sum(1))
-        assert int(mism.sum()) <= 8
-    else:
-        assert np.all(na == cfg.ffn_dim)
+        err = np.abs(lg - ref.logits)
+        assert np.all(err <= L_ABS_AFTER_FLIP + L_REL_AFTER_FLIP * np.abs(ref.logits)), float(err.max())
+        eps = float(err.max())
     if margin(ref.logits) > 2 * eps:
         assert int(tok_gpu) == so.argmax_lowest(ref.logits)
     assert int(tok_gpu) == int(np.argmax(lg))
+    return flips
 
 
 def gpu_correct(ctx, cfg, kernel_tokens, T, r):
@@ -301,3 +330,42 @@ def test_8b2l_batched_decode_rows_path(l2, batch):
     refs = [oracle_script(cfg, wh, thr, p, 1, 6, 128) for p in prompts]
     ctx = make_ctx(cfg, sg.device_weights(cfg), thr, batch, 128)
     gpu_script(ctx, cfg, thr, prompts, refs, 1, 6)
+
+
+# ------------------------------------------------------------------ free-running, token-exact at 8B-2L
+EPS_E2E = 5e-3    # >= the largest logit difference measured on an 8B-2L row without an active-set difference
+EPS_DRAFT = 5e-2  # a sparse drafting row may carry an explained active-set difference (up to ~4e-2 measured)
+
+
+def ambiguity_events(ref, r):
+    """Rows where the float tolerance could legitimately change a decision: a drafting or verify row
+    whose top-2 margin is <= 2 eps, or an accept decision with |ln q - ln r| <= 2 eps + 1e-5."""
+    ev = 0
+    for k in ref.kernels:
+        ev += int(np.sum(k.draft_margin <= 2 * EPS_DRAFT))
+        ev += int(k.verify_margin[k.j] <= 2 * EPS_E2E)
+        g = len(k.tokens)
+        for i in range(min(k.j + 1, g - 1)):  # the decisions actually taken: accepts before j, reject at j
+            ev += int(abs(np.log(max(k.q[i], 1e-30)) - np.log(r)) <= 2 * EPS_E2E + 1e-5)
+    return ev
+
+
+@pytest.mark.parametrize("r,seed", [(0.1, 5), (0.3, 9)])
+def test_8b2l_free_running_token_exact(l2, r, seed):
+    """The whole Sirius loop free-running at the Llama-3-8B layer shapes (2 layers, full vocab), in
+    the bench's configuration (batch 1, gamma 16, CATS 50%): prompt 128, 48 generated tokens.  The
+    GPU (driver over the C ABI) and the oracle (so.generate) must produce identical tokens and
+    identical per-kernel advances; the oracle's rows are scanned for ambiguity events (a top-2 margin
+    or accept decision within the float tolerance), and the chosen prompts have none."""
+    from paper_2409_03856_b200 import driver
+    from synth import gpu as sg
+    cfg, wh = l2
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, seed, 128)
+    ref = so.generate(so.OracleModel(cfg, wh, max_seq=256, max_gamma=GAMMA), prompt, 48, GAMMA, r, thr)
+    assert ambiguity_events(ref, r) == 0
+    ctx = make_ctx(cfg, sg.device_weights(cfg), thr, 1, 256)
+    out = driver.Driver(ctx).sirius([prompt], 48, GAMMA, r)
+    assert out.tokens[0] == ref.tokens
+    assert out.advances(0) == ref.advances[:len(out.kernels)]
+    assert any(a < GAMMA for a in ref.advances) or r < 0.3  # the correction branch fires at r = 0.3

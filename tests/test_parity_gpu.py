@@ -261,3 +261,23 @@ def test_greedy_run_chunked_positions(tiny_models):
         d.greedy_run(d.pending, d.T, 50, dense)  # 7 chunks of 8 steps
         torch.cuda.synchronize()
         assert int(d.drafts[0, 0].item()) == ref[50]
+
+
+@pytest.mark.parametrize("mode", ["interleave", "kv_rewrite", "kv_rewrite+interleave", "rollback+interleave"])
+@pytest.mark.parametrize("r", [0.3, 0.6])
+def test_component_ablation_token_exact(tiny_models, mode, r):
+    """Table 4's component ablation (reading D27) through the same kernels: the
+    driver's KV-rewrite / interleave / rollback switches against the oracle's, token for token."""
+    from paper_2409_03856_b200 import driver
+    flags = {"interleave": (False, True, False), "kv_rewrite": (True, False, False),
+             "kv_rewrite+interleave": (True, True, False), "rollback+interleave": (False, True, True)}[mode]
+    cfg, wh, wd = tiny_models
+    thr = synth.layer_thresholds(cfg, 0.1)
+    prompt = synth.eval_prompt(cfg, 2, 64)
+    ref = so.generate(so.OracleModel(cfg, wh, max_seq=256, max_gamma=16), prompt, 32, 4, r, thr,
+                      rewrite=flags[0], interleave=flags[1], rollback=flags[2])
+    d = driver.Driver(make_ctx(cfg, wd, thr), rewrite=flags[0], interleave=flags[1], rollback=flags[2])
+    out = d.sirius([prompt], 32, 4, r)
+    assert out.tokens[0] == ref.tokens
+    assert out.advances(0)[:len(ref.advances)] == ref.advances[:len(out.kernels)]
+    assert [k.j for k in ref.kernels][:len(out.kernels)] == [int(k.j[0]) for k in out.kernels][:len(ref.kernels)]
