@@ -31,6 +31,22 @@ SIRIUS_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+SIRIUS_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+SIRIUS_DEV void tma_load_4d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar,
+                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6], %7;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 SIRIUS_DEV void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -146,9 +162,14 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_ptr_s = reinterpret_cast<uint32_t*>(acc_empty + 2);
   unsigned* flag_s = tmem_ptr_s + 1;
-  const int NBUF = 2 * NACC * MP <= 512 ? 2 : 1;
+  // Activation terms side by side along N (one 128 x NB*MP x 16 MMA per k-step and operand instead of
+  // NB MMAs of N = MP: the verify GEMMs at MP = 16 were bound by the MMA issue rate, not by HBM);
+  // the epilogue sums the NB accumulator column groups.  NB*MP > 256: one MMA per term, one group.
+  const bool cat = NB * MP <= 256;
+  const int ACCW = cat ? NB * MP : MP;  // accumulator columns per operand
+  const int NBUF = 2 * NACC * ACCW <= 512 ? 2 : 1;
   uint32_t ncols = 32;
-  while (ncols < (uint32_t)(NBUF * NACC * MP)) ncols <<= 1;
+  while (ncols < (uint32_t)(NBUF * NACC * ACCW)) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -176,9 +197,25 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_ptr_s;
   // instruction descriptor, kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
   // both K-major, N>>3 at [17,23), M>>4 at [24,29)
-  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((128u >> 4) << 24);
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((cat ? NB * MP : MP) >> 3) << 17) |
+                         ((128u >> 4) << 24);
   const uint32_t tx_bytes = NACC * A_BYTES + NB * b_bytes;
   const long long nq = w1 - w0;  // the CTA's k-iterations, over all its segments
+  // weight tiles of a stage: [x][128 rows][128 B] — one 3-D op (box 64 x 128 rows x KBOX) per operand,
+  // or KBOX 2-D boxes.  TMA ops have a fixed per-op cost (tools/bw_probe.cu: 1-D bulk copies of 4 / 8 /
+  // 16 KB stream at 3.0 / 6.0 / 7.1 TB/s whatever the ring depth), so a stage is as few ops as possible.
+  auto load_a = [&](uint8_t* st, int t, int kc, uint64_t* bar, uint64_t pol) {
+    if (g.coarse) {
+      tma_load_3d(st, &tmA0, 0, t * 128, kc / 64, bar, pol);
+      if (DUAL) tma_load_3d(st + A_BYTES, &tmA1, 0, t * 128, kc / 64, bar, pol);
+    } else {
+#pragma unroll
+      for (int x = 0; x < KBOX; ++x) {
+        tma_load_2d(st + x * BOX_BYTES, &tmA0, kc + 64 * x, t * 128, bar, pol);
+        if (DUAL) tma_load_2d(st + A_BYTES + x * BOX_BYTES, &tmA1, kc + 64 * x, t * 128, bar, pol);
+      }
+    }
+  };
   pdl_trigger();
 
   if (warp == 4) {
@@ -191,11 +228,7 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* st = smem + (size_t)i * stage_bytes;
         mbar_arrive_expect_tx(&full[i], tx_bytes);
         const int t = (int)(w / g.kb), kc = (int)(w % g.kb) * 64 * KBOX;
-#pragma unroll
-        for (int x = 0; x < KBOX; ++x) {
-          tma_load_2d(st + x * BOX_BYTES, &tmA0, kc + 64 * x, t * 128, &full[i], pol_w);
-          if (DUAL) tma_load_2d(st + A_BYTES + x * BOX_BYTES, &tmA1, kc + 64 * x, t * 128, &full[i], pol_w);
-        }
+        load_a(st, t, kc, &full[i], pol_w);
       }
       gstamp(g, 1);
       pdl_wait();
@@ -208,18 +241,20 @@ __global__ void __launch_bounds__(192, 1)
         if (q >= npre) {
           mbar_wait(&empty[s], ((uint32_t)(q / stages) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&full[s], tx_bytes);
+          load_a(st, t, kc, &full[s], pol_w);
+        }
+        // B boxes of a stage: [x][term][MP rows][128 B]
+        if (g.coarse) {  // all terms, rows and K boxes of the stage in one 4-D op
+          tma_load_4d(st + NACC * A_BYTES, &tmB, 0, g.row0, 0, kc / 64, &full[s], pol_x);
+        } else {
 #pragma unroll
           for (int x = 0; x < KBOX; ++x) {
-            tma_load_2d(st + x * BOX_BYTES, &tmA0, kc + 64 * x, t * 128, &full[s], pol_w);
-            if (DUAL) tma_load_2d(st + A_BYTES + x * BOX_BYTES, &tmA1, kc + 64 * x, t * 128, &full[s], pol_w);
+            uint8_t* bx = st + NACC * A_BYTES + (size_t)x * NB * MP * 128;
+            for (int p = 0; p < NB; ++p)
+              for (int r = 0; r < MP / 16; ++r)
+                tma_load_2d(bx + (p * MP + r * 16) * 128, &tmB, kc + 64 * x, p * g.plane_rows + g.row0 + r * 16,
+                            &full[s], pol_x);
           }
-        }
-#pragma unroll
-        for (int x = 0; x < KBOX; ++x) {
-          uint8_t* bx = st + NACC * A_BYTES + x * (b_bytes / KBOX);
-          for (int p = 0; p < NB; ++p)
-            for (int r = 0; r < MP / 16; ++r)
-              tma_load_2d(bx + p * b_bytes + r * 2048, &tmB, kc + 64 * x, p * g.plane_rows + g.row0 + r * 16, &full[s], pol_x);
         }
       }
     }
@@ -233,7 +268,7 @@ __global__ void __launch_bounds__(192, 1)
         const int buf = sidx % NBUF;
         if (sidx >= NBUF) mbar_wait(&acc_empty[buf], (uint32_t)((sidx / NBUF) - 1) & 1u);
         tc_fence_after();
-        const uint32_t acc = tmem + (uint32_t)(buf * NACC * MP);
+        const uint32_t acc = tmem + (uint32_t)(buf * NACC * ACCW);
         for (long long i = 0; w + i < wend; ++i, ++q) {
           const int s = (int)(q % stages);
           mbar_wait(&full[s], (uint32_t)(q / stages) & 1u);
@@ -244,13 +279,21 @@ __global__ void __launch_bounds__(192, 1)
           for (int x = 0; x < KBOX; ++x) {
             const uint64_t a0 = sw128_desc(st + x * BOX_BYTES);
             const uint64_t a1 = DUAL ? sw128_desc(st + A_BYTES + x * BOX_BYTES) : 0ull;
+            uint8_t* bx = st + NACC * A_BYTES + (size_t)x * NB * MP * 128;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 64 = 4 x UMMA_K(16); +32 bytes per step inside the swizzle atom
-              for (int p = 0; p < NB; ++p) {  // the activation's bf16 terms, all into one accumulator
-                const uint64_t bp = sw128_desc(st + NACC * A_BYTES + p * b_bytes + x * (b_bytes / KBOX));
-                const uint32_t accf = (i > 0 || x > 0 || k > 0 || p > 0) ? 1u : 0u;
+              if (cat) {  // all terms in one MMA (N = NB * MP), each into its own column group
+                const uint64_t bp = sw128_desc(bx);
+                const uint32_t accf = (i > 0 || x > 0 || k > 0) ? 1u : 0u;
                 mma_bf16(acc, a0 + 2 * k, bp + 2 * k, idesc, accf);
-                if (DUAL) mma_bf16(acc + MP, a1 + 2 * k, bp + 2 * k, idesc, accf);
+                if (DUAL) mma_bf16(acc + ACCW, a1 + 2 * k, bp + 2 * k, idesc, accf);
+              } else {
+                for (int p = 0; p < NB; ++p) {  // the activation's bf16 terms, all into one accumulator
+                  const uint64_t bp = sw128_desc(bx + p * MP * 128);
+                  const uint32_t accf = (i > 0 || x > 0 || k > 0 || p > 0) ? 1u : 0u;
+                  mma_bf16(acc, a0 + 2 * k, bp + 2 * k, idesc, accf);
+                  if (DUAL) mma_bf16(acc + ACCW, a1 + 2 * k, bp + 2 * k, idesc, accf);
+                }
               }
             }
           }
@@ -271,14 +314,25 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&acc_full[buf], (uint32_t)(sidx / NBUF) & 1u);
       if (tid == 0 && sidx == 0) gstamp(g, 4);
       tc_fence_after();
-      const uint32_t tbase = tmem + (uint32_t)(buf * NACC * MP) + ((uint32_t)(warp * 32) << 16);
+      const uint32_t tbase = tmem + (uint32_t)(buf * NACC * ACCW) + ((uint32_t)(warp * 32) << 16);
       const int n = t * 128 + tid;
       const bool complete = (kbeg == 0 && wend == (long long)(t + 1) * g.kb);
+      const int ngrp = cat ? NB : 1;
+      // columns j0..j0+15 of operand a, the term column groups summed in term order
+      auto acc_ld = [&](int a, int j0, float* v) {
+        tmem_ld16(tbase + a * ACCW + j0, v);
+        for (int p = 1; p < ngrp; ++p) {
+          float u[16];
+          tmem_ld16(tbase + a * ACCW + p * MP + j0, u);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += u[j];
+        }
+      };
       if (complete) {
         for (int j0 = 0; j0 < MP; j0 += 16) {
           float v0[16], v1[16];
-          tmem_ld16(tbase + j0, v0);
-          if (DUAL) tmem_ld16(tbase + MP + j0, v1);
+          acc_ld(0, j0, v0);
+          if (DUAL) acc_ld(1, j0, v1);
 #pragma unroll
           for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, v0[j], DUAL ? v1[j] : 0.f);
         }
@@ -291,7 +345,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int j0 = 0; j0 < MP; j0 += 16) {
           float v[16];
           for (int a = 0; a < NACC; ++a) {
-            tmem_ld16(tbase + a * MP + j0, v);
+            acc_ld(a, j0, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j) mine[((size_t)a * 256 + j0 + j) * 128 + tid] = v[j];
           }
@@ -352,30 +406,64 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// 2-D bf16 tensor map over a row-major [rows, K] matrix; box = 64 (K) x box_rows, SWIZZLE_128B.
-bool make_tmap(void* map, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
+// bf16 tensor map, SWIZZLE_128B (64-element = 128-byte inner box), rank 2..4; strides in bytes.
+static bool encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {K, rows};
-  cuuint64_t strides[1] = {K * 2};
-  cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+// weights [N, K] row-major.  coarse: 3-D view (64, N, K/64) — strides K*2 (rows), 128 B (K blocks) — with a
+// box of 64 x 128 rows x kbox, so one op fetches a stage's [kbox][128 rows][64] tile; else 2-D box 64 x 128.
+static bool map_weights(CUtensorMap* m, const void* w, int N, int K, int kbox, bool coarse) {
+  if (coarse) {
+    cuuint64_t dims[3] = {64, (cuuint64_t)N, (cuuint64_t)(K / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+    cuuint32_t box[3] = {64, 128, (cuuint32_t)kbox};
+    return encode(m, w, 3, dims, strides, box);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)N};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {64, 128};
+  return encode(m, w, 2, dims, strides, box);
+}
+// activation term planes [nt][rows][K].  coarse: 4-D view (64, rows, nt, K/64) with a box of
+// 64 x MP x nt x kbox -> smem [kbox][nt][MP][64] in one op; else 2-D [nt * rows, K], box 64 x 16 rows.
+static bool map_acts(CUtensorMap* m, const void* x, int nt, int rows, int K, int MP, int kbox, bool coarse) {
+  if (coarse) {
+    cuuint64_t dims[4] = {64, (cuuint64_t)rows, (cuuint64_t)nt, (cuuint64_t)(K / 64)};
+    cuuint64_t strides[3] = {(cuuint64_t)K * 2, (cuuint64_t)rows * K * 2, 128};
+    cuuint32_t box[4] = {64, (cuuint32_t)MP, (cuuint32_t)nt, (cuuint32_t)kbox};
+    return encode(m, x, 4, dims, strides, box);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)nt * rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {64, 16};
+  return encode(m, x, 2, dims, strides, box);
+}
+int g_gemm_coarse = 1;  // SIRIUS_GEMM_COARSE=0: one TMA op per 64-wide box (A/B timing)
 
 size_t gemm_workspace_bytes(int num_sms) { return (size_t)num_sms * 2 * 2 * 256 * 128 * sizeof(float); }
 
 int g_gemm_kbox = 2;  // 64-wide K boxes per stage (SIRIUS_GEMM_KBOX)
 
 template <bool DUAL, int KBOX>
-static cudaError_t gemm_k(const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b, GemmArgs g, int MP,
-                          int num_sms, size_t smem_budget, cudaStream_t st) {
+static cudaError_t gemm_k(const void* w0, const void* w1, const void* x, GemmArgs g, int MP, int num_sms,
+                          size_t smem_budget, cudaStream_t st) {
   const int NACC = DUAL ? 2 : 1;
   const int NB = g.nterms;
   g.kb = (g.K + 64 * KBOX - 1) / (64 * KBOX);
+  // coarse boxes need whole 64-wide K blocks and <= 256 activation rows per box
+  g.coarse = (g_gemm_coarse && g.K % 64 == 0 && MP <= 256) ? 1 : 0;
+  CUtensorMap a0, a1, b;
+  if (!map_weights(&a0, w0, g.N, g.K, KBOX, g.coarse) || (DUAL && !map_weights(&a1, w1, g.N, g.K, KBOX, g.coarse)) ||
+      !map_acts(&b, x, NB, g.plane_rows, g.K, MP, KBOX, g.coarse))
+    return cudaErrorInvalidValue;
+  if (!DUAL) a1 = a0;
   const size_t stage_bytes = ((size_t)KBOX * (NACC * 16384 + (size_t)NB * MP * 128) + 1023) & ~(size_t)1023;
   const size_t extra = 1024 + 512;
   int stages = (int)((smem_budget - extra) / stage_bytes);
@@ -387,16 +475,13 @@ static cudaError_t gemm_k(const CUtensorMap* a0, const CUtensorMap* a1, const CU
   auto kern = gemm_tc_kernel<DUAL, KBOX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_chain(kern, dim3(grid), dim3(192), smem, st, *a0, *a1, *b, g, MP, stages);
+  return launch_chain(kern, dim3(grid), dim3(192), smem, st, a0, a1, b, g, MP, stages);
 }
 
-cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const GemmArgs& g, int MP, int num_sms,
+cudaError_t gemm(const void* a0, const void* a1, const void* b, const GemmArgs& g, int MP, int num_sms,
                  size_t smem_budget, cudaStream_t st) {
   if (MP < 16 || MP > 256 || MP % 16 || g.nterms < 1 || g.nterms > 3) return cudaErrorInvalidValue;
-  const bool dual = tmA1 != nullptr;
-  const CUtensorMap* a0 = reinterpret_cast<const CUtensorMap*>(tmA0);
-  const CUtensorMap* a1 = reinterpret_cast<const CUtensorMap*>(dual ? tmA1 : tmA0);
-  const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmB);
+  const bool dual = a1 != nullptr;
   // KBOX boxes per stage need room for >= 2 stages (dual operands at large MP fall back to fewer)
   auto fits = [&](int kb) {
     return (size_t)kb * ((dual ? 2 : 1) * 16384 + (size_t)g.nterms * MP * 128) * 2 + 1536 <= smem_budget;

@@ -15,6 +15,8 @@ struct GemmArgs {
   int nterms;           // B operand terms (1: plain bf16 activations; 3: fp32 activations split3)
   int plane_rows;       // rows between the B operand's term planes in its tensor map
   int row0;             // first B operand row of this launch (row chunks of large M)
+  int coarse;           // 1: one TMA op per stage per operand (3-D weight / 4-D activation boxes);
+                        // 0: one op per 64-wide weight box and per 16-row activation term box
   float* part;          // stream-K partials [num_sms, 2, NACC, 256, 128]
   unsigned* counters;   // [n_tiles] (self-resetting)
   unsigned long long* trace;  // debug: [8][grid] %globaltimer stamps of thread 0 / the MMA thread, or NULL
@@ -28,14 +30,13 @@ struct GemmArgs {
 };
 
 namespace launch {
-constexpr size_t kTmapBytes = 128;  // sizeof(CUtensorMap)
-bool make_tmap(void* map, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows);
 size_t gemm_workspace_bytes(int num_sms);
-// tmA1 == nullptr: single GEMM (fp32 out); else dual gate/up GEMM with the SwiGLU epilogue.
-// tmB: the activation operand, g.nterms planes of g.plane_rows rows each ([nterms * plane_rows, K]);
-// with 3 terms (split3 of an fp32 tensor) every term is multiplied and accumulated: fp32 activations
-// on the bf16 tensor cores, exactly represented.
-cudaError_t gemm(const void* tmA0, const void* tmA1, const void* tmB, const GemmArgs& g, int MP, int num_sms,
+// w1 == nullptr: single GEMM (fp32 out); else dual gate/up GEMM with the SwiGLU epilogue.  w0, w1: bf16
+// weights [N, K] row-major.  x: the activation operand, g.nterms planes of g.plane_rows rows each
+// ([nterms][plane_rows][K] bf16); with 3 terms (split3 of an fp32 tensor) every term is multiplied and
+// accumulated: fp32 activations on the bf16 tensor cores, exactly represented.  The tensor maps are
+// encoded here for the launch's tile shape (captured by value when the launch is graph-captured).
+cudaError_t gemm(const void* w0, const void* w1, const void* x, const GemmArgs& g, int MP, int num_sms,
                  size_t smem_budget, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius

@@ -31,6 +31,7 @@ int decode_step_splits(int B, int KV, int num_sms);
 cudaError_t decode_step(const StepArgs& a, int B, int grid, cudaStream_t st);
 bool attn_stage_supported(int hd, int G);
 extern int g_gemm_kbox;
+extern int g_gemm_coarse;
 cudaError_t attn_stage(const StepArgs& a, int l, int B, cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius
@@ -77,10 +78,6 @@ constexpr int kAttnRowUnits = 1024;  // (sequence, kv head, row block, split) pa
 }  // namespace
 
 // ----------------------------------------------------------------------------- context
-struct TmapBuf {
-  alignas(64) unsigned char b[128];
-};
-
 struct RankState {
   int rank = 0;
   // weights (borrowed) + owned transposed W_down copies for the verify GEMM (K-major in ffn)
@@ -100,9 +97,6 @@ struct RankState {
   unsigned long long* ffn_barrier = nullptr;
   unsigned* attn_bar = nullptr;  // split-group barriers (count, generation) of the attention kernels
   unsigned *attn_cnt = nullptr, *gemm_cnt = nullptr, *head_cnt = nullptr;
-  // tensor maps
-  std::vector<TmapBuf> tm_qkv, tm_o, tm_gate, tm_up, tm_down;
-  TmapBuf tm_head, tm_xn, tm_ob, tm_mb;  // activation maps: [3 * MAXM, K], box 16 rows
 };
 
 struct sirius_ctx {
@@ -405,9 +399,8 @@ struct GemmMask {  // CATS mask of the dual (SwiGLU) GEMM in the batched sparse 
 
 // out: fp32 [M, ldc] (single) or, dual (wb != NULL), the SwiGLU product's three bf16 term planes
 // (plane stride MAXM * ldc).  x: the activation's three term planes ([3 * MAXM, K] map).
-sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const TmapBuf* wb, const TmapBuf& x, int N,
-                       int K, int M, void* out, int ldc, unsigned long long* trace = nullptr,
-                       const GemmMask* mask = nullptr) {
+sirius_status run_gemm(sirius_ctx* c, RankState& R, const void* wa, const void* wb, const void* x, int N, int K,
+                       int M, void* out, int ldc, unsigned long long* trace = nullptr, const GemmMask* mask = nullptr) {
   GemmArgs g = {};
   g.trace = trace;
   if (mask) {
@@ -440,7 +433,7 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const TmapBuf& wa, const Tma
     if (gc.gate_out) gc.gate_out += (size_t)r0 * gc.gate_stride;
     if (r0) gc.trace = nullptr;
     const int MP = round_up(Mc, 16);
-    LCU(launch::gemm(wa.b, wb ? wb->b : nullptr, x.b, gc, MP, c->num_sms,
+    LCU(launch::gemm(wa, wb, x, gc, MP, c->num_sms,
                      MP <= 64 ? c->gemm_smem : c->smem_optin, c->stream));
   }
   return SIRIUS_OK;
@@ -480,7 +473,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       na.plane = (size_t)c->MAXM * d;
       LCU(launch::norm_rows(na, M, c->stream));
       unsigned long long* gtr = (!to_cache && l == c->trace_layer && c->trace) ? c->trace + 8 * 1024 : nullptr;
-      OK(run_gemm(c, R, R.tm_qkv[l], nullptr, R.tm_xn, c->Nqkv, d, M, R.qkv, c->Nqkv, gtr));
+      OK(run_gemm(c, R, R.w_qkv[l], nullptr, R.xn3, c->Nqkv, d, M, R.qkv, c->Nqkv, gtr));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
       if (mode == ROWS_DECODE && c->attn_stage) {
@@ -507,7 +500,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         sa.group_bar = R.attn_bar;
         sa.err = c->err_dev;
         LCU(launch::attn_stage(sa, l, cf.batch, c->stream));
-        OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob, d, c->Hr * hd, M, R.dA, d));
+        OK(run_gemm(c, R, R.w_o[l], nullptr, R.ob3, d, c->Hr * hd, M, R.dA, d));
         continue;
       }
       RopeStoreArgs ra = {};
@@ -553,7 +546,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       int splits = launch::attn_rows_splits(nseq, c->KVr, row_blocks, cf.max_seq, c->num_sms);
       while (splits > 1 && nseq * c->KVr * row_blocks * splits > kAttnRowUnits) --splits;  // workspace bound
       LCU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
-      OK(run_gemm(c, R, R.tm_o[l], nullptr, R.tm_ob, d, c->Hr * hd, M, R.dA, d, gtr ? gtr + 8 * 1024 : nullptr));
+      OK(run_gemm(c, R, R.w_o[l], nullptr, R.ob3, d, c->Hr * hd, M, R.dA, d, gtr ? gtr + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
     for (auto& R : c->ranks) {
@@ -580,8 +573,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         mk.gate_out = gate_act_out + (size_t)l * Ff + (c->emulated ? (size_t)R.rank * c->Fr : 0);
         mk.gate_stride = (long long)L * Ff;
       }
-      OK(run_gemm(c, R, R.tm_gate[l], &R.tm_up[l], R.tm_xn, c->Fr, d, M, R.mb3, c->Fr, gtr2, &mk));
-      OK(run_gemm(c, R, R.tm_down[l], nullptr, R.tm_mb, d, c->Fr, M, R.dF, d, gtr2 ? gtr2 + 8 * 1024 : nullptr));
+      OK(run_gemm(c, R, R.w_gate[l], R.w_up[l], R.xn3, c->Fr, d, M, R.mb3, c->Fr, gtr2, &mk));
+      OK(run_gemm(c, R, R.w_down_t[l], nullptr, R.mb3, d, c->Fr, M, R.dF, d, gtr2 ? gtr2 + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
   }
@@ -660,6 +653,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_GEMM_KBOX")) launch::g_gemm_kbox = atoi(e);
+  if (const char* e = getenv("SIRIUS_GEMM_COARSE")) launch::g_gemm_coarse = atoi(e);
   auto cleanup_fail = [&](sirius_status s) {
     sirius_destroy(c);
     return s;
@@ -741,28 +735,6 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       if (alloc(c, &R.w_down_t[l], (size_t)d * c->Fr, false)) return cleanup_fail(SIRIUS_ERR_CUDA);
       if (launch::transpose_bf16(R.w_down[l], R.w_down_t[l], c->Fr, d, c->stream) != cudaSuccess)
         return cleanup_fail(SIRIUS_ERR_CUDA);
-    }
-    // tensor maps: weights (box 128 rows) and activations (box 16 rows)
-    R.tm_qkv.resize(L);
-    R.tm_o.resize(L);
-    R.tm_gate.resize(L);
-    R.tm_up.resize(L);
-    R.tm_down.resize(L);
-    bool ok = true;
-    for (int l = 0; l < L; ++l) {
-      ok &= launch::make_tmap(R.tm_qkv[l].b, R.w_qkv[l], c->Nqkv, d, 128);
-      ok &= launch::make_tmap(R.tm_o[l].b, R.w_o[l], d, c->Hr * hd, 128);
-      ok &= launch::make_tmap(R.tm_gate[l].b, R.w_gate[l], c->Fr, d, 128);
-      ok &= launch::make_tmap(R.tm_up[l].b, R.w_up[l], c->Fr, d, 128);
-      ok &= launch::make_tmap(R.tm_down[l].b, R.w_down_t[l], d, c->Fr, 128);
-    }
-    ok &= launch::make_tmap(R.tm_head.b, R.lm_head, c->Vr, d, 128);
-    ok &= launch::make_tmap(R.tm_xn.b, R.xn3, 3 * M, d, 16);
-    ok &= launch::make_tmap(R.tm_ob.b, R.ob3, 3 * M, c->Hr * hd, 16);
-    ok &= launch::make_tmap(R.tm_mb.b, R.mb3, 3 * M, c->Fr, 16);
-    if (!ok) {
-      c->last_error = "cuTensorMapEncodeTiled failed";
-      return cleanup_fail(SIRIUS_ERR_CUDA);
     }
   }
   cudaMemcpy(c->dA_ptrs, dA_h.data(), sizeof(float*) * dA_h.size(), cudaMemcpyHostToDevice);
@@ -1148,7 +1120,7 @@ static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* kernel_to
     LCU(launch::norm_rows(na, M, c->stream));
     float* lo = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : R.logits;
     const int ldl = logits_out ? (c->emulated ? cf.vocab : c->Vr) : c->Vr;
-    OK(run_gemm(c, R, R.tm_head, nullptr, R.tm_xn, c->Vr, d, M, lo, ldl));
+    OK(run_gemm(c, R, R.lm_head, nullptr, R.xn3, c->Vr, d, M, lo, ldl));
     AcceptStatsArgs as = {};
     as.logits = lo;
     as.ldl = ldl;
@@ -1389,9 +1361,8 @@ int sirius_debug_gemm(const void* X, int nterms, int x_rows, const void* Wt, con
     if (cudaMalloc(&cnt, 65536 * sizeof(unsigned))) return -1;
     cudaMemset(cnt, 0, 65536 * sizeof(unsigned));
   }
-  TmapBuf ta, tb, tx;
-  if (!launch::make_tmap(ta.b, Wt, N, K, 128) || !launch::make_tmap(tx.b, X, (uint64_t)nterms * x_rows, K, 16)) return -2;
-  if (W2 && !launch::make_tmap(tb.b, W2, N, K, 128)) return -2;
+  if (const char* e = getenv("SIRIUS_GEMM_KBOX")) launch::g_gemm_kbox = atoi(e);
+  if (const char* e = getenv("SIRIUS_GEMM_COARSE")) launch::g_gemm_coarse = atoi(e);
   GemmArgs g = {};
   g.N = N;
   g.K = K;
@@ -1405,7 +1376,7 @@ int sirius_debug_gemm(const void* X, int nterms, int x_rows, const void* Wt, con
   g.plane_rows = x_rows;
   g.part = part;
   g.counters = cnt;
-  cudaError_t e = launch::gemm(ta.b, W2 ? tb.b : nullptr, tx.b, g, round_up(M, 16), sms, (size_t)optin - 1024, 0);
+  cudaError_t e = launch::gemm(Wt, W2, X, g, round_up(M, 16), sms, (size_t)optin - 1024, 0);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaDeviceSynchronize();
 }

@@ -30,6 +30,9 @@ last = fin[-1]
 j = last
 while j > 0 and names[j] != "gemv_kernel": j -= 1
 seg_summary("correct_kernel (last)", order[j + 1:last + 1])
+# the verify's first layers launch by launch (GEMMs in order: QKV, O, gate+up, down)
+print("   first verify launches:", ", ".join(f"{names[i].replace('_kernel', '')} {launch[order[i]].get('gpu__time_duration.sum', 0) / 1e3:.1f}"
+                                         for i in range(j + 1, min(j + 18, last + 1))))
 # one decode step: the launches between the last two head GEMVs before the verify
 heads = [i for i in range(j + 1) if names[i] == "gemv_kernel" and launch[order[i]].get("dram__bytes_read.sum", 0) > 5e8]
 if len(heads) >= 2:
