@@ -21,6 +21,7 @@ namespace sirius {
 namespace launch {
 int gemv_grid(int rows, int num_sms);
 cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st);
+
 cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st);
 int ffn_grid(int F, int num_sms);
 int attn_splits(int B, int KVr, int num_sms);
@@ -1342,6 +1343,50 @@ int sirius_debug_ffn(sirius_ctx* c, int layer, const float* x, int dense, float*
   OK(launch_decode_ffn(c, c->ranks[0], layer, x, nullptr, nullptr, out, dense != 0, n_active, 1, gate_out, c->Fr));
   CU(cudaStreamSynchronize(c->stream));
   return SIRIUS_OK;
+}
+
+// ---------------------------------------------------------------- test-only entry: the decode GEMV
+// out[b, r] = sum_k W[r, k] h[b, k] through the decode GEMV kernel (the launch run_gemv makes); h = x (fp32 [B, K]), or with norm_w h = RMSNorm(x + delta) * norm_w
+// (res_out = x + delta), or with embed h = RMSNorm(embed[tokens]) * norm_w (eps 1e-5); argmax (optional,
+// DEV int32 [B]) = lowest-index argmax.
+// Synchronous.  Returns cudaError_t.
+int sirius_debug_gemv(const void* W, int rows, int K, const float* x, int B, float* out, int32_t* argmax,
+                      const float* delta, const void* norm_w, float* res_out, const int32_t* tokens,
+                      const void* embed, int vocab) {
+  static unsigned long long* amax = nullptr;
+  static unsigned* cnt = nullptr;
+  if (!amax) {
+    if (cudaMalloc(&amax, 64 * sizeof(unsigned long long)) || cudaMalloc(&cnt, 16 * sizeof(unsigned))) return -1;
+    cudaMemset(amax, 0, 64 * sizeof(unsigned long long));
+    cudaMemset(cnt, 0, 16 * sizeof(unsigned));
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  GemvArgs a = {};
+  a.pro.mode = embed ? IN_EMBED : (norm_w ? IN_RESID : IN_F32);
+  a.pro.in_f32 = x;
+  a.pro.base = x;
+  a.pro.delta = delta;
+  a.pro.norm_w = static_cast<const uint16_t*>(norm_w);
+  a.pro.eps = 1e-5f;
+  a.pro.res_out = res_out;
+  a.pro.tokens = tokens;
+  a.pro.embed = static_cast<const uint16_t*>(embed);
+  a.pro.vocab = vocab;
+  a.W = static_cast<const uint16_t*>(W);
+  a.rows = rows;
+  a.K = K;
+  a.epi = argmax ? EPI_ARGMAX : EPI_STORE;
+  a.out = out;
+  a.ldo = rows;
+  a.amax = amax;
+  a.finalize = 1;
+  a.done_counter = cnt;
+  a.token_out = argmax;
+  cudaError_t e = launch::gemv(a, B, launch::gemv_grid(rows, sms), 0);
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaDeviceSynchronize();
 }
 
 // ---------------------------------------------------------------- test-only entry: the tcgen05 GEMM

@@ -102,6 +102,8 @@ def load():
         lib.sirius_debug_profile_read.argtypes = [P, P, P]
         lib.sirius_debug_profile_read.restype = I
         lib.sirius_debug_gemm.restype = I
+        lib.sirius_debug_gemv.argtypes = [P, I, I, P, I, P, P, P, P, P, P, P, I]
+        lib.sirius_debug_gemv.restype = I
         lib.sirius_nccl_available.restype = I
         lib.sirius_nccl_unique_id.argtypes = [P]
         lib.sirius_nccl_unique_id.restype = I
@@ -235,3 +237,17 @@ def debug_gemm(X, W, out, M: int, W2=None) -> None:
     r = lib.sirius_debug_gemm(X.data_ptr(), nterms, rows, W.data_ptr(), _ptr(W2), out.data_ptr(), M, N, K)
     if r != 0:
         raise RuntimeError(f"sirius_debug_gemm failed: {r}")
+
+
+def debug_gemv(W, x, out, argmax=None, delta=None, norm_w=None, res_out=None, tokens=None, embed=None) -> None:
+    """Test-only: out [B, rows] fp32 = h @ W.T (W bf16 [rows, K]) through the decode GEMV kernel;
+    h = x (fp32 [B, K]); with norm_w (bf16 [K])
+    h = RMSNorm(x + delta) * norm_w, res_out = x + delta; with embed (bf16 [V, K]) and tokens (int32 [B])
+    h = RMSNorm(embed[tokens]) * norm_w (eps 1e-5); argmax: int32 [B] or None."""
+    lib = load()
+    rows, K = W.shape
+    B = tokens.shape[0] if embed is not None else x.shape[0]
+    r = lib.sirius_debug_gemv(W.data_ptr(), rows, K, _ptr(x), B, out.data_ptr(), _ptr(argmax), _ptr(delta), _ptr(norm_w), _ptr(res_out), _ptr(tokens), _ptr(embed),
+                              embed.shape[0] if embed is not None else 0)
+    if r != 0:
+        raise RuntimeError(f"sirius_debug_gemv failed: {r}")

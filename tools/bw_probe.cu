@@ -89,8 +89,8 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     printf("%-48s %8.1f GB/s  (%s)\n", name, 5.0 * total / (ms / 1e3) / 1e9, cudaGetErrorString(cudaGetLastError()));
   };
-  for (int rb : {4096, 8192, 16384, 32768}) {
-    for (int ns : {8, 16, 24}) {
+  for (int rb : {8192, 16384, 32768, 65536}) {
+    for (int ns : {2, 3, 4, 6, 8, 12}) {
       size_t smem = (size_t)ns * rb + 2 * ns * 8;
       if (smem > 227 * 1024) continue;
       cudaFuncSetAttribute(ring_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -100,6 +100,10 @@ int main() {
       timeit([&] { ring_kernel<0><<<sms, 288, smem>>>(W, total, rb, ns, sink); }, nm);
       snprintf(nm, 96, "bulk ring row=%d nslot=%d read", rb, ns);
       timeit([&] { ring_kernel<1><<<sms, 288, smem>>>(W, total, rb, ns, sink); }, nm);
+      if (2 * smem <= 227 * 1024) {  // two CTAs per SM, each with its own ring
+        snprintf(nm, 96, "bulk ring row=%d nslot=%d read, 2 CTAs/SM", rb, ns);
+        timeit([&] { ring_kernel<1><<<2 * sms, 288, smem>>>(W, total, rb, ns, sink); }, nm);
+      }
     }
   }
   for (int bpsm : {2, 4, 8}) {
