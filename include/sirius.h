@@ -54,9 +54,11 @@ typedef enum {
   SIRIUS_ERR_STATE = -3,       /* call-order violation (kv_rewrite without a preceding
                                   correct_kernel; decode before prefill)                             */
   SIRIUS_ERR_CUDA = -4,        /* sticky                                                             */
-  SIRIUS_ERR_NCCL = -5,        /* sticky                                                             */
-  SIRIUS_ERR_UNSUPPORTED = -6  /* shape not compiled: head_dim not in {64,128}, d_model % 256,
-                                  ffn_dim % (32*tp) , etc.                                           */
+  SIRIUS_ERR_NCCL = -5,        /* sticky; includes asynchronous communicator errors, which every
+                                  entry point polls (ncclCommGetAsyncError) before enqueuing          */
+  SIRIUS_ERR_UNSUPPORTED = -6  /* shape not compiled: head_dim not in {64,128}; d_model % 256;
+                                  (n_heads/tp * head_dim) % 64; (ffn_dim/tp) % 8; max_gamma > 64;
+                                  batch * max_gamma > 256; batch not in {1, 2, 4, 8, 16}            */
 } sirius_status;
 
 /* Model shape + runtime capacities.  Llama-3 conventions: rotate-half RoPE with base rope_theta,
@@ -65,10 +67,12 @@ typedef struct {
   int32_t vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn_dim;
   float rope_theta, rms_eps;
   int32_t batch;     /* number of sequences (slots 0..batch-1), fixed for the context's life;
-                        one of 1, 2, 4, 8 (else SIRIUS_ERR_UNSUPPORTED); batch * max_gamma <= 256     */
+                        one of 1, 2, 4, 8, 16 (else SIRIUS_ERR_UNSUPPORTED); batch * max_gamma <= 256;
+                        batch >= 8 decodes through the tensor-core row path        */
   int32_t max_seq;   /* KV capacity per sequence (>= prompt + generated + max_gamma)              */
   int32_t max_gamma; /* max verify rows per sequence per correct_kernel call (<= 64)              */
-  int32_t tp_size, tp_rank; /* n_heads, n_kv_heads, ffn_dim, vocab divisible by tp_size          */
+  int32_t tp_size, tp_rank; /* n_heads, n_kv_heads, ffn_dim, vocab divisible by tp_size (else
+                               UNSUPPORTED)                                                      */
 } sirius_config;
 
 /* DEVICE pointers to this rank's weight shard: bf16, row-major, a "row" is an output feature or
@@ -107,6 +111,10 @@ enum {
  *  cats_threshold HOST [n_layers] fp32, copied; per-layer CATS threshold t_l >= 0.
  *                 A neuron i of layer l is active iff |SiLU(g_i)| >= t_l (readings D1, D2, D4).
  *  nccl_comm      ncclComm_t (borrowed) when tp_size > 1 with one process per GPU, else NULL.
+ *                 (Test/bench only: with the environment variable SIRIUS_DEBUG_STUB_COMM=1 and
+ *                 tp_size > 1, a non-NULL comm is never used — every collective is skipped, so one
+ *                 GPU runs exactly one rank's share of the work: a compute-only timing proxy of a
+ *                 TP rank whose outputs are rank-local partials.)
  *  stream         cudaStream_t (borrowed); every call enqueues on it.
  *  out            receives the context.
  * Errors: INVALID_ARG (NULL / non-positive / inconsistent shape), UNSUPPORTED, CUDA (allocation). */

@@ -62,21 +62,6 @@ struct FfnArgs {
   unsigned long long* trace;  // debug: [8][1024] %globaltimer stamps per CTA (phase boundaries), or NULL
 };
 
-// ---- decode attention (RoPE + KV append + split-K flash decode + last-CTA combine)
-struct AttnArgs {
-  const float* qkv;        // [B, (Hr + 2 KVr) * hd] raw projections (pre-RoPE), fp32
-  const int32_t* pos;      // [B]
-  const float* rope_cos;   // [max_seq, hd/2]
-  const float* rope_sin;
-  uint16_t* k_cache;       // this layer: [B, KVr, max_seq, hd]
-  uint16_t* v_cache;
-  int Hr, KVr, max_seq, splits;
-  float* part;             // workspace [B, KVr, splits, G, hd + 2]
-  unsigned* counters;      // unused
-  unsigned* group_bar;     // [B, KVr][2] barrier (count, generation) of the split groups
-  float* out;              // [B, Hr * hd] fp32
-  int* err;                // sticky device error word
-};
 
 // ---- persistent decode step (decode_step.cu): the whole TP-1 decode step in one cooperative launch
 struct StepArgs {

@@ -16,7 +16,7 @@
 //   P5  deterministic column reduction of the partials                -> x = x1 + sum_c partial_c
 // then final RMSNorm + LM head + packed (value, lowest index) argmax -> token_out.
 // Arithmetic per element is the same as the one-kernel-per-stage path (gemv_ffn.cu,
-// attn_decode.cu), which the TP > 1 path still uses (its all-reduces sit between the stages).
+// attn_stage_kernel below), which the TP > 1 path uses (its all-reduces sit between the stages).
 // Numeric contract (D15): bf16 weights and KV cache, fp32 activations and accumulation.
 #include "common.cuh"
 #include "decode_kernels.cuh"

@@ -7,16 +7,18 @@
 //                  bank-conflict free; warp-shuffle reduction.  Prologue fuses residual add + RMSNorm
 //                  (or the embedding gather).  Epilogues: store, or packed (value, lowest index) argmax.
 //  * ffn_kernel  : the CATS-sparse MLP of one layer in one
-//                  cooperative launch, one CTA (16 warps) per SM, neurons split evenly over the CTAs:
+//                  launch, neurons split evenly over the CTAs:
 //                    A  dense gate rows -> g -> a = SiLU(g)                        (warp per row)
 //                    B  CATS threshold |a| >= t_l, warp-ballot compaction per 32-neuron chunk
 //                    C  ACTIVE W_up rows only -> u -> m = a * u                    (warp per row)
 //                    D  ACTIVE W_down rows only -> y += m * W_down[n]   (threads own output columns)
-//                  so HBM bytes scale with the density; grid barrier; deterministic column reduction
-//                  of the per-CTA partial outputs.
-// Design note: an earlier version staged rows through a 1-D bulk-copy (TMA) mbarrier
-// ring; the per-row handoff capped it at ~3.3 TB/s for 8 KB rows (tools/bw_probe.cu), direct
-// 128-bit loads with many rows in flight reach ~7.3 TB/s.
+//                  so HBM bytes scale with the density.  Default (atomic mode): 8-warp CTAs, 2 per SM,
+//                  partials added into the pre-zeroed output with float4 atomics.  SIRIUS_FFN_ATOMIC=0:
+//                  16-warp CTAs, one per SM, cooperative launch, grid barrier and a deterministic
+//                  fixed-order column reduction of the per-CTA partials.
+// Design note: 1-D bulk-copy (TMA) staging of 8 KB rows caps at ~3.3 TB/s with a reader
+// (TMA ops have a fixed per-op cost; tools/bw_probe.cu, profiles/r02_bw_probe*.txt), direct 128-bit
+// loads with many rows in flight reach ~7.3 TB/s.
 // Numeric contract (D15): bf16 weights, fp32 activations and accumulation.
 #include "common.cuh"
 #include "decode_kernels.cuh"
@@ -107,6 +109,16 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
       const unsigned long long k = atomicExch(a.amax + tid, 0ull);  // read + reset for the next step
       a.token_out[tid] = (int32_t)argmax_key_index(k);
     }
+  }
+}
+
+// TP > 1: the per-rank packed keys were max-reduced across ranks (NCCL) -> token, amax reset
+__global__ void argmax_finalize_kernel(unsigned long long* amax, int B, int32_t* token_out) {
+  const int b = threadIdx.x;
+  if (b < B) {
+    const unsigned long long k = amax[b];
+    amax[b] = 0ull;
+    token_out[b] = (int32_t)argmax_key_index(k);
   }
 }
 
@@ -345,6 +357,11 @@ static cudaError_t gemv_b(const GemvArgs& a, int grid, cudaStream_t st) {
   if (cpl <= 16) return gemv_bc<B, 16>(a, grid, st);
   if (cpl <= 32) return gemv_bc<B, 32>(a, grid, st);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st) {
+  argmax_finalize_kernel<<<1, 32, 0, st>>>(amax, B, token_out);
+  return cudaGetLastError();
 }
 
 int gemv_grid(int rows, int num_sms) {

@@ -24,9 +24,7 @@ cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st);
 
 cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st);
 int ffn_grid(int F, int num_sms);
-int attn_splits(int B, int KVr, int num_sms);
 cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st);
-cudaError_t attn_decode(const AttnArgs& a, int B, int hd, int group, cudaStream_t st);
 bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms);
 int decode_step_splits(int B, int KV, int num_sms);
 cudaError_t decode_step(const StepArgs& a, int B, int grid, cudaStream_t st);
@@ -53,6 +51,7 @@ struct NcclApi {
   ncclResult_t_ (*getUniqueId)(void*) = nullptr;
   ncclResult_t_ (*commInitRank)(void**, int, NcclUid, int) = nullptr;
   ncclResult_t_ (*commDestroy)(void*) = nullptr;
+  ncclResult_t_ (*commGetAsyncError)(void*, ncclResult_t_*) = nullptr;
 };
 // nccl.h enum values (stable ABI): ncclUint8 = 1... ncclUint64 = 5, ncclFloat32 = 7; ncclSum = 0, ncclMax = 2
 constexpr int kNcclUint8 = 1, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclSum = 0, kNcclMax = 2;
@@ -68,6 +67,7 @@ NcclApi& nccl() {
       api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
       api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
       api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
       api.loaded = api.allReduce && api.allGather && api.getUniqueId && api.commInitRank;
     }
   }
@@ -104,18 +104,18 @@ struct sirius_ctx {
   sirius_config cfg;
   int nranks = 1;  // ranks run by this context (tp_size when emulating, else 1)
   bool emulated = false;
+  bool stub_comm = false;  // SIRIUS_DEBUG_STUB_COMM: tp_size > 1 on one GPU with every collective skipped
+                           // (one rank's compute, timing proxy only: results are rank-local partials)
   void* comm = nullptr;
   cudaStream_t stream = nullptr;
   int Hr = 0, KVr = 0, Fr = 0, Vr = 0, Nqkv = 0, G = 0, MAXM = 0;
   int num_sms = 148;
   size_t smem_optin = 0;
   size_t gemm_smem = 0;
-  int attn_splits = 1;
   bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   int ffn_split = 2;       // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)
   bool decode_rows = false;  // batched decode through the tensor-core row path (batch >= 8; SIRIUS_DECODE_ROWS)
   int32_t* dec_nacc = nullptr;
-  bool attn_stage = false;  // decode attention as the 512-thread item kernel (SIRIUS_ATTN_STAGE=0: old kernel)
   int attn_stage_splits = 1;
   int accept_splits = 8;
   std::vector<RankState> ranks;
@@ -249,6 +249,17 @@ sirius_status alloc(sirius_ctx* c, T** p, size_t count, bool zero = true) {
 
 sirius_status check_sticky(sirius_ctx* c) {
   if (c->sticky != SIRIUS_OK) return c->sticky;
+  // asynchronous NCCL failures (a peer died, a network/NVLink error) surface through the communicator,
+  // not through the enqueueing call: poll it on every entry and make the failure sticky
+  if (c->comm && !c->emulated && !c->stub_comm && nccl().commGetAsyncError) {
+    ncclResult_t_ ar = 0;
+    const ncclResult_t_ q = nccl().commGetAsyncError(c->comm, &ar);
+    if (q != 0 || (ar != 0 && ar != 7 /* ncclInProgress */)) {
+      const int code = q != 0 ? q : ar;
+      return fail(c, SIRIUS_ERR_NCCL, std::string("NCCL asynchronous error: ") +
+                                          (nccl().getErrorString ? nccl().getErrorString(code) : std::to_string(code)));
+    }
+  }
   if (*c->err_host != 0) {
     int e = *c->err_host;
     return fail(c, SIRIUS_ERR_CAPACITY,
@@ -340,7 +351,7 @@ sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev,
   const size_t n = rows * c->cfg.d_model;
   if (c->nranks > 1) {
     LCU(launch::sum_ranks(ptrs_dev, c->nranks, rows, c->cfg.d_model, c->cfg.d_model, c->stream));
-  } else if (c->cfg.tp_size > 1) {
+  } else if (c->cfg.tp_size > 1 && !c->stub_comm) {
     NcclApi& api = nccl();
     float* p = c->ranks[0].*buf;
     int r = api.allReduce(p, p, n, kNcclFloat32, kNcclSum, c->comm, c->stream);
@@ -477,7 +488,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       OK(run_gemm(c, R, R.w_qkv[l], nullptr, R.xn3, c->Nqkv, d, M, R.qkv, c->Nqkv, gtr));
       const size_t kv_layer = (size_t)cf.batch * c->KVr * cf.max_seq * hd;
       const size_t st_layer = (size_t)cf.batch * c->KVr * cf.max_gamma * hd;
-      if (mode == ROWS_DECODE && c->attn_stage) {
+      if (mode == ROWS_DECODE) {
         // one query row per sequence (batched decode): the decode-attention item kernel does RoPE,
         // the K/V append at pos and split-K attention, writing the O-proj operand as a hi/lo pair
         StepArgs sa = {};
@@ -618,6 +629,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   c->stream = (cudaStream_t)stream;
   c->comm = nccl_comm;
   c->emulated = emulate;
+  if (const char* e = getenv("SIRIUS_DEBUG_STUB_COMM")) c->stub_comm = !emulate && cf.tp_size > 1 && atoi(e) != 0;
   c->nranks = emulate ? cf.tp_size : 1;
   c->Hr = cf.n_heads / cf.tp_size;
   c->KVr = cf.n_kv_heads / cf.tp_size;
@@ -641,9 +653,11 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     delete c;
     return s;
   }
-  c->attn_splits = launch::attn_splits(cf.batch, c->KVr, c->num_sms);  // ~one wave of split CTAs
-  c->attn_stage = launch::attn_stage_supported(cf.head_dim, c->G);
-  if (const char* e = getenv("SIRIUS_ATTN_STAGE")) c->attn_stage = c->attn_stage && atoi(e) != 0;
+  if (!launch::attn_stage_supported(cf.head_dim, c->G)) {  // decode attention instantiations (decode_step.cu)
+    sirius_status s = fail(c, SIRIUS_ERR_UNSUPPORTED, "decode attention: (head_dim, GQA group) not compiled");
+    delete c;
+    return s;
+  }
   if (const char* e = getenv("SIRIUS_FFN_ATOMIC")) c->ffn_atomic = atoi(e) != 0;
   c->decode_rows = cf.batch >= 8;
   if (const char* e = getenv("SIRIUS_DECODE_ROWS")) c->decode_rows = atoi(e) != 0;
@@ -828,7 +842,7 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
           OK(run_gemv(c, a, 1));
         }
         if (cf.tp_size > 1) {
-          if (!c->emulated) {
+          if (!c->emulated && !c->stub_comm) {
             NcclApi& api = nccl();
             int r = api.allReduce(c->amax, c->amax, 1, kNcclUint64, kNcclMax, c->comm, c->stream);
             if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllReduce(max)");
@@ -961,25 +975,9 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       prof_begin(c, P_QKV);
       OK(run_gemv(c, a, B));
       prof_end(c);
-      AttnArgs at = {};
       const size_t kv_layer = (size_t)B * c->KVr * cf.max_seq * hd;
-      at.qkv = R.qkv;
-      at.pos = pos;
-      at.rope_cos = c->rope_cos;
-      at.rope_sin = c->rope_sin;
-      at.k_cache = R.k_cache + l * kv_layer;
-      at.v_cache = R.v_cache + l * kv_layer;
-      at.Hr = c->Hr;
-      at.KVr = c->KVr;
-      at.max_seq = cf.max_seq;
-      at.splits = c->attn_splits;
-      at.part = R.attn_part;
-      at.counters = R.attn_cnt;
-      at.group_bar = R.attn_bar;
-      at.out = R.ob;
-      at.err = c->err_dev;
       prof_begin(c, P_ATTN);
-      if (c->attn_stage) {  // 512-thread item kernel with the last-split combine (decode_step.cu)
+      {  // one (sequence, kv head, split) item per 512-thread CTA, last-split combine (decode_step.cu)
         StepArgs sa = {};
         sa.d = d;
         sa.Hr = c->Hr;
@@ -1000,8 +998,6 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
         sa.group_bar = R.attn_bar;
         sa.err = c->err_dev;
         LCU(launch::attn_stage(sa, l, B, c->stream));
-      } else {
-        LCU(launch::attn_decode(at, B, hd, c->G, c->stream));
       }
       prof_end(c);
       GemvArgs o = {};
@@ -1060,7 +1056,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     prof_end(c);
   }
   if (cf.tp_size > 1) {
-    if (!c->emulated) {
+    if (!c->emulated && !c->stub_comm) {
       NcclApi& api = nccl();
       int r = api.allReduce(c->amax, c->amax, B, kNcclUint64, kNcclMax, c->comm, c->stream);
       if (r != 0) return fail(c, SIRIUS_ERR_NCCL, "ncclAllReduce(max)");
@@ -1136,7 +1132,7 @@ static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* kernel_to
   }
   const RowStat* stats = c->stats;
   int nranks = c->nranks;
-  if (cf.tp_size > 1 && !c->emulated) {
+  if (cf.tp_size > 1 && !c->emulated && !c->stub_comm) {
     NcclApi& api = nccl();
     int r = api.allGather(c->stats, c->stats_gather, (size_t)M * c->accept_splits * sizeof(RowStat), kNcclUint8,
                           c->comm, c->stream);

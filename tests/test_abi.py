@@ -56,3 +56,12 @@ def test_sass_is_sm100a_with_tcgen05_and_bulk_copies():
         "arch = sm_100a" in sass
     for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UTCATOMSWS"):
         assert mnem in sass, mnem
+
+
+def test_library_resolves_all_its_own_symbols():
+    """Every sirius:: symbol the library references is defined in it (a kernel launcher moved or
+    deleted without its callers shows up here, not at first load on the GPU box)."""
+    if not os.path.exists(LIB):
+        pytest.skip("library not built")
+    und = subprocess.run(["nm", "-D", "--undefined-only", LIB], capture_output=True, text=True).stdout
+    assert "sirius" not in und, [l for l in und.splitlines() if "sirius" in l]

@@ -5,7 +5,14 @@ tokens, PAPER.md:30 / :216), measured CATS density, effective density (Eq. 3, PA
 ((n_period - 1) I + 1) / n_AAL with I = the measured global density of the sparse model).
 
     python tools/sweep.py [--rho 0.3,0.4,0.5,0.6,0.7] [--gamma 4,8,16,32] [--r 0.01,0.03,0.1,0.2,0.3]
-                          [--kernels 6] [--out profiles/sweep_r01.csv]
+                          [--kernels 32] [--out profiles/sweep_r02.csv]
+
+Every cell starts a fresh session (dense prefill of the same prompt), runs one untimed kernel (graph
+capture) and K timed kernels; AAL is reported with its standard error over the K kernels.  The
+speculative-decoding baseline of the same gamma (greedy-match acceptance, EXACT_ARGMAX: a draft is
+kept iff it equals the full model's argmax) is the row with r = "sd".  The
+0-based draft index of every rejection is written to <out>.rejections.csv.
+SM clocks are sampled with nvidia-smi during the sweep.
 """
 import argparse
 import csv
@@ -32,14 +39,15 @@ def main():
     ap.add_argument("--rho", default="0.3,0.4,0.5,0.6,0.7")
     ap.add_argument("--gamma", default="4,8,16,32")
     ap.add_argument("--r", default="0.01,0.03,0.1,0.2,0.3")
-    ap.add_argument("--kernels", type=int, default=6)
+    ap.add_argument("--kernels", type=int, default=32)
     ap.add_argument("--prompt", type=int, default=900)
-    ap.add_argument("--out", default="profiles/sweep_r01.csv")
+    ap.add_argument("--out", default="profiles/sweep_r02.csv")
+    ap.add_argument("--no-sd", action="store_true")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.model]
     w = sg.device_weights(cfg)
     prompt = synth.eval_prompt(cfg, 0, a.prompt)
-    gammas, rs = lst(a.gamma, int), lst(a.r, float)
+    gammas, rs = lst(a.gamma, int), lst(a.r, float) + ([] if a.no_sd else ["sd"])
     gmax = max(gammas)
     rows = []
     stream = torch.cuda.current_stream()
@@ -47,9 +55,13 @@ def main():
     counts = {"ffn": 3 * cfg.n_layers * cfg.ffn_dim * cfg.d_model}
     total = (cfg.n_layers * (cfg.qkv_rows * cfg.d_model + cfg.d_model * cfg.n_heads * cfg.head_dim)
              + counts["ffn"] + cfg.vocab * cfg.d_model)
+    import bench
+    clocks = bench.Clocks(0)
+    clocks.start()
+    rej_rows = []
     for rho in lst(a.rho, float):
         thr = synth.layer_thresholds(cfg, rho)
-        max_seq = a.prompt + (len(rs) * (a.kernels + 2) + 4) * gmax + 64
+        max_seq = a.prompt + (a.kernels + 3) * gmax + 64
         ctx = S.Sirius(cfg, w, thr, batch=1, max_seq=max_seq, max_gamma=gmax)
         drv = driver.Driver(ctx)
         drv.begin([prompt])
@@ -65,33 +77,47 @@ def main():
         # global density I of the sparse model (gate dense, up/down scaled by rho_meas)
         sparse_params = total - counts["ffn"] + cfg.n_layers * cfg.ffn_dim * cfg.d_model * (1 + 2 * rho_meas)
         I = sparse_params / total
-        drv.begin([prompt])  # fresh session (cache rewritten from the prompt)
         for g in gammas:
             for r in rs:
-                drv.step(g, r)  # warm-up / graph capture of this gamma
+                sd = r == "sd"
+                mode = S.ACCEPT_EXACT_ARGMAX if sd else S.ACCEPT_THRESHOLD
+                rv = 0.0 if sd else r
+                drv.flush()
+                drv.begin([prompt])  # fresh session per cell (cache rewritten from the prompt)
+                drv.step(g, rv, mode)  # warm-up / graph capture of this gamma
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
                 e0.record(stream)
-                committed = sum(drv.step(g, r) for _ in range(a.kernels))
+                committed = sum(drv.step(g, rv, mode) for _ in range(a.kernels))
                 e1.record(stream)
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1)
-                adv = [int(k.j[0]) + 1 for k in drv.log[-a.kernels:]]
+                adv = np.array([int(k.j[0]) + 1 for k in drv.log[-a.kernels:]], dtype=np.float64)
                 aal = committed / a.kernels
-                rejected = sum(1 for x in adv if x < g)
+                rejected = int(np.sum(adv < g))
+                for k in drv.log[-a.kernels:]:
+                    if int(k.j[0]) < g - 1:
+                        rej_rows.append(dict(rho_target=rho, gamma=g, r=r, rejected_at=int(k.j[0])))
                 row = dict(rho_target=rho, rho_measured=round(rho_meas, 4), gamma=g, r=r,
                            ms_per_token=round(ms / committed, 4), aal=round(aal, 3),
+                           aal_stderr=round(float(adv.std(ddof=1) / np.sqrt(len(adv))) if len(adv) > 1 else 0.0, 3),
                            correction_rate=round(rejected / committed, 4),
                            effective_density=round(((g - 1) * I + 1) / aal, 4), global_density_I=round(I, 4),
                            kernels=a.kernels)
                 rows.append(row)
                 print(row, flush=True)
-                if drv.T[0] + (a.kernels + 2) * gmax >= max_seq:
-                    drv.flush()
-                    drv.begin([prompt])
         drv.flush()
         del drv, ctx
         torch.cuda.empty_cache()
+    ck = clocks.stop()
+    print("clocks", ck)
+    for row in rows:
+        row["sm_mhz_median"] = ck["sm_mhz"]
+        row["clock_reasons"] = "|".join(ck["reasons"])
+    with open(a.out + ".rejections.csv", "w", newline="") as f:
+        wr = csv.DictWriter(f, fieldnames=["rho_target", "gamma", "r", "rejected_at"])
+        wr.writeheader()
+        wr.writerows(rej_rows)
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w", newline="") as f:
         wr = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
