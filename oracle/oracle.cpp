@@ -10,6 +10,8 @@
 //   * CATS / FSparse (§2.1; PAPER.md:121 footnote; §3.2):
 //     the gate is dense, a = SiLU(x·W_gate) is thresholded per layer, |a| >= t_l, and only
 //     the active columns of W_up / rows of W_down are used ("Up and Down linear layers only"),
+//   * CSparse / Griffin (§2.1): a per-prompt neuron set fixed for the whole
+//     generation, the MLP restricted to it (plan argument of oracle_forward_row / oracle_mlp),
 //   * the shared KV cache of Algorithm 1 (PAPER.md:242 Require; "Enables Full to
 //     directly rewrites KV Cache"; §4.2): a row is written at its position either
 //     into the cache (sparse/dense decode, prefill) or into a staging area (full-model verify of a
@@ -181,8 +183,12 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row, bool k
 //   h2 = RMSNorm(x);  g = h2 . W_gate (dense, always);  a = SiLU(g) = g / (1 + e^-g)
 //   active_i  <=>  dense  or  |a_i| >= t_l
 //   u_i = h2 . W_up[i]  (active i only);  m_i = a_i * u_i;  x += sum_{active i, ascending} m_i W_down[i]
+// CSparse (§2.1: "within the same input prompt, the sparsity pattern is fixed for all
+// tokens generated"; Griffin): plan != NULL gives the prompt's fixed neuron set of this
+// layer (plan[i] = 1 iff neuron i is kept) and active_i <=> plan[i]; the MLP is then the dense MLP of
+// the kept neurons (gate, up and down restricted to them; a_i of the others is computed but unused).
 void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_out, uint8_t* mask_out,
-               int* n_active) {
+               int* n_active, const uint8_t* plan = nullptr) {
   const int d = o->d, F = o->ffn;
   std::vector<double> h2(d), g(F), a(F), m(F, 0.0);
   std::vector<uint8_t> mask(F);
@@ -191,7 +197,7 @@ void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_o
   int cnt = 0;
   for (int i = 0; i < F; ++i) {
     a[i] = g[i] / (1.0 + std::exp(-g[i]));
-    mask[i] = (!sparse || std::fabs(a[i]) >= t) ? 1 : 0;
+    mask[i] = plan ? plan[i] : ((!sparse || std::fabs(a[i]) >= t) ? 1 : 0);
     cnt += mask[i];
   }
   const uint16_t* Wu = o->wup[l];
@@ -263,21 +269,23 @@ void oracle_set_layer(void* h, int l, const uint16_t* attn_norm, const uint16_t*
   o->wgate[l] = wgate; o->wup[l] = wup; o->wdown[l] = wdown;
 }
 
-// Full row forward.  sparse: 0 = dense model M_F, 1 = CATS sparse model M_S (thresholds[L], fp32).
+// Full row forward.  sparse: 0 = dense model M_F, 1 = CATS sparse model M_S (thresholds[L], fp32),
+// 2 = CSparse model M_S with the fixed neuron plan[L*ffn] (1 = kept).
 // stage_row < 0: write K/V to cache slot pos; >= 0: write to staging row stage_row (verify).
 // logits: [vocab] fp64 or NULL.  gate_out: [L*ffn] a = SiLU(g) or NULL.  mask_out: [L*ffn] or NULL.
 // n_active: [L] or NULL.  x_out: [d] final residual (pre final-norm) or NULL.
 void oracle_forward_row(void* h, int tok, int pos, int sparse, const float* thresholds, int stage_row,
-                        double* logits, double* gate_out, uint8_t* mask_out, int* n_active, double* x_out) {
+                        double* logits, double* gate_out, uint8_t* mask_out, int* n_active, double* x_out,
+                        const uint8_t* plan) {
   Oracle* o = (Oracle*)h;
   const int d = o->d;
   std::vector<double> x(d), hf(d);
   for (int k = 0; k < d; ++k) x[k] = bf16_value(o->embed[(size_t)tok * d + k]);  // x = E[tok]
   for (int l = 0; l < o->L; ++l) {
     attention_block(o, l, x.data(), pos, stage_row);
-    mlp_block(o, l, x.data(), sparse, sparse ? (double)thresholds[l] : 0.0,
+    mlp_block(o, l, x.data(), sparse, sparse == 1 ? (double)thresholds[l] : 0.0,
               gate_out ? gate_out + (size_t)l * o->ffn : nullptr, mask_out ? mask_out + (size_t)l * o->ffn : nullptr,
-              n_active ? n_active + l : nullptr);
+              n_active ? n_active + l : nullptr, sparse == 2 ? plan + (size_t)l * o->ffn : nullptr);
   }
   if (x_out) std::memcpy(x_out, x.data(), sizeof(double) * d);
   if (logits) {
@@ -302,10 +310,11 @@ void oracle_prefill_kv_row(void* h, int tok, int pos) {
   attention_block(o, o->L - 1, x.data(), pos, -1, true);
 }
 
-// Layer-isolated MLP (kernel-level parity at full shapes): x[d] in/out.
+// Layer-isolated MLP (kernel-level parity at full shapes): x[d] in/out.  sparse 2: plan[ffn] (CSparse).
 void oracle_mlp(void* h, int l, double* x, int sparse, float threshold, double* gate_out, uint8_t* mask_out,
-                int* n_active) {
-  mlp_block((Oracle*)h, l, x, sparse, sparse ? (double)threshold : 0.0, gate_out, mask_out, n_active);
+                int* n_active, const uint8_t* plan) {
+  mlp_block((Oracle*)h, l, x, sparse, sparse == 1 ? (double)threshold : 0.0, gate_out, mask_out, n_active,
+            sparse == 2 ? plan : nullptr);
 }
 
 // KV rewrite (Algorithm 1, §4.2): staging rows [0, n) -> cache slots [T, T+n).

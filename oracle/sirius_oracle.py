@@ -53,9 +53,10 @@ def _lib():
         lib.oracle_destroy.argtypes = [P]
         lib.oracle_set_global.argtypes = [P, P, P, P]
         lib.oracle_set_layer.argtypes = [P, ctypes.c_int] + [P] * 7
-        lib.oracle_forward_row.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P, P, P]
+        lib.oracle_forward_row.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P, P, P,
+                                           P]
         lib.oracle_prefill_kv_row.argtypes = [P, ctypes.c_int, ctypes.c_int]
-        lib.oracle_mlp.argtypes = [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_float, P, P, P]
+        lib.oracle_mlp.argtypes = [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_float, P, P, P, P]
         lib.oracle_kv_rewrite.argtypes = [P, ctypes.c_int, ctypes.c_int]
         lib.oracle_read_cache.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
         lib.oracle_round_bf16.argtypes = [ctypes.c_double]
@@ -111,7 +112,10 @@ class OracleModel:
 
     # ------------------------------------------------------------ one row
     def forward_row(self, tok: int, pos: int, sparse: bool = False, thresholds: Optional[np.ndarray] = None,
-                    stage_row: int = -1, want_gate: bool = False, want_mask: bool = False) -> RowOut:
+                    stage_row: int = -1, want_gate: bool = False, want_mask: bool = False,
+                    plan: Optional[np.ndarray] = None) -> RowOut:
+        """sparse with plan (uint8 [L, ffn], csparse_plan): the CSparse model; sparse with thresholds:
+        the CATS (FSparse) model; else the dense model."""
         cfg = self.cfg
         assert 0 <= tok < cfg.vocab and 0 <= pos < self.max_seq
         assert stage_row < self.max_gamma
@@ -119,23 +123,31 @@ class OracleModel:
         gate = np.empty((cfg.n_layers, cfg.ffn_dim), dtype=np.float64) if want_gate else None
         mask = np.empty((cfg.n_layers, cfg.ffn_dim), dtype=np.uint8) if want_mask else None
         nact = np.empty(cfg.n_layers, dtype=np.int32)
-        thr = None
-        if sparse:
+        thr = pl = None
+        mode = 0
+        if sparse and plan is not None:
+            pl = np.ascontiguousarray(plan, dtype=np.uint8)
+            assert pl.shape == (cfg.n_layers, cfg.ffn_dim)
+            mode = 2
+        elif sparse:
             thr = np.ascontiguousarray(thresholds, dtype=np.float32)
             assert thr.shape == (cfg.n_layers,)
-        _lib().oracle_forward_row(self.h, int(tok), int(pos), 1 if sparse else 0, _ptr(thr), int(stage_row),
-                                  _ptr(logits), _ptr(gate), _ptr(mask), _ptr(nact), None)
+            mode = 1
+        _lib().oracle_forward_row(self.h, int(tok), int(pos), mode, _ptr(thr), int(stage_row),
+                                  _ptr(logits), _ptr(gate), _ptr(mask), _ptr(nact), None, _ptr(pl))
         return RowOut(logits, gate, mask, nact)
 
-    def mlp(self, layer: int, x: np.ndarray, sparse: bool, threshold: float = 0.0):
-        """Layer-isolated MLP on residual x (fp64 [d]); returns (x_out, a, mask, n_active)."""
+    def mlp(self, layer: int, x: np.ndarray, sparse: bool, threshold: float = 0.0, plan: Optional[np.ndarray] = None):
+        """Layer-isolated MLP on residual x (fp64 [d]); returns (x_out, a, mask, n_active).  With plan
+        (uint8 [ffn]) the CSparse MLP of that neuron set."""
         cfg = self.cfg
         xx = np.ascontiguousarray(x, dtype=np.float64).copy()
         gate = np.empty(cfg.ffn_dim, dtype=np.float64)
         mask = np.empty(cfg.ffn_dim, dtype=np.uint8)
         n = np.empty(1, dtype=np.int32)
-        _lib().oracle_mlp(self.h, layer, _ptr(xx), 1 if sparse else 0, float(threshold), _ptr(gate), _ptr(mask),
-                          _ptr(n))
+        pl = None if plan is None else np.ascontiguousarray(plan, dtype=np.uint8)
+        mode = 2 if (sparse and pl is not None) else (1 if sparse else 0)
+        _lib().oracle_mlp(self.h, layer, _ptr(xx), mode, float(threshold), _ptr(gate), _ptr(mask), _ptr(n), _ptr(pl))
         return xx, gate, mask, int(n[0])
 
     def kv_rewrite(self, T: int, n: int) -> None:
@@ -165,6 +177,19 @@ class OracleModel:
             lib.oracle_prefill_kv_row(self.h, int(t), i)
         return self.forward_row(tokens[-1], len(tokens) - 1).logits
 
+    def prefill_stats(self, tokens: Sequence[int]):
+        """Dense prefill that also returns the CSparse statistic of every layer's neurons over the
+        prompt (§2.1 "the sparsity pattern is fixed for all tokens generated", decided
+        after prefilling; reading D28): stats[l, i] = sum over prompt positions p of
+        |a_{p,i}|, a = SiLU(g) of the dense model.  Returns (logits [P, vocab], stats [L, ffn])."""
+        stats = np.zeros((self.cfg.n_layers, self.cfg.ffn_dim), dtype=np.float64)
+        logits = []
+        for i, t in enumerate(tokens):
+            row = self.forward_row(t, i, want_gate=True)
+            stats += np.abs(row.gate)
+            logits.append(row.logits)
+        return np.stack(logits), stats
+
     def decode(self, tok: int, pos: int, sparse: bool, thresholds=None, **kw) -> RowOut:
         """One decode step of M_S (sparse) or M_F (dense): writes K/V at cache slot pos."""
         return self.forward_row(tok, pos, sparse, thresholds, -1, **kw)
@@ -174,6 +199,24 @@ class OracleModel:
         PAPER.md:258; §4.2): rows [pending, d_1..d_{g-1}] at positions T..T+g-1,
         K/V into staging, each row attends to cache[0,T) + staging[0..i].  Returns logits [g, vocab]."""
         return np.stack([self.forward_row(t, T + i, False, None, i).logits for i, t in enumerate(kernel_tokens)])
+
+
+def csparse_keep_count(ffn: int, keep: float) -> int:
+    """Neurons kept per layer: round(keep * ffn), halves rounded up (reading D28)."""
+    return int(np.floor(keep * ffn + 0.5))
+
+
+def csparse_plan(stats: np.ndarray, keep: float) -> np.ndarray:
+    """CSparse neuron plan (reading D28): per layer the csparse_keep_count(ffn, keep) neurons with
+    the largest statistic, exact ties to the lower neuron index.  Returns uint8 [L, ffn] (1 = kept)."""
+    L, F = stats.shape
+    k = csparse_keep_count(F, keep)
+    plan = np.zeros((L, F), dtype=np.uint8)
+    idx = np.arange(F)
+    for l in range(L):
+        order = np.lexsort((idx, -stats[l]))  # primary: statistic descending; secondary: index ascending
+        plan[l, order[:k]] = 1
+    return plan
 
 
 def top2_margin(l: np.ndarray) -> float:
@@ -229,6 +272,7 @@ class GenerateResult:
     tokens: List[int]
     kernels: List[KernelRecord] = field(default_factory=list)
     all_tokens: List[int] = field(default_factory=list)  # untruncated (includes the last kernel's surplus)
+    plan: Optional[np.ndarray] = None  # CSparse neuron plan [L, ffn] when csparse_keep was given
 
     @property
     def advances(self) -> List[int]:
@@ -241,8 +285,8 @@ class GenerateResult:
 
 
 def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: int, r: float,
-             thresholds: np.ndarray, accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True,
-             interleave: bool = True, rollback: bool = True) -> GenerateResult:
+             thresholds: Optional[np.ndarray], accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True,
+             interleave: bool = True, rollback: bool = True, csparse_keep: Optional[float] = None) -> GenerateResult:
     """The Sirius loop, Algorithm 1, readings D5-D18:
       * dense prefill of the prompt; the first generated token is the dense argmax (D17);
       * kernel size n = gamma: the sparse model drafts gamma-1 tokens after the pending token,
@@ -260,20 +304,30 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
     draft d_{i+1} (q_i < r) by the full model's argmax of verify row i ("only letting the LLM correct
     the token it is evaluating"), then the full model's token of the last row; with `rewrite` the
     full model's K/V of the g verified rows overwrite the cache rows [T, T+g).  KernelRecord.j stays
-    the first rejection (the statistic), the advance is then g."""
+    the first rejection (the statistic), the advance is then g.
+
+    csparse_keep: the sparse model is CSparse (Griffin PAPER.md:471) instead of CATS: the
+    neuron plan of the prompt (prefill_stats + csparse_plan, reading D28) fixed for the generation."""
     assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
     P = len(prompt)
     assert P + n_tokens + gamma <= model.max_seq and gamma >= 1
     # dense prefill; only the last row's logits are needed (prefill_last: same cache, pinned bitwise
     # against prefill() in tests/test_oracle_pins.py)
-    out = [argmax_lowest(model.prefill_last(prompt))]  # out[-1] is the pending token at position T
+    plan = None
+    if csparse_keep is None:
+        out = [argmax_lowest(model.prefill_last(prompt))]  # out[-1] is the pending token at position T
+    else:
+        lg, stats = model.prefill_stats(prompt)
+        plan = csparse_plan(stats, csparse_keep)
+        out = [argmax_lowest(lg[-1])]
     T = P
     res = GenerateResult(out)
+    res.plan = plan
     while len(out) < n_tokens:
         ins = [out[-1]]
         nact, dmarg = [], []
         for i in range(gamma - 1):  # sparse drafting, greedy (D13)
-            row = model.decode(ins[i], T + i, True, thresholds)
+            row = model.decode(ins[i], T + i, True, thresholds, plan=plan)
             nact.append(row.n_active)
             dmarg.append(top2_margin(row.logits))
             ins.append(argmax_lowest(row.logits))

@@ -1,0 +1,114 @@
+"""Pins for the oracle's CSparse (Griffin-style coarse-grained sparsity) part — SURVEY.md §8(f) N2,
+PAPER.md:62 (§2.1: "within the same input prompt, the sparsity pattern is fixed for all tokens
+generated"), :182 (§3.2: the pattern is predetermined after prefilling, so the gate is sparsified
+too), :471 (Griffin, the paper's latency setting).  Reading D28: statistic = sum over the
+prompt of |SiLU(g)| per neuron, keep round(keep * ffn) (halves up) per layer, ties to the lower index.
+CPU only."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import sirius_oracle as so
+
+from test_oracle_pins import _f64, _hf_full_fp64, _hf_llama
+
+
+def test_csparse_stats_match_hf_llama_activations(tiny, monkeypatch):
+    """The statistic equals sum_p |act_fn(gate_proj(post_attention_layernorm(x_p)))| taken from
+    transformers.LlamaForCausalLM (fp64, hooks on the MLP activation) over the same prompt."""
+    torch = pytest.importorskip("torch")
+    cfg, w = tiny
+    m = _hf_llama(cfg, w)
+    _hf_full_fp64(monkeypatch, m, cfg)
+    prompt = synth.eval_prompt(cfg, 4, 40)
+    acts = {}
+
+    def hook(l):
+        def f(mod, inp, out):
+            acts[l] = out[0].abs().sum(0).numpy()  # [ffn]: sum over prompt positions
+        return f
+
+    hs = [m.model.layers[l].mlp.act_fn.register_forward_hook(hook(l)) for l in range(cfg.n_layers)]
+    with torch.no_grad():
+        m(torch.tensor(prompt[None].astype(np.int64)))
+    for h in hs:
+        h.remove()
+    _, stats = so.OracleModel(cfg, w, max_seq=64, round_kv=False).prefill_stats(prompt)
+    for l in range(cfg.n_layers):
+        np.testing.assert_allclose(stats[l], acts[l], rtol=1e-9, atol=1e-9)
+
+
+def test_csparse_plan_selection_brute_force():
+    """Top-k by the statistic, ties to the lower index, |set| = round(keep * ffn) (halves up), and the
+    set at a smaller keep is a subset of the set at a larger keep."""
+    rng = np.random.default_rng(11)
+    F = 37
+    s = rng.integers(0, 9, size=(3, F)).astype(np.float64)  # many exact ties
+    for keep in (0.1, 0.25, 0.5, 0.7, 1.0):
+        k = so.csparse_keep_count(F, keep)
+        assert k == int(keep * F + 0.5)
+        plan = so.csparse_plan(s, keep)
+        for l in range(3):
+            brute = sorted(range(F), key=lambda i: (-s[l, i], i))[:k]  # pure-Python definition
+            assert sorted(np.flatnonzero(plan[l]).tolist()) == sorted(brute)
+    for lo, hi in ((0.25, 0.5), (0.5, 0.7)):
+        assert np.all(so.csparse_plan(s, lo) <= so.csparse_plan(s, hi))
+    assert so.csparse_keep_count(688, 0.5) == 344 and so.csparse_keep_count(5, 0.5) == 3
+
+
+def test_csparse_mlp_equals_dense_mlp_with_unplanned_neurons_zeroed(tiny):
+    """Brute force: the CSparse MLP equals the dense MLP on weights whose W_gate, W_up and
+    W_down rows outside the plan are zeroed — exact (the gate is sparsified too)."""
+    cfg, w = tiny
+    rng = np.random.default_rng(12)
+    m = so.OracleModel(cfg, w, max_seq=8)
+    plan = np.zeros(cfg.ffn_dim, dtype=np.uint8)
+    plan[rng.permutation(cfg.ffn_dim)[:300]] = 1
+    x = rng.standard_normal(cfg.d_model) * 2.0
+    for l in range(cfg.n_layers):
+        xs, _, mask, n = m.mlp(l, x, True, plan=plan)
+        assert n == 300 and np.array_equal(mask, plan)
+        w2 = dict(w)
+        for name in ("w_gate", "w_up", "w_down"):
+            z = w[f"layers.{l}.{name}"].copy()
+            z[plan == 0] = 0
+            w2[f"layers.{l}.{name}"] = z
+        xd, _, _, _ = so.OracleModel(cfg, w2, max_seq=8).mlp(l, x, False)
+        np.testing.assert_array_equal(xs, xd)
+        # and the numpy form of the restricted MLP
+        mr = so.OracleModel(cfg, w, max_seq=8, round_kv=False)
+        h = x / np.sqrt(np.mean(x * x) + cfg.rms_eps) * _f64(w[f"layers.{l}.ffn_norm"])
+        sel = plan.astype(bool)
+        g = _f64(w[f"layers.{l}.w_gate"])[sel] @ h
+        u = _f64(w[f"layers.{l}.w_up"])[sel] @ h
+        ref = x + _f64(w[f"layers.{l}.w_down"])[sel].T @ (g / (1 + np.exp(-g)) * u)
+        np.testing.assert_allclose(mr.mlp(l, x, True, plan=plan)[0], ref, rtol=1e-11, atol=1e-11)
+
+
+def test_csparse_keep_one_equals_dense(tiny):
+    """keep = 1: the plan keeps every neuron and the CSparse model is the dense model — bitwise."""
+    cfg, w = tiny
+    prompt = synth.eval_prompt(cfg, 5, 20)
+    om = so.OracleModel(cfg, w, max_seq=64)
+    _, stats = om.prefill_stats(prompt)
+    plan = so.csparse_plan(stats, 1.0)
+    assert plan.all()
+    r1 = om.decode(9, 20, True, plan=plan)
+    om2 = so.OracleModel(cfg, w, max_seq=64)
+    om2.prefill(prompt)
+    r2 = om2.decode(9, 20, False)
+    np.testing.assert_array_equal(r1.logits, r2.logits)
+
+
+def test_csparse_sirius_generate_accounting(tiny):
+    """CSparse Sirius loop: the plan is the prompt's, fixed for the generation; r = 0 accepts every
+    draft; EXACT_ARGMAX reproduces dense greedy (the correction is lossless in that mode)."""
+    cfg, w = tiny
+    prompt = synth.eval_prompt(cfg, 6, 24)
+    res = so.generate(so.OracleModel(cfg, w, max_seq=128), prompt, 20, 4, 0.0, None, csparse_keep=0.5)
+    assert res.plan is not None and int(res.plan[0].sum()) == so.csparse_keep_count(cfg.ffn_dim, 0.5)
+    assert all(a == 4 for a in res.advances[:-1])
+    ex = so.generate(so.OracleModel(cfg, w, max_seq=128), prompt, 20, 4, 0.0, None,
+                     accept_mode=so.ACCEPT_EXACT_ARGMAX, csparse_keep=0.5)
+    dense = so.greedy_decode(so.OracleModel(cfg, w, max_seq=128), prompt, 20)
+    assert ex.tokens == dense
