@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1, 2, 4, 8)")
     ap.add_argument("--baseline-tokens", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--csparse-keep", type=float, default=0.5,
+                    help="CSparse (Griffin-style) keep fraction for the csparse rows (0: skip)")
     return ap.parse_args()
 
 
@@ -343,6 +345,44 @@ def main():
                "rejection_positions": [int(k.j[b]) for k in tl for b in range(B) if int(k.j[b]) < a.gamma - 1],
                "vs_dense": (t_alt / c_alt) / base["dense"]}
         drv.flush()
+    # ---------------- CSparse (Griffin-style, the sparse model of the paper's latency tables):
+    # the same context with the prompt's fixed neuron set; Sirius over the CSparse draft model, and
+    # CSparse-only greedy decode
+    csp = None
+    if a.csparse_keep > 0 and B == 1:
+        ctx.sirius_csparse_enable(a.csparse_keep)
+        dcs = driver.Driver(ctx, csparse=True)
+        dcs.begin(prompts)
+        for _ in range(a.warmup):
+            dcs.step(a.gamma, a.r)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            dcs.step(a.gamma, a.r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_cs_sir = max_over_ranks(e0.elapsed_time(e1))
+        adv_cs = [int(k.j[0]) + 1 for k in dcs.log[a.warmup:a.warmup + a.steps]]
+        dcs.flush()
+        Tc = [t + 8 for t in dcs.T]
+        dcs.greedy_run(dcs.pending, Tc, a.gamma, False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dcs.greedy_run(dcs.pending, Tc, a.baseline_tokens, False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_cs_only = max_over_ranks(e0.elapsed_time(e1)) / a.baseline_tokens
+        kk = int(np.floor(a.csparse_keep * cfg.ffn_dim // tp + 0.5))
+        cs_bytes = step_bytes(cfg, tp, dcs.T[0], None, B) - cfg.n_layers * 3 * (cfg.ffn_dim // tp - kk) * cfg.d_model * 2
+        csp = {"keep": a.csparse_keep, "neurons_per_layer": kk,
+               "sirius_ms_per_token": t_cs_sir / sum(adv_cs), "aal": sum(adv_cs) / a.steps,
+               "cs_only_ms_per_token": t_cs_only, "cs_only_hbm_gbs": cs_bytes / (t_cs_only / 1e3) / 1e9,
+               "sirius_vs_dense": (t_cs_sir / sum(adv_cs)) / base["dense"],
+               "global_density": cs_bytes / step_bytes(cfg, tp, dcs.T[0], None, B)}
+        ctx.sirius_csparse_enable(0.0)
     # ---------------- latency model: per committed token
     # ((gamma-1) t_CS + t_verify + t_rewrite + t_host) / AAL, the components measured above
     t_ver = prof.get("correct_kernel", (0.0, 0))
@@ -437,6 +477,7 @@ def main():
                         "tokens_per_s_aggregate": B * 1e3 / base["cs_only"]},
             "sirius_vs_dense": sirius_ms_tok / base["dense"],
             "sirius_r_alt": alt,
+            "csparse": csp,
             "latency_model": model,
             "roofline": roof, "per_kernel_device_ms": per_kernel,
             "cpu_baseline": cpu,

@@ -15,6 +15,7 @@
  *                         §4.2)
  *   kv_rewrite          — commit + rollback: overwrite the committed span with the full model's K/V
  *
+ *   sirius_csparse_enable — CSparse draft model: the prompt's fixed neuron set
  *   sirius_destroy / sirius_last_error
  *
  * Conventions (all entry points):
@@ -92,7 +93,11 @@ typedef struct {
 } sirius_weights;
 
 /* sparse_decode_step flags */
-enum { SIRIUS_DENSE = 1u /* run M_F (dense FFN) instead of M_S */ };
+enum {
+  SIRIUS_DENSE = 1u,  /* run M_F (dense FFN) instead of M_S                                            */
+  SIRIUS_CSPARSE = 2u /* run M_S as the CSparse model: the FFN restricted to the last prompt's neuron
+                         plan (sirius_csparse_enable), instead of CATS      */
+};
 
 /* correct_kernel accept modes */
 enum {
@@ -131,8 +136,10 @@ sirius_status sirius_prefill(sirius_ctx* ctx, const int32_t* tokens, const int32
 
 /* One decode step for every sequence: the token token_in[b] at position pos[b] is run through M_S
  * (CATS-sparse FFN: dense gate, |SiLU(g)| >= t_l, only active W_up / W_down rows read) or, with
- * SIRIUS_DENSE, through M_F; its K/V are written to cache slot pos[b]; the greedy next token
- * (lowest id on ties) goes to token_out[b].  (Alg. 1 "Running sparse model".)
+ * SIRIUS_DENSE, through M_F, or with SIRIUS_CSPARSE through the CSparse model (state error without a
+ * plan from sirius_csparse_enable + sirius_prefill; gate_act_out must then be NULL); its K/V are
+ * written to cache slot pos[b]; the greedy next token (lowest id on ties) goes to token_out[b].
+ * (Alg. 1 "Running sparse model".)
  *  token_in, pos   DEV int32 [batch]; pos[b] in [0, max_seq) (device-checked).
  *  token_out       DEV int32 [batch].
  *  logits_out      DEV fp32 [batch, vocab/tp] or NULL.
@@ -169,6 +176,20 @@ sirius_status correct_kernel(sirius_ctx* ctx, const int32_t* kernel_tokens, cons
  *  n_rows     DEV int32 [batch], each in [1, gamma of that call] (device-checked).
  * Errors: STATE if no correct_kernel preceded it. */
 sirius_status kv_rewrite(sirius_ctx* ctx, const int32_t* start_pos, const int32_t* n_rows);
+
+/* CSparse / Griffin-style coarse-grained sparsity (§2.1 "within the
+ * same input prompt, the sparsity pattern is fixed for all tokens generated", :182 §3.2 the pattern is
+ * set after prefilling so the gate is sparse too, :471 the paper's latency numbers use Griffin).
+ * After this call every sirius_prefill also accumulates, per layer and neuron of this rank's shard, the
+ * statistic s_i = sum over the prompt of |SiLU(g_i)| of the dense model, and then keeps the
+ * k = round(keep_fraction * ffn/tp) neurons with the largest s_i (exact ties to the lower index;
+ * reading D28), gathering their W_gate / W_up / W_down rows into context-owned compact matrices
+ * (3 k d bf16 per layer).  sparse_decode_step(..., SIRIUS_CSPARSE) then runs the FFN as the dense
+ * SiLU-gated MLP of the kept neurons.  keep_fraction 0 disables.  TP > 1: each rank keeps the top
+ * k of its own shard.
+ * Errors: INVALID_ARG (keep_fraction outside [0, 1]); UNSUPPORTED (batch != 1, or k not a positive
+ * multiple of 8); CUDA (allocation).  Synchronous. */
+sirius_status sirius_csparse_enable(sirius_ctx* ctx, float keep_fraction);
 
 /* The full model's greedy token (argmax, lowest id on ties) of EVERY verify row of the last
  * correct_kernel call — the interleaving candidates of the component ablation without rollback

@@ -32,6 +32,10 @@ bool attn_stage_supported(int hd, int G);
 extern int g_gemm_kbox;
 extern int g_gemm_coarse;
 cudaError_t attn_stage(const StepArgs& a, int l, int B, cudaStream_t st);
+cudaError_t csparse_colsum(const float* a, int M, int F, long long lda, float* stats, cudaStream_t st);
+cudaError_t csparse_select(const float* stats, int L, int F, int k, int32_t* idx, cudaStream_t st);
+cudaError_t csparse_gather(const uint16_t* src, const int32_t* idx, int k, int d, uint16_t* dst, int num_sms,
+                           cudaStream_t st);
 }  // namespace launch
 }  // namespace sirius
 
@@ -98,12 +102,20 @@ struct RankState {
   unsigned long long* ffn_barrier = nullptr;
   unsigned* attn_bar = nullptr;  // split-group barriers (count, generation) of the attention kernels
   unsigned *attn_cnt = nullptr, *gemm_cnt = nullptr, *head_cnt = nullptr;
+  // CSparse (csparse.cu): prompt statistic [L][Fr], the plan [L][k], a-export of a prefill chunk
+  // [MAXM][Fr], compact weights [3][L][k][d] (gate, up, down rows of the kept neurons)
+  float *cs_stats = nullptr, *cs_scratch = nullptr;
+  int32_t* cs_idx = nullptr;
+  uint16_t* cs_w = nullptr;
 };
 
 struct sirius_ctx {
   sirius_config cfg;
   int nranks = 1;  // ranks run by this context (tp_size when emulating, else 1)
   bool emulated = false;
+  float cs_keep = 0.f;   // CSparse keep fraction (sirius_csparse_enable); 0 = off
+  int cs_k = 0;          // neurons kept per layer (this rank's shard)
+  bool cs_ready = false; // the plan of the last prefill is built
   bool stub_comm = false;  // SIRIUS_DEBUG_STUB_COMM: tp_size > 1 on one GPU with every collective skipped
                            // (one rank's compute, timing proxy only: results are rank-local partials)
   void* comm = nullptr;
@@ -364,7 +376,7 @@ sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev,
 // contribution to the residual (accumulated into out, which the O-proj GEMV zeroed, in atomic mode)
 sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float* base, const float* delta,
                                 float* res_out, float* out, bool dense, int32_t* n_active_out, int n_active_stride,
-                                float* gate_out, long long gate_stride) {
+                                float* gate_out, long long gate_stride, bool csparse = false) {
   const sirius_config& cf = c->cfg;
   FfnArgs f = {};
   f.pro.mode = IN_RESID;
@@ -377,6 +389,14 @@ sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float*
   f.w_up = R.w_up[l];
   f.w_down = R.w_down[l];
   f.F = c->Fr;
+  if (csparse) {  // the prompt's fixed neuron set: the dense FFN over the compact [k, d] matrices
+    const size_t per = (size_t)c->cs_k * cf.d_model, L = cf.n_layers;
+    f.w_gate = R.cs_w + (0 * L + l) * per;
+    f.w_up = R.cs_w + (1 * L + l) * per;
+    f.w_down = R.cs_w + (2 * L + l) * per;
+    f.F = c->cs_k;
+    dense = true;
+  }
   f.d = cf.d_model;
   f.threshold = c->thresholds + l;
   f.dense = dense ? 1 : 0;
@@ -390,7 +410,8 @@ sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float*
   f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
   f.gate_out = gate_out;
   f.gate_stride = gate_stride;
-  const int grid = c->ffn_atomic ? std::min((c->Fr + 7) / 8, c->ffn_split * c->num_sms) : launch::ffn_grid(c->Fr, c->num_sms);
+  const int grid = c->ffn_atomic ? std::min((f.F + 7) / 8, c->ffn_split * c->num_sms) : launch::ffn_grid(f.F, c->num_sms);
+  if (grid < 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "FFN width not supported by the decode FFN kernel");
   LCU(launch::ffn(f, cf.batch, grid, c->stream));
   return SIRIUS_OK;
 }
@@ -585,7 +606,13 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         mk.gate_out = gate_act_out + (size_t)l * Ff + (c->emulated ? (size_t)R.rank * c->Fr : 0);
         mk.gate_stride = (long long)L * Ff;
       }
+      const bool cs_stats = mode == ROWS_PREFILL && c->cs_keep > 0.f;  // CSparse statistic of the prompt
+      if (cs_stats) {
+        mk.gate_out = R.cs_scratch;
+        mk.gate_stride = c->Fr;
+      }
       OK(run_gemm(c, R, R.w_gate[l], R.w_up[l], R.xn3, c->Fr, d, M, R.mb3, c->Fr, gtr2, &mk));
+      if (cs_stats) LCU(launch::csparse_colsum(R.cs_scratch, M, c->Fr, c->Fr, R.cs_stats + (size_t)l * c->Fr, c->stream));
       OK(run_gemm(c, R, R.w_down_t[l], nullptr, R.mb3, d, c->Fr, M, R.dF, d, gtr2 ? gtr2 + 8 * 1024 : nullptr));
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
@@ -813,6 +840,9 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
     if (prompt_len[b] > cf.max_seq - cf.max_gamma) return fail(c, SIRIUS_ERR_CAPACITY, "prompt longer than max_seq - max_gamma");
   }
   const int d = cf.d_model;
+  c->cs_ready = false;
+  if (c->cs_keep > 0.f)
+    for (auto& R : c->ranks) CU(cudaMemsetAsync(R.cs_stats, 0, sizeof(float) * cf.n_layers * c->Fr, c->stream));
   for (int b = 0; b < cf.batch; ++b) {
     const int P = prompt_len[b];
     for (int s = 0; s < P; s += c->MAXM) {
@@ -853,11 +883,65 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
     }
     off += P;
   }
+  if (c->cs_keep > 0.f) {  // CSparse plan of this prompt (reading D28) + compact weights
+    const int L = cf.n_layers, k = c->cs_k;
+    const size_t per = (size_t)k * d;
+    for (auto& R : c->ranks) {
+      LCU(launch::csparse_select(R.cs_stats, L, c->Fr, k, R.cs_idx, c->stream));
+      for (int l = 0; l < L; ++l) {
+        const int32_t* idx = R.cs_idx + (size_t)l * k;
+        LCU(launch::csparse_gather(R.w_gate[l], idx, k, d, R.cs_w + (0 * (size_t)L + l) * per, c->num_sms, c->stream));
+        LCU(launch::csparse_gather(R.w_up[l], idx, k, d, R.cs_w + (1 * (size_t)L + l) * per, c->num_sms, c->stream));
+        LCU(launch::csparse_gather(R.w_down[l], idx, k, d, R.cs_w + (2 * (size_t)L + l) * per, c->num_sms, c->stream));
+      }
+    }
+    c->cs_ready = true;
+  }
   mirror_err(c);
   CU(cudaGetLastError());
   c->prefilled = true;
   c->have_correct = false;
   return SIRIUS_OK;
+}
+
+// CSparse: allocate the plan and the compact weights; every later sirius_prefill
+// gathers the statistic and builds the plan (reading D28); SIRIUS_CSPARSE decode steps use it.
+sirius_status sirius_csparse_enable(sirius_ctx* c, float keep_fraction) {
+  if (!c || !(keep_fraction >= 0.f && keep_fraction <= 1.f)) return SIRIUS_ERR_INVALID_ARG;
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  if (keep_fraction == 0.f) {
+    c->cs_keep = 0.f;
+    c->cs_ready = false;
+    return SIRIUS_OK;
+  }
+  if (cf.batch != 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "CSparse: batch 1 only (one prompt, one neuron set)");
+  const int k = (int)std::floor((double)keep_fraction * c->Fr + 0.5);
+  if (k < 8 || k % 8) return fail(c, SIRIUS_ERR_UNSUPPORTED, "CSparse: kept neurons per rank must be a multiple of 8");
+  const int L = cf.n_layers;
+  for (auto& R : c->ranks) {
+    if (R.cs_stats) continue;  // allocated by an earlier call for the full width
+    if (alloc(c, &R.cs_stats, (size_t)L * c->Fr) || alloc(c, &R.cs_scratch, (size_t)c->MAXM * c->Fr) ||
+        alloc(c, &R.cs_idx, (size_t)L * c->Fr) || alloc(c, &R.cs_w, (size_t)3 * L * c->Fr * cf.d_model, false))
+      return SIRIUS_ERR_CUDA;
+  }
+  c->cs_keep = keep_fraction;
+  c->cs_k = k;
+  c->cs_ready = false;
+  return SIRIUS_OK;
+}
+
+// test/debug: the last prefill's statistic [n_layers, ffn/tp] (DEV fp32) and plan [n_layers, k] (DEV
+// int32, ascending neuron indices within the shard); either may be NULL.  Synchronous.
+int sirius_debug_csparse_plan(sirius_ctx* c, float* stats_out, int32_t* idx_out, int32_t* k_out) {
+  if (!c || !c->cs_ready) return SIRIUS_ERR_STATE;
+  RankState& R = c->ranks[0];
+  const int L = c->cfg.n_layers;
+  if (k_out) *k_out = c->cs_k;
+  cudaStreamSynchronize(c->stream);
+  if (stats_out) cudaMemcpy(stats_out, R.cs_stats, sizeof(float) * L * c->Fr, cudaMemcpyDeviceToDevice);
+  if (idx_out) cudaMemcpy(idx_out, R.cs_idx, sizeof(int32_t) * L * c->cs_k, cudaMemcpyDeviceToDevice);
+  return (int)cudaGetLastError();
 }
 
 static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* tokens, int gamma, int M, float* logits_out,
@@ -888,10 +972,11 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
   const sirius_config& cf = c->cfg;
   const int B = cf.batch, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   const bool dense = flags & SIRIUS_DENSE;
+  const bool csparse = flags & SIRIUS_CSPARSE;
   if (c->decode_rows) return enqueue_decode_rows(c, token_in, pos, dense, token_out, logits_out, n_active_out,
                                                  gate_act_out);
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
-  if (c->use_step) {  // the whole step in one persistent launch (decode_step.cu)
+  if (c->use_step && !csparse) {  // the whole step in one persistent launch (decode_step.cu)
     RankState& R = c->ranks[0];
     StepArgs s = {};
     s.d = d;
@@ -1028,7 +1113,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       }
       prof_begin(c, P_FFN);
       OK(launch_decode_ffn(c, R, l, R.resA, R.dA, R.resB, R.dF, dense, n_active_out ? n_active_out + l : nullptr, L,
-                           g_out, g_stride));
+                           g_out, g_stride, csparse));
       prof_end(c);
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
@@ -1070,8 +1155,12 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
 sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
                                  int32_t* token_out, float* logits_out, int32_t* n_active_out, float* gate_act_out) {
   if (!c || !token_in || !pos || !token_out) return SIRIUS_ERR_INVALID_ARG;
-  if (flags & ~(uint32_t)SIRIUS_DENSE) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
+  if (flags & ~(uint32_t)(SIRIUS_DENSE | SIRIUS_CSPARSE)) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
+  if ((flags & SIRIUS_CSPARSE) && (flags & SIRIUS_DENSE)) return fail(c, SIRIUS_ERR_INVALID_ARG, "CSPARSE with DENSE");
+  if ((flags & SIRIUS_CSPARSE) && gate_act_out) return fail(c, SIRIUS_ERR_INVALID_ARG, "CSPARSE exports no gate");
   OK(check_sticky(c));
+  if ((flags & SIRIUS_CSPARSE) && !c->cs_ready)
+    return fail(c, SIRIUS_ERR_STATE, "CSPARSE decode without a plan (sirius_csparse_enable + sirius_prefill)");
   GraphKey key = {0xDEC0u, flags, (uintptr_t)token_in, (uintptr_t)pos, (uintptr_t)token_out, (uintptr_t)logits_out,
                   (uintptr_t)n_active_out, (uintptr_t)gate_act_out};
   return run_graphed(c, key, [&] {

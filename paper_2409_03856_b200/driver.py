@@ -50,10 +50,14 @@ class GenOut:
 
 
 class Driver:
-    def __init__(self, ctx: S.Sirius, rewrite: bool = True, interleave: bool = True, rollback: bool = True):
+    def __init__(self, ctx: S.Sirius, rewrite: bool = True, interleave: bool = True, rollback: bool = True,
+                 csparse: bool = False):
+        """csparse: the draft model M_S is the CSparse model of the prompt (sirius_csparse_enable must
+        have been called on ctx; the plan is built by every begin()) instead of CATS."""
         import torch
         assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
         self.rewrite, self.interleave, self.rollback = rewrite, interleave, rollback
+        self.sparse_flags = S.SIRIUS_CSPARSE if csparse else 0
         self.ctx, self.torch = ctx, torch
         B, gm = ctx.batch, ctx.max_gamma
         dev = "cuda"
@@ -139,7 +143,7 @@ class Driver:
         if self.need_rewrite:  # commit + rollback of the previous kernel
             self.ctx.kv_rewrite(self.start[(self.kidx - 1) % 2], self.n_rows)
         for i in range(gamma - 1):  # M_S drafts gamma-1 tokens (Alg. 1 lines 6-11)
-            self.ctx.sparse_decode_step(self.drafts[i], self.pos[i], 0, self.drafts[i + 1])
+            self.ctx.sparse_decode_step(self.drafts[i], self.pos[i], self.sparse_flags, self.drafts[i + 1])
         if B == 1:
             kt = self.drafts[:gamma].view(1, gamma)
         else:
@@ -210,7 +214,7 @@ class Driver:
         return GenOut([host[:, b].tolist() for b in range(B)], steps=n_tokens - 1)
 
     def greedy_steps(self, toks, pos, n: int, dense: bool, first: int = 0) -> None:
-        flags = S.SIRIUS_DENSE if dense else 0
+        flags = S.SIRIUS_DENSE if dense else self.sparse_flags
         for i in range(first, first + n):
             self.ctx.sparse_decode_step(toks[i], pos[i], flags, toks[i + 1])
 
@@ -219,7 +223,7 @@ class Driver:
         T, T+1, ...: chunks of max_gamma steps over fixed buffer slots (so each step replays a cached
         CUDA graph), one H2D of the chunk's positions per chunk, no host sync."""
         B, m = self.B, self.gmax
-        flags = S.SIRIUS_DENSE if dense else 0
+        flags = S.SIRIUS_DENSE if dense else self.sparse_flags
         T = list(T)
         self.drafts[0].copy_(self.torch.tensor(pending, dtype=self.torch.int32), non_blocking=False)
         done = 0

@@ -19,12 +19,14 @@ SIRIUS_ERR_INVALID_ARG, SIRIUS_ERR_CAPACITY, SIRIUS_ERR_STATE = -1, -2, -3
 SIRIUS_ERR_CUDA, SIRIUS_ERR_NCCL, SIRIUS_ERR_UNSUPPORTED = -4, -5, -6
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "CAPACITY", -3: "STATE", -4: "CUDA", -5: "NCCL", -6: "UNSUPPORTED"}
 SIRIUS_DENSE = 1
+SIRIUS_CSPARSE = 2
 ACCEPT_THRESHOLD = 0
 ACCEPT_EXACT_ARGMAX = 1
 
 # every symbol include/sirius.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
-               "sirius_verify_row_argmax", "sirius_destroy", "sirius_last_error", "sirius_version")
+               "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_destroy", "sirius_last_error",
+               "sirius_version")
 
 
 class SiriusError(RuntimeError):
@@ -76,6 +78,10 @@ def load():
         lib.kv_rewrite.restype = I
         lib.sirius_verify_row_argmax.argtypes = [P, P]
         lib.sirius_verify_row_argmax.restype = I
+        lib.sirius_csparse_enable.argtypes = [P, F]
+        lib.sirius_csparse_enable.restype = I
+        lib.sirius_debug_csparse_plan.argtypes = [P, P, P, ctypes.POINTER(I)]
+        lib.sirius_debug_csparse_plan.restype = I
         lib.sirius_destroy.argtypes = [P]
         lib.sirius_destroy.restype = I
         lib.sirius_last_error.argtypes = [P]
@@ -186,6 +192,20 @@ class Sirius:
 
     def sirius_verify_row_argmax(self, out):
         self._check(self.lib.sirius_verify_row_argmax(self.h, _ptr(out)))
+
+    def sirius_csparse_enable(self, keep_fraction: float):
+        self._check(self.lib.sirius_csparse_enable(self.h, float(keep_fraction)))
+
+    def debug_csparse_plan(self):
+        """Test-only: (statistic fp32 [L, ffn/tp], plan int32 [L, k]) of the last prefill."""
+        torch = self.torch
+        k = ctypes.c_int32(0)
+        self._check(self.lib.sirius_debug_csparse_plan(self.h, None, None, ctypes.byref(k)))
+        L, F = self.cfg.n_layers, self.cfg.ffn_dim // self.tp_size
+        stats = torch.zeros((L, F), dtype=torch.float32, device="cuda")
+        idx = torch.zeros((L, k.value), dtype=torch.int32, device="cuda")
+        self._check(self.lib.sirius_debug_csparse_plan(self.h, _ptr(stats), _ptr(idx), None))
+        return stats, idx
 
     # ---- instrumentation (bench / tests) ------------------------------------------------
     def debug_ffn(self, layer: int, x, dense: bool, out, gate_out=None, n_active=None) -> None:
