@@ -117,8 +117,11 @@ size_t kv_index(const Oracle* o, int l, int slot, int nslots, int kvh) {
 // One decoder layer's attention block for a row at position pos.
 // Visible keys: if stage_row < 0, cache slots [0, pos] (the row's own K/V were just written to
 // slot pos); else cache slots [0, pos - stage_row) followed by staging rows [0, stage_row].
+// Tree rows (tree_vis != 0): cache slots [0, n_cache) followed by
+// the staging rows whose bit is set in tree_vis (the row's ancestor chain and itself), in index order.
 // kv_only: stop after the row's K/V are stored (nothing downstream of them is wanted).
-void attention_block(Oracle* o, int l, double* x, int pos, int stage_row, bool kv_only = false) {
+void attention_block(Oracle* o, int l, double* x, int pos, int stage_row, bool kv_only = false,
+                     uint64_t tree_vis = 0, int tree_n_cache = 0) {
   const int d = o->d, H = o->H, KV = o->KV, hd = o->hd, rows = (H + 2 * KV) * hd;
   std::vector<double> h(d), qkv(rows), attn(H * hd), y(d);
   rmsnorm(o, x, o->attn_norm[l], h.data());
@@ -142,8 +145,16 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row, bool k
       }
     }
   if (kv_only) return;
-  const int n_cache = stage_row < 0 ? pos + 1 : pos - stage_row;
-  const int n_stage = stage_row < 0 ? 0 : stage_row + 1;
+  int n_cache = stage_row < 0 ? pos + 1 : pos - stage_row;
+  std::vector<int> srows;  // visible staging rows, ascending
+  if (tree_vis) {
+    n_cache = tree_n_cache;
+    for (int r = 0; r < 64; ++r)
+      if ((tree_vis >> r) & 1ull) srows.push_back(r);
+  } else if (stage_row >= 0) {
+    for (int r = 0; r <= stage_row; ++r) srows.push_back(r);
+  }
+  const int n_stage = (int)srows.size();
   const int n_vis = n_cache + n_stage;
   const double scale = 1.0 / std::sqrt((double)hd);
   std::vector<double> s(n_vis);
@@ -152,11 +163,11 @@ void attention_block(Oracle* o, int l, double* x, int pos, int stage_row, bool k
     const double* qh = q + hh * hd;
     auto key = [&](int p) -> const double* {
       return p < n_cache ? &o->kc[kv_index(o, l, p, o->max_seq, kh)]
-                         : &o->ks[kv_index(o, l, p - n_cache, o->max_gamma, kh)];
+                         : &o->ks[kv_index(o, l, srows[p - n_cache], o->max_gamma, kh)];
     };
     auto val = [&](int p) -> const double* {
       return p < n_cache ? &o->vc[kv_index(o, l, p, o->max_seq, kh)]
-                         : &o->vs[kv_index(o, l, p - n_cache, o->max_gamma, kh)];
+                         : &o->vs[kv_index(o, l, srows[p - n_cache], o->max_gamma, kh)];
     };
     double mx = -INFINITY;
     for (int p = 0; p < n_vis; ++p) {
@@ -274,15 +285,17 @@ void oracle_set_layer(void* h, int l, const uint16_t* attn_norm, const uint16_t*
 // stage_row < 0: write K/V to cache slot pos; >= 0: write to staging row stage_row (verify).
 // logits: [vocab] fp64 or NULL.  gate_out: [L*ffn] a = SiLU(g) or NULL.  mask_out: [L*ffn] or NULL.
 // n_active: [L] or NULL.  x_out: [d] final residual (pre final-norm) or NULL.
+// tree_vis != 0 (tree rows, stage_row >= 0): the row sees cache [0, tree_n_cache) and the staging rows of
+// its bits (ancestor chain + itself) instead of staging [0, stage_row].
 void oracle_forward_row(void* h, int tok, int pos, int sparse, const float* thresholds, int stage_row,
                         double* logits, double* gate_out, uint8_t* mask_out, int* n_active, double* x_out,
-                        const uint8_t* plan) {
+                        const uint8_t* plan, uint64_t tree_vis, int tree_n_cache) {
   Oracle* o = (Oracle*)h;
   const int d = o->d;
   std::vector<double> x(d), hf(d);
   for (int k = 0; k < d; ++k) x[k] = bf16_value(o->embed[(size_t)tok * d + k]);  // x = E[tok]
   for (int l = 0; l < o->L; ++l) {
-    attention_block(o, l, x.data(), pos, stage_row);
+    attention_block(o, l, x.data(), pos, stage_row, false, tree_vis, tree_n_cache);
     mlp_block(o, l, x.data(), sparse, sparse == 1 ? (double)thresholds[l] : 0.0,
               gate_out ? gate_out + (size_t)l * o->ffn : nullptr, mask_out ? mask_out + (size_t)l * o->ffn : nullptr,
               n_active ? n_active + l : nullptr, sparse == 2 ? plan + (size_t)l * o->ffn : nullptr);
@@ -326,6 +339,19 @@ void oracle_kv_rewrite(void* h, int T, int n) {
         for (int i = 0; i < o->hd; ++i) {
           o->kc[kv_index(o, l, T + r, o->max_seq, kh) + i] = o->ks[kv_index(o, l, r, o->max_gamma, kh) + i];
           o->vc[kv_index(o, l, T + r, o->max_seq, kh) + i] = o->vs[kv_index(o, l, r, o->max_gamma, kh) + i];
+        }
+}
+
+// Tree commit ("select the one that reaches the longest advance length", with the KV rewrite
+// of P:257): staging rows rows[0..n) -> cache slots [T, T+n).
+void oracle_kv_rewrite_rows(void* h, int T, int n, const int* rows) {
+  Oracle* o = (Oracle*)h;
+  for (int l = 0; l < o->L; ++l)
+    for (int r = 0; r < n; ++r)
+      for (int kh = 0; kh < o->KV; ++kh)
+        for (int i = 0; i < o->hd; ++i) {
+          o->kc[kv_index(o, l, T + r, o->max_seq, kh) + i] = o->ks[kv_index(o, l, rows[r], o->max_gamma, kh) + i];
+          o->vc[kv_index(o, l, T + r, o->max_seq, kh) + i] = o->vs[kv_index(o, l, rows[r], o->max_gamma, kh) + i];
         }
 }
 

@@ -54,7 +54,8 @@ def _lib():
         lib.oracle_set_global.argtypes = [P, P, P, P]
         lib.oracle_set_layer.argtypes = [P, ctypes.c_int] + [P] * 7
         lib.oracle_forward_row.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P, P, P,
-                                           P]
+                                           P, ctypes.c_uint64, ctypes.c_int]
+        lib.oracle_kv_rewrite_rows.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
         lib.oracle_prefill_kv_row.argtypes = [P, ctypes.c_int, ctypes.c_int]
         lib.oracle_mlp.argtypes = [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_float, P, P, P, P]
         lib.oracle_kv_rewrite.argtypes = [P, ctypes.c_int, ctypes.c_int]
@@ -113,7 +114,7 @@ class OracleModel:
     # ------------------------------------------------------------ one row
     def forward_row(self, tok: int, pos: int, sparse: bool = False, thresholds: Optional[np.ndarray] = None,
                     stage_row: int = -1, want_gate: bool = False, want_mask: bool = False,
-                    plan: Optional[np.ndarray] = None) -> RowOut:
+                    plan: Optional[np.ndarray] = None, tree_vis: int = 0, tree_n_cache: int = 0) -> RowOut:
         """sparse with plan (uint8 [L, ffn], csparse_plan): the CSparse model; sparse with thresholds:
         the CATS (FSparse) model; else the dense model."""
         cfg = self.cfg
@@ -134,7 +135,8 @@ class OracleModel:
             assert thr.shape == (cfg.n_layers,)
             mode = 1
         _lib().oracle_forward_row(self.h, int(tok), int(pos), mode, _ptr(thr), int(stage_row),
-                                  _ptr(logits), _ptr(gate), _ptr(mask), _ptr(nact), None, _ptr(pl))
+                                  _ptr(logits), _ptr(gate), _ptr(mask), _ptr(nact), None, _ptr(pl),
+                                  int(tree_vis), int(tree_n_cache))
         return RowOut(logits, gate, mask, nact)
 
     def mlp(self, layer: int, x: np.ndarray, sparse: bool, threshold: float = 0.0, plan: Optional[np.ndarray] = None):
@@ -153,6 +155,12 @@ class OracleModel:
     def kv_rewrite(self, T: int, n: int) -> None:
         assert 1 <= n <= self.max_gamma and T + n <= self.max_seq
         _lib().oracle_kv_rewrite(self.h, int(T), int(n))
+
+    def kv_rewrite_rows(self, T: int, rows: Sequence[int]) -> None:
+        """Commit staging rows `rows` (in order) into cache slots [T, T + len(rows)) (tree commit)."""
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        assert 1 <= len(r) and T + len(r) <= self.max_seq and r.max() < self.max_gamma
+        _lib().oracle_kv_rewrite_rows(self.h, int(T), len(r), _ptr(r))
 
     def read_cache(self, layer: int, n: int):
         cfg = self.cfg
@@ -265,6 +273,100 @@ class KernelRecord:
     draft_margin: np.ndarray = None   # [g-1] top-2 logit margin of each sparse drafting row
     verify_margin: np.ndarray = None  # [g] top-2 logit margin of each verify row
     advance: int = 0                  # tokens committed by this kernel (j + 1 with rollback, else g)
+    tree: Optional["TreeKernel"] = None  # the tree of a tree kernel (tree_width given)
+
+
+def log_softmax(l: np.ndarray) -> np.ndarray:
+    m = l.max()
+    return l - (m + np.log(np.exp(l - m).sum()))
+
+
+@dataclass
+class TreeKernel:
+    """One tree correction kernel (reading D29).  Flattened rows:
+    0 = the pending token at position T; node w of step s (1 <= s <= gamma-1) = row 1 + (s-1) W + w at
+    position T + s."""
+    tokens: List[int]
+    parent: List[int]
+    cum: List[float]        # cumulative sparse log-likelihood of the node's path (root 0)
+    vis: List[int]          # 64-bit ancestor-or-self masks over the flattened rows
+    q: np.ndarray           # full-model probability of each node's token given its ancestors (root: nan)
+    path: List[int]         # winning path rows, root first, up to the cut (length j + 1)
+    j: int                  # accepted nodes on the winning path
+    next_token: int
+    leaf_accept: List[int]  # accepted length of every leaf's path
+
+
+def tree_kernel(model: OracleModel, pending: int, T: int, gamma: int, r: float, thresholds, width: int,
+                branch: int = 3, accept_mode: int = ACCEPT_THRESHOLD, plan=None) -> TreeKernel:
+    """Hardware-friendly tree building and verification (reading D29):
+      * drafting (Alg. 1 lines 6-11 with a tree): step s decodes the step-(s-1) nodes with the sparse
+        model (each node attends the committed cache [0, T) and its ancestor chain), expands each
+        with its top-`branch` tokens of the sparse log-softmax (temperature 1), and keeps the `width`
+        candidates of largest cumulative log-likelihood, ties to the lower parent rank then the lower
+        token id ("a fixed number of leaves ... through tree pruning based on ranking the cumulative
+        log-likelihood of the path"); step 1 keeps the root's top max(width, branch) tokens pruned to
+        `width`;
+      * verification: one dense forward over all 1 + (gamma-1) width rows with ancestor masks;
+      * every leaf's path is scanned like a linear kernel (q = softmax(full logits of the parent
+        row)[node token] >= r); the path with the longest accepted prefix wins ("select the one that
+        reaches the longest advance length"), ties to the higher leaf cumulative log-likelihood, then
+        the lower leaf row; the interleaved token is the full model's argmax at the cut node;
+      * the winning path's full-model K/V rows are rewritten into cache slots [T, T+j] (rollback +
+        KV rewrite on a tree)."""
+    S, W = gamma - 1, width
+    n_rows = 1 + S * W
+    assert n_rows <= min(64, model.max_gamma), "tree rows must fit the 64-bit masks and the staging area"
+    toks, parent, cum, vis = [pending], [-1], [0.0], [1]
+    frontier = [0]
+    for s in range(1, S + 1):
+        cands = []  # (cum, parent rank, token, parent row)
+        for pr, f in enumerate(frontier):
+            row = model.forward_row(toks[f], T + s - 1, True, thresholds, stage_row=f, plan=plan, tree_vis=vis[f],
+                                    tree_n_cache=T)
+            lp = log_softmax(row.logits)
+            nb = max(W, branch) if s == 1 else branch
+            top = np.lexsort((np.arange(lp.size), -lp))[:nb]
+            cands += [(cum[f] + float(lp[t]), pr, int(t), f) for t in top]
+        keep = sorted(cands, key=lambda c: (-c[0], c[1], c[2]))[:W]
+        frontier = []
+        for w, (c, pr, t, f) in enumerate(keep):
+            n = 1 + (s - 1) * W + w
+            toks.append(t)
+            parent.append(f)
+            cum.append(c)
+            vis.append(vis[f] | (1 << n))
+            frontier.append(n)
+    step = [0] + [1 + (n - 1) // W for n in range(1, n_rows)]
+    lf = np.stack([model.forward_row(toks[n], T + step[n], False, None, stage_row=n, tree_vis=vis[n], tree_n_cache=T).logits
+                   for n in range(n_rows)])
+    q = np.full(n_rows, np.nan)
+    for n in range(1, n_rows):
+        q[n] = softmax_prob(lf[parent[n]], toks[n])
+    best, leaf_acc = None, []
+    for w in range(W):
+        leaf = 1 + (S - 1) * W + w if S > 0 else 0
+        chain = []
+        n = leaf
+        while n > 0:
+            chain.append(n)
+            n = parent[n]
+        chain.reverse()
+        acc = 0
+        for n in chain:
+            ok = q[n] >= r if accept_mode == ACCEPT_THRESHOLD else toks[n] == argmax_lowest(lf[parent[n]])
+            if not ok:
+                break
+            acc += 1
+        leaf_acc.append(acc)
+        key = (acc, cum[leaf], -leaf)
+        if best is None or key > best[0]:
+            best = (key, [0] + chain[:acc])
+    path = best[1]
+    j = len(path) - 1
+    nxt = argmax_lowest(lf[path[-1]])
+    model.kv_rewrite_rows(T, path)
+    return TreeKernel(toks, parent, cum, vis, q, path, j, nxt, leaf_acc)
 
 
 @dataclass
@@ -286,7 +388,8 @@ class GenerateResult:
 
 def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: int, r: float,
              thresholds: Optional[np.ndarray], accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True,
-             interleave: bool = True, rollback: bool = True, csparse_keep: Optional[float] = None) -> GenerateResult:
+             interleave: bool = True, rollback: bool = True, csparse_keep: Optional[float] = None,
+             tree_width: Optional[int] = None, tree_branch: int = 3) -> GenerateResult:
     """The Sirius loop, Algorithm 1, readings D5-D18:
       * dense prefill of the prompt; the first generated token is the dense argmax (D17);
       * kernel size n = gamma: the sparse model drafts gamma-1 tokens after the pending token,
@@ -307,7 +410,10 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
     the first rejection (the statistic), the advance is then g.
 
     csparse_keep: the sparse model is CSparse (Griffin PAPER.md:471) instead of CATS: the
-    neuron plan of the prompt (prefill_stats + csparse_plan, reading D28) fixed for the generation."""
+    neuron plan of the prompt (prefill_stats + csparse_plan, reading D28) fixed for the generation.
+
+    tree_width: hardware-friendly tree building and verification (tree_kernel)
+    instead of the greedy chain; width 1 is the chain (pinned bitwise)."""
     assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
     P = len(prompt)
     assert P + n_tokens + gamma <= model.max_seq and gamma >= 1
@@ -323,6 +429,14 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
     T = P
     res = GenerateResult(out)
     res.plan = plan
+    while len(out) < n_tokens and tree_width is not None:
+        assert rewrite and interleave and rollback, "tree kernels run with every correction component"
+        tk = tree_kernel(model, out[-1], T, gamma, r, thresholds, tree_width, tree_branch, accept_mode, plan)
+        committed = [tk.tokens[n] for n in tk.path[1:]] + [tk.next_token]
+        out += committed
+        res.kernels.append(KernelRecord(T, [tk.tokens[n] for n in tk.path], tk.j, tk.q, tk.next_token,
+                                        np.zeros((0, model.cfg.n_layers), dtype=np.int32), advance=tk.j + 1, tree=tk))
+        T += tk.j + 1
     while len(out) < n_tokens:
         ins = [out[-1]]
         nact, dmarg = [], []
