@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1, 2, 4, 8)")
     ap.add_argument("--baseline-tokens", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tree-width", type=int, default=4, help="tree kernels timed at r_alt (0: skip)")
     ap.add_argument("--csparse-keep", type=float, default=0.5,
                     help="CSparse (Griffin-style) keep fraction for the csparse rows (0: skip)")
     return ap.parse_args()
@@ -345,6 +346,32 @@ def main():
                "rejection_positions": [int(k.j[b]) for k in tl for b in range(B) if int(k.j[b]) < a.gamma - 1],
                "vs_dense": (t_alt / c_alt) / base["dense"]}
         drv.flush()
+    # ---------------- tree building + tree verification at r_alt: the tree's AAL against
+    # the chain's at the same threshold, and its cost per kernel
+    tree = None
+    if a.tree_width > 0 and B == 1 and tp == 1 and 1 + (a.gamma - 1) * a.tree_width <= 64 and alt is not None:
+        ctx_t = S.Sirius(cfg, weights, thr, batch=1, max_seq=max_seq, max_gamma=64)
+        dt = driver.Driver(ctx_t)
+        dt.begin(prompts)
+        for _ in range(a.warmup):
+            dt.step_tree(a.gamma, a.r_alt, a.tree_width)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            dt.step_tree(a.gamma, a.r_alt, a.tree_width)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_tree = max_over_ranks(e0.elapsed_time(e1))
+        adv_t = [int(k.j[0]) + 1 for k in dt.log[a.warmup:a.warmup + a.steps]]
+        dt.flush()
+        tree = {"width": a.tree_width, "branch": 3, "r": a.r_alt, "rows_verified": 1 + (a.gamma - 1) * a.tree_width,
+                "aal": sum(adv_t) / a.steps, "aal_chain_same_r": alt["aal"], "ms_per_kernel": t_tree / a.steps,
+                "ms_per_token": t_tree / sum(adv_t),
+                "note": "tree drafting runs W rows per step through the verify-row machinery (tcgen05 GEMMs over "
+                        "all FFN rows, ancestor-masked attention): ~a verify pass per step"}
+        del dt, ctx_t
+        torch.cuda.empty_cache()
     # ---------------- CSparse (Griffin-style, the sparse model of the paper's latency tables):
     # the same context with the prompt's fixed neuron set; Sirius over the CSparse draft model, and
     # CSparse-only greedy decode
@@ -478,6 +505,7 @@ def main():
             "sirius_vs_dense": sirius_ms_tok / base["dense"],
             "sirius_r_alt": alt,
             "csparse": csp,
+            "tree": tree,
             "latency_model": model,
             "roofline": roof, "per_kernel_device_ms": per_kernel,
             "cpu_baseline": cpu,

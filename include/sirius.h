@@ -16,6 +16,7 @@
  *   kv_rewrite          — commit + rollback: overwrite the committed span with the full model's K/V
  *
  *   sirius_csparse_enable — CSparse draft model: the prompt's fixed neuron set
+ *   sirius_tree_kernel  — tree building + tree verification of one kernel
  *   sirius_destroy / sirius_last_error
  *
  * Conventions (all entry points):
@@ -176,6 +177,28 @@ sirius_status correct_kernel(sirius_ctx* ctx, const int32_t* kernel_tokens, cons
  *  n_rows     DEV int32 [batch], each in [1, gamma of that call] (device-checked).
  * Errors: STATE if no correct_kernel preceded it. */
 sirius_status kv_rewrite(sirius_ctx* ctx, const int32_t* start_pos, const int32_t* n_rows);
+
+/* Tree correction kernel: hardware-friendly tree building and verification (PAPER.md
+ * :299-319 §4.3; reading D29).  Batch 1, TP 1.  One call replaces the gamma-1 sparse_decode_step calls
+ * and correct_kernel of a kernel: the sparse model drafts a fixed-shape tree of `width` nodes per step
+ * (step 1: the pending token's top max(width, branch) tokens; later steps: every node's top `branch`
+ * tokens) kept by cumulative log-likelihood (ties to the lower parent rank, then the lower token id);
+ * the full model verifies all 1 + (gamma-1)·width rows in one forward with ancestor masks; every leaf's
+ * path is scanned as in correct_kernel and the longest accepted path wins (ties to the higher leaf
+ * cumulative log-likelihood, then the lower leaf row); the interleaved token is the full model's argmax
+ * at the cut.  The following kv_rewrite commits the winning path's full-model K/V.
+ *  pending          DEV int32 [1]: the pending token (position T).
+ *  start_pos        DEV int32 [1] = T.
+ *  gamma            kernel size; 1 + (gamma-1)·width <= min(64, max_gamma) (else CAPACITY).
+ *  width, branch    tree width in [1, 8] (width 1: the greedy chain), children per node in [1, 8].
+ *  accept_threshold, accept_mode   as correct_kernel.
+ *  n_accept_out     DEV int32 [1] = j, accepted nodes on the winning path.
+ *  next_token_out   DEV int32 [1] = the full model's argmax at the cut node.
+ *  path_tokens_out  DEV int32 [gamma]: the winning path's tokens, pending first; entries > j are -1.
+ * Errors: INVALID_ARG, CAPACITY, UNSUPPORTED (batch != 1 or tp_size != 1), CUDA. */
+sirius_status sirius_tree_kernel(sirius_ctx* ctx, const int32_t* pending, const int32_t* start_pos, int32_t gamma,
+                                 int32_t width, int32_t branch, float accept_threshold, int32_t accept_mode,
+                                 int32_t* n_accept_out, int32_t* next_token_out, int32_t* path_tokens_out);
 
 /* CSparse / Griffin-style coarse-grained sparsity (§2.1 "within the
  * same input prompt, the sparsity pattern is fixed for all tokens generated", :182 §3.2 the pattern is

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
   const int r_base = rb * kRows;                                  // row index r = i * G + g
   const int nr = min(kRows, rows * G - r_base);                   // valid rows in this block
   const int i_last = (r_base + nr - 1) / G;
-  const int nkeys = max(0, T + i_last + 1);
+  const int nkeys = max(0, T + a.stage_base + i_last + 1);  // own staging row = stage_base + i
   const int S = gridDim.x;
   const int chunk = (nkeys + S - 1) / S;
   const int k0 = min(nkeys, split * chunk), k1 = min(nkeys, k0 + chunk);
@@ -151,8 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
 #pragma unroll
       for (int j = 0; j < RPT; ++j) {
         const int r = r0 + RSTEP * j;
-        const int i = (r_base + r) / G;
-        const bool vis = kk < nb && r < nr && p0 + kk <= T + i;
+        const int i = (r_base + r) / G, p = p0 + kk;
+        bool vis = kk < nb && r < nr;
+        if (p >= T) vis = vis && (a.tree_vis ? ((a.tree_vis[a.stage_base + i] >> (p - T)) & 1ull) != 0 : p <= T + i);
         p_s[r * (kKB + 1) + kk] = vis ? s[j] : -INFINITY;
       }
     }

@@ -16,6 +16,7 @@
 #include "decode_kernels.cuh"
 #include "gemm_tc.cuh"
 #include "verify_kernels.cuh"
+#include "tree.cuh"
 
 namespace sirius {
 namespace launch {
@@ -142,6 +143,8 @@ struct sirius_ctx {
   int32_t* pre_start_host = nullptr;
   int32_t* scratch_tok = nullptr;
   int32_t* row_argmax = nullptr;  // [MAXM] full-model argmax of every row of the last verify
+  TreeState* tree = nullptr;      // tree correction kernels (tree.cu): the last tree and its winning path
+  bool tree_last = false;         // the last correction was a tree kernel (kv_rewrite commits its path)
   int last_gamma = 0;
   bool have_correct = false;
   bool prefilled = false;
@@ -481,9 +484,12 @@ sirius_status run_gemm(sirius_ctx* c, RankState& R, const void* wa, const void* 
 // sparse: CATS mask on the FFN (batched sparse decode, rows_per_seq = 1); n_active_out [rows, L] and
 // gate_act_out [rows, L, ffn] (emulated TP: rank shards concatenated) optional.
 enum RowsMode { ROWS_PREFILL = 0, ROWS_VERIFY = 1, ROWS_DECODE = 2 };
+// Tree rows (tree.cu, batch 1, ROWS_VERIFY): stage_base = staging row of the call's row 0, row_off [rows] =
+// each row's position offset from start, tree_vis = the ancestor masks (attn_rows).
 sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* start, int b_base, int nseq,
                            int rows_per_seq, RowsMode mode, bool sparse = false, int32_t* n_active_out = nullptr,
-                           float* gate_act_out = nullptr) {
+                           float* gate_act_out = nullptr, int stage_base = 0, const int32_t* row_off = nullptr,
+                           const unsigned long long* tree_vis = nullptr) {
   const bool to_cache = mode != ROWS_VERIFY;
   const sirius_config& cf = c->cfg;
   const int M = nseq * rows_per_seq, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
@@ -549,6 +555,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       ra.max_seq = cf.max_seq;
       ra.max_gamma = cf.max_gamma;
       ra.to_cache = to_cache ? 1 : 0;
+      ra.stage_base = stage_base;
+      ra.row_off = row_off;
       ra.q_out = R.qb;
       ra.k_dst = to_cache ? R.k_cache + l * kv_layer : R.stage_k + l * st_layer;
       ra.v_dst = to_cache ? R.v_cache + l * kv_layer : R.stage_v + l * st_layer;
@@ -569,6 +577,8 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       aa.v_fresh = R.stage_v + l * st_layer;
       aa.fresh_stride = cf.max_gamma;
       aa.fresh_in_cache = to_cache ? 1 : 0;
+      aa.stage_base = stage_base;
+      aa.tree_vis = tree_vis;
       aa.part = R.attn_part;
       aa.counters = R.attn_cnt;
       aa.group_bar = R.attn_bar;
@@ -708,7 +718,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       alloc(c, &c->stats_gather, (size_t)cf.tp_size * c->MAXM * c->accept_splits) ||
       alloc(c, &c->dA_ptrs, 64) || alloc(c, &c->dF_ptrs, 64) || alloc(c, &c->pre_start, B) ||
       alloc(c, &c->dec_nacc, B) || alloc(c, &c->row_argmax, 256) ||
-      alloc(c, &c->scratch_tok, 64))
+      alloc(c, &c->scratch_tok, 64) || alloc(c, &c->tree, 1))
     return cleanup_fail(SIRIUS_ERR_CUDA);
   if (cudaHostAlloc(&c->err_host, 64, cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc(&c->pre_start_host, sizeof(int32_t) * B, cudaHostAllocDefault) != cudaSuccess)
@@ -1267,6 +1277,85 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
   }));
   c->last_gamma = gamma;
   c->have_correct = true;
+  c->tree_last = false;
+  return SIRIUS_OK;
+}
+
+// ---- tree correction kernel (tree.cu, reading D29), batch 1, TP 1:
+// drafting steps s = 1 .. gamma-1 through the verify row machinery with the CATS FFN and ancestor-masked
+// attention (the step-(s-1) nodes' sparse K/V land in their staging rows), head GEMM, top-k + prune; then
+// one dense forward over every tree row, head GEMM, per-row LSE / argmax, accept on every leaf's path.
+static sirius_status head_rows(sirius_ctx* c, RankState& R, int M) {  // final RMSNorm + LM head -> R.logits
+  const sirius_config& cf = c->cfg;
+  NormRowsArgs na = {};
+  na.base = R.resB;
+  na.delta = R.dF;
+  na.vocab = cf.vocab;
+  na.d = cf.d_model;
+  na.norm_w = R.final_norm;
+  na.eps = cf.rms_eps;
+  na.out3 = R.xn3;
+  na.plane = (size_t)c->MAXM * cf.d_model;
+  LCU(launch::norm_rows(na, M, c->stream));
+  OK(run_gemm(c, R, R.lm_head, nullptr, R.xn3, c->Vr, cf.d_model, M, R.logits, c->Vr));
+  return SIRIUS_OK;
+}
+
+static sirius_status enqueue_tree(sirius_ctx* c, const int32_t* pending, const int32_t* start_pos, int gamma,
+                                  int width, int branch, float r, int mode, int32_t* n_accept_out,
+                                  int32_t* next_token_out, int32_t* path_tokens_out) {
+  RankState& R = c->ranks[0];
+  TreeState* ts = c->tree;
+  const int S = gamma - 1, W = width, n_rows = 1 + S * W;
+  const int kb = W > branch ? W : branch;
+  prof_begin(c, P_VERIFY);
+  LCU(launch::tree_init(ts, pending, c->stream));
+  for (int s = 1; s <= S; ++s) {  // sparse drafting (Alg. 1 lines 6-11 with a tree)
+    const int np = s == 1 ? 1 : W, f0 = s == 1 ? 0 : 1 + (s - 2) * W;
+    OK(forward_rows(c, ts->tok + f0, start_pos, 0, 1, np, ROWS_VERIFY, true, nullptr, nullptr, f0, ts->row_off + f0,
+                    ts->vis));
+    OK(head_rows(c, R, np));
+    LCU(launch::tree_topk(R.logits, c->Vr, c->Vr, np, kb, ts, f0, c->stream));
+    LCU(launch::tree_prune(ts, s, W, branch, c->stream));
+  }
+  // full-model verification of every tree row (staging rows [0, n_rows) rewritten with the full K/V)
+  OK(forward_rows(c, ts->tok, start_pos, 0, 1, n_rows, ROWS_VERIFY, false, nullptr, nullptr, 0, ts->row_off, ts->vis));
+  OK(head_rows(c, R, n_rows));
+  LCU(launch::tree_topk(R.logits, c->Vr, c->Vr, n_rows, 1, ts, 0, c->stream));
+  LCU(launch::tree_accept(R.logits, c->Vr, ts, S, W, r, mode, n_accept_out, next_token_out, path_tokens_out, gamma,
+                          c->stream));
+  prof_end(c);
+  mirror_err(c);
+  CU(cudaGetLastError());
+  return SIRIUS_OK;
+}
+
+sirius_status sirius_tree_kernel(sirius_ctx* c, const int32_t* pending, const int32_t* start_pos, int32_t gamma,
+                                 int32_t width, int32_t branch, float accept_threshold, int32_t accept_mode,
+                                 int32_t* n_accept_out, int32_t* next_token_out, int32_t* path_tokens_out) {
+  if (!c || !pending || !start_pos || !n_accept_out || !next_token_out || !path_tokens_out)
+    return SIRIUS_ERR_INVALID_ARG;
+  if (accept_mode != SIRIUS_ACCEPT_THRESHOLD && accept_mode != SIRIUS_ACCEPT_EXACT_ARGMAX)
+    return fail(c, SIRIUS_ERR_INVALID_ARG, "accept_mode");
+  if (!(accept_threshold >= 0.f && accept_threshold <= 1.f)) return fail(c, SIRIUS_ERR_INVALID_ARG, "r outside [0,1]");
+  if (gamma < 1 || width < 1 || width > kTreeMaxW || branch < 1 || branch > kTreeMaxKB)
+    return fail(c, SIRIUS_ERR_INVALID_ARG, "gamma / width / branch");
+  const int n_rows = 1 + (gamma - 1) * width;
+  if (n_rows > kTreeMaxRows || n_rows > c->cfg.max_gamma) return fail(c, SIRIUS_ERR_CAPACITY, "tree rows > max_gamma / 64");
+  if (c->cfg.batch != 1 || c->cfg.tp_size != 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "tree kernels: batch 1, TP 1");
+  OK(check_sticky(c));
+  uint32_t rbits;
+  memcpy(&rbits, &accept_threshold, 4);
+  GraphKey key = {0x7EEEu, (uintptr_t)gamma, (uintptr_t)width, (uintptr_t)branch, (uintptr_t)rbits,
+                  (uintptr_t)accept_mode, (uintptr_t)pending, (uintptr_t)start_pos, (uintptr_t)n_accept_out,
+                  (uintptr_t)next_token_out, (uintptr_t)path_tokens_out};
+  OK(run_graphed(c, key, [&] {
+    return enqueue_tree(c, pending, start_pos, gamma, width, branch, accept_threshold, accept_mode, n_accept_out,
+                        next_token_out, path_tokens_out);
+  }));
+  c->last_gamma = gamma;
+  c->have_correct = true;
+  c->tree_last = true;
   return SIRIUS_OK;
 }
 
@@ -1286,6 +1375,7 @@ static sirius_status enqueue_rewrite(sirius_ctx* c, const int32_t* start_pos, co
     a.max_seq = cf.max_seq;
     a.max_gamma = cf.max_gamma;
     a.gamma = c->last_gamma;
+    a.rows = c->tree_last ? c->tree->path : nullptr;  // tree kernel: the winning path's staging rows
     a.err = c->err_dev;
     prof_begin(c, P_REWRITE);
     LCU(launch::kv_rewrite(a, cf.n_layers, c->stream));
@@ -1300,7 +1390,7 @@ sirius_status kv_rewrite(sirius_ctx* c, const int32_t* start_pos, const int32_t*
   if (!c || !start_pos || !n_rows) return SIRIUS_ERR_INVALID_ARG;
   if (!c->have_correct) return fail(c, SIRIUS_ERR_STATE, "kv_rewrite without a preceding correct_kernel");
   OK(check_sticky(c));
-  GraphKey key = {0xE11Eu, (uintptr_t)start_pos, (uintptr_t)n_rows, (uintptr_t)c->last_gamma};
+  GraphKey key = {0xE11Eu, (uintptr_t)start_pos, (uintptr_t)n_rows, (uintptr_t)c->last_gamma, (uintptr_t)c->tree_last};
   OK(run_graphed(c, key, [&] { return enqueue_rewrite(c, start_pos, n_rows); }));
   c->have_correct = false;
   return SIRIUS_OK;

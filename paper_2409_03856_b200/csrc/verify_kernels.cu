@@ -93,8 +93,9 @@ __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
   pdl_wait();
   const int m = blockIdx.x, tid = threadIdx.x, hd = a.hd, half = hd / 2;
   const int b = a.b_base + m / a.rows_per_seq, i = m % a.rows_per_seq;
-  const int pos = a.start[b] + i;
-  const bool bad = pos < 0 || pos >= a.max_seq || (a.to_cache == 0 && i >= a.max_gamma);
+  const int pos = a.start[b] + (a.row_off ? a.row_off[i] : i);
+  const int si = a.stage_base + i;  // staging row
+  const bool bad = pos < 0 || pos >= a.max_seq || (a.to_cache == 0 && si >= a.max_gamma);
   if (bad) {
     if (tid == 0) atomicOr(a.err, 2);
     return;
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
     } else {
       const int kvh = h - a.Hr;
       uint16_t* dst = a.to_cache ? a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_seq + pos) * hd
-                                 : a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + i) * hd;
+                                 : a.k_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + si) * hd;
       *reinterpret_cast<uint2*>(dst + e) = make_uint2(pack_bf16(y0.x, y0.y), pack_bf16(y0.z, y0.w));
       *reinterpret_cast<uint2*>(dst + e + half) = make_uint2(pack_bf16(y1.x, y1.y), pack_bf16(y1.z, y1.w));
     }
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(128) rope_store_kernel(RopeStoreArgs a) {
     if (it >= v4) continue;
     const int kvh = (it * 4) / hd, e = (it * 4) % hd;
     uint16_t* dst = a.to_cache ? a.v_dst + (((size_t)b * a.KVr + kvh) * a.max_seq + pos) * hd
-                               : a.v_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + i) * hd;
+                               : a.v_dst + (((size_t)b * a.KVr + kvh) * a.max_gamma + si) * hd;
     *reinterpret_cast<uint2*>(dst + e) = make_uint2(pack_bf16(vv[j].x, vv[j].y), pack_bf16(vv[j].z, vv[j].w));
   }
   }
@@ -272,10 +273,13 @@ __global__ void __launch_bounds__(128) kv_rewrite_kernel(KvRewriteArgs a) {
   const uint4* vs = reinterpret_cast<const uint4*>(a.stage_v + hb * a.max_gamma * a.hd);
   uint4* kd = reinterpret_cast<uint4*>(a.k_cache + (hb * a.max_seq + T) * a.hd);
   uint4* vd = reinterpret_cast<uint4*>(a.v_cache + (hb * a.max_seq + T) * a.hd);
-  const int nvec = n * a.hd / 8;
+  const int rv = a.hd / 8;  // uint4 per row
+  const int nvec = n * rv;
   for (int e = threadIdx.x; e < nvec; e += 128) {
-    kd[e] = ks[e];
-    vd[e] = vs[e];
+    const int r = e / rv, c = e % rv;
+    const int src = a.rows ? a.rows[r] * rv + c : e;  // tree commit: the winning path's staging rows
+    kd[e] = ks[src];
+    vd[e] = vs[src];
   }
 }
 

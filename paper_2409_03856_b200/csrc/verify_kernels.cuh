@@ -26,7 +26,9 @@ struct RopeStoreArgs {
   const float* rope_cos;   // [max_seq, hd/2]
   const float* rope_sin;
   int Hr, KVr, hd, max_seq, max_gamma;
-  int to_cache;            // 1: K/V -> cache slots pos (prefill); 0: -> staging row i (verify)
+  int to_cache;            // 1: K/V -> cache slots pos (prefill); 0: -> staging row stage_base + i (verify)
+  int stage_base;          // staging row of the call's row 0 (tree drafting steps); 0 otherwise
+  const int32_t* row_off;  // [M] position offset of each row from start (tree rows: their step), or NULL (= i)
   float* q_out;            // [M, Hr * hd] fp32 (post-RoPE)
   uint16_t* k_dst;         // this layer's cache [B, KVr, max_seq, hd] or staging [B, KVr, max_gamma, hd]
   uint16_t* v_dst;
@@ -42,6 +44,10 @@ struct AttnRowsArgs {
   const uint16_t* k_fresh;  // staging [B, KVr, fresh_stride, hd] (ignored if fresh_in_cache)
   const uint16_t* v_fresh;
   int fresh_stride, fresh_in_cache;
+  int stage_base;                      // staging row of the call's row 0 (tree drafting steps)
+  const unsigned long long* tree_vis;  // tree rows: [64] ancestor-or-self bit masks over the staging rows
+                                       // (row i sees staging row f iff bit f of tree_vis[stage_base + i]);
+                                       // NULL: causal (row i sees staging rows [0, i])
   float* part;              // workspace
   unsigned* counters;       // unused (kept for ABI-internal layout)
   unsigned* group_bar;      // [nseq * KVr * row_blocks][2] barrier (count, generation) of the split groups
@@ -81,6 +87,7 @@ struct KvRewriteArgs {
   const int32_t* start;
   const int32_t* n_rows;
   int B, KVr, hd, max_seq, max_gamma, gamma;
+  const int32_t* rows;      // tree commit: staging row of each committed slot [gamma] (batch 1), or NULL
   int* err;
 };
 

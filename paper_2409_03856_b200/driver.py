@@ -72,6 +72,7 @@ class Driver:
         self.next_tok = torch.zeros(B, dtype=i32, device=dev)
         self.q = torch.zeros((B, gm), dtype=torch.float32, device=dev)
         self.row_am = torch.zeros((B, gm), dtype=torch.int32, device=dev)
+        self.path = torch.zeros(gm, dtype=torch.int32, device=dev)  # tree kernels: winning path tokens
         # pinned staging: out = [n_rows(B) | start(B) | pending(B) | pos(gm*B)], in = [n_accept | next | drafts]
         self.h_out = torch.zeros(3 * B + gm * B, dtype=i32).pin_memory()
         self.h_in = torch.zeros(2 * B + (gm + 1) * B, dtype=i32).pin_memory()
@@ -190,6 +191,51 @@ class Driver:
         self.need_rewrite = self.rewrite
         self.kidx += 1
         return advs[0]
+
+    def step_tree(self, gamma: int, r: float, width: int, branch: int = 3,
+                  accept_mode: int = S.ACCEPT_THRESHOLD) -> int:
+        """One tree correction kernel (sirius_tree_kernel: tree drafting + tree verification, PAPER.md:
+        299-319); batch 1.  Same host round trip as step(): the accepted count, the interleaved token and
+        the winning path's tokens come back; the commit (kv_rewrite of the path) is enqueued next time."""
+        torch = self.torch
+        assert self.B == 1 and self.rollback and self.interleave
+        self._upload(gamma)
+        d = self.d_out
+        cur = self.start[self.kidx % 2]
+        self.n_rows.copy_(d[0:1])
+        cur.copy_(d[1:2])
+        self.drafts[0].copy_(d[2:3])
+        if self.need_rewrite:
+            self.ctx.kv_rewrite(self.start[(self.kidx - 1) % 2], self.n_rows)
+        self.ctx.sirius_tree_kernel(self.drafts[0], cur, gamma, width, branch, r, accept_mode, self.n_accept,
+                                    self.next_tok, self.path)
+        n = 2 + gamma
+        self.d_in[0:1].copy_(self.n_accept)
+        self.d_in[1:2].copy_(self.next_tok)
+        self.d_in[2:n].copy_(self.path[:gamma])
+        self.h_in[:n].copy_(self.d_in[:n], non_blocking=True)
+        self.d2h_bytes += 4 * n
+        torch.cuda.current_stream().synchronize()
+        h = self.h_in.numpy()
+        j, nxt = int(h[0]), int(h[1])
+        path = h[2:n].copy()
+        self.log.append(KernelLog(list(self.T), path[None, :].copy(), np.array([j]), np.array([nxt])))
+        committed = [int(x) for x in path[1:j + 1]] + [nxt]
+        self.out[0] += committed
+        self.n_rows_h[0] = len(committed)
+        self.T[0] += len(committed)
+        self.pending[0] = committed[-1]
+        self.need_rewrite = True
+        self.kidx += 1
+        return len(committed)
+
+    def sirius_tree(self, prompts, n_tokens: int, gamma: int, r: float, width: int, branch: int = 3,
+                    accept_mode: int = S.ACCEPT_THRESHOLD) -> GenOut:
+        self.begin(prompts)
+        while len(self.out[0]) < n_tokens:
+            self.step_tree(gamma, r, width, branch, accept_mode)
+        self.flush()
+        return GenOut([o[:n_tokens] for o in self.out], list(self.log))
 
     # ------------------------------------------------------------------ whole generations
     def sirius(self, prompts, n_tokens: int, gamma: int, r: float, accept_mode: int = S.ACCEPT_THRESHOLD,

@@ -25,8 +25,8 @@ ACCEPT_EXACT_ARGMAX = 1
 
 # every symbol include/sirius.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
-               "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_destroy", "sirius_last_error",
-               "sirius_version")
+               "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_tree_kernel", "sirius_destroy",
+               "sirius_last_error", "sirius_version")
 
 
 class SiriusError(RuntimeError):
@@ -78,6 +78,8 @@ def load():
         lib.kv_rewrite.restype = I
         lib.sirius_verify_row_argmax.argtypes = [P, P]
         lib.sirius_verify_row_argmax.restype = I
+        lib.sirius_tree_kernel.argtypes = [P, P, P, I, I, I, F, I, P, P, P]
+        lib.sirius_tree_kernel.restype = I
         lib.sirius_csparse_enable.argtypes = [P, F]
         lib.sirius_csparse_enable.restype = I
         lib.sirius_debug_csparse_plan.argtypes = [P, P, P, ctypes.POINTER(I)]
@@ -192,6 +194,12 @@ class Sirius:
 
     def sirius_verify_row_argmax(self, out):
         self._check(self.lib.sirius_verify_row_argmax(self.h, _ptr(out)))
+
+    def sirius_tree_kernel(self, pending, start_pos, gamma: int, width: int, branch: int, accept_threshold: float,
+                           accept_mode: int, n_accept_out, next_token_out, path_tokens_out):
+        self._check(self.lib.sirius_tree_kernel(self.h, _ptr(pending), _ptr(start_pos), gamma, width, branch,
+                                                accept_threshold, accept_mode, _ptr(n_accept_out),
+                                                _ptr(next_token_out), _ptr(path_tokens_out)))
 
     def sirius_csparse_enable(self, keep_fraction: float):
         self._check(self.lib.sirius_csparse_enable(self.h, float(keep_fraction)))
