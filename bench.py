@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--baseline-tokens", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tree-width", type=int, default=4, help="tree kernels timed at r_alt (0: skip)")
+    ap.add_argument("--topk-keep", type=float, default=0.5, help="top-k FSparse rows (0: skip)")
     ap.add_argument("--csparse-keep", type=float, default=0.5,
                     help="CSparse (Griffin-style) keep fraction for the csparse rows (0: skip)")
     return ap.parse_args()
@@ -372,6 +373,35 @@ def main():
                         "all FFN rows, ancestor-masked attention): ~a verify pass per step"}
         del dt, ctx_t
         torch.cuda.empty_cache()
+    # ---------------- top-k FSparse (the paper's own FSparse, PAPER.md:121 footnote): Sirius and sparse-only
+    tk = None
+    if a.topk_keep > 0 and tp == 1 and B <= 4:
+        ctx.sirius_topk_enable(a.topk_keep)
+        dk = driver.Driver(ctx, topk=True)
+        dk.begin(prompts)
+        for _ in range(a.warmup):
+            dk.step(a.gamma, a.r)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            dk.step(a.gamma, a.r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_k = max_over_ranks(e0.elapsed_time(e1))
+        adv_k = [int(k.j[0]) + 1 for k in dk.log[a.warmup:a.warmup + a.steps]]
+        dk.flush()
+        Tk = [t + 8 for t in dk.T]
+        dk.greedy_run(dk.pending, Tk, a.gamma, False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dk.greedy_run(dk.pending, Tk, a.baseline_tokens, False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tk = {"keep": a.topk_keep, "sirius_ms_per_token": t_k / sum(adv_k), "aal": sum(adv_k) / a.steps,
+              "sparse_only_ms_per_token": max_over_ranks(e0.elapsed_time(e1)) / a.baseline_tokens}
+        ctx.sirius_topk_enable(0.0)
     # ---------------- CSparse (Griffin-style, the sparse model of the paper's latency tables):
     # the same context with the prompt's fixed neuron set; Sirius over the CSparse draft model, and
     # CSparse-only greedy decode
@@ -506,6 +536,7 @@ def main():
             "sirius_r_alt": alt,
             "csparse": csp,
             "tree": tree,
+            "topk_fsparse": tk,
             "latency_model": model,
             "roofline": roof, "per_kernel_device_ms": per_kernel,
             "cpu_baseline": cpu,

@@ -17,6 +17,7 @@
  *
  *   sirius_csparse_enable — CSparse draft model: the prompt's fixed neuron set
  *   sirius_tree_kernel  — tree building + tree verification of one kernel
+ *   sirius_topk_enable  — top-k FSparse draft model (PAPER.md:121 footnote)
  *   sirius_destroy / sirius_last_error
  *
  * Conventions (all entry points):
@@ -96,8 +97,10 @@ typedef struct {
 /* sparse_decode_step flags */
 enum {
   SIRIUS_DENSE = 1u,  /* run M_F (dense FFN) instead of M_S                                            */
-  SIRIUS_CSPARSE = 2u /* run M_S as the CSparse model: the FFN restricted to the last prompt's neuron
-                         plan (sirius_csparse_enable), instead of CATS      */
+  SIRIUS_CSPARSE = 2u, /* run M_S as the CSparse model: the FFN restricted to the last prompt's neuron
+                          plan (sirius_csparse_enable), instead of CATS     */
+  SIRIUS_TOPK = 4u     /* run M_S as the top-k FSparse model (sirius_topk_enable; PAPER.md:121 footnote
+                          "topk on the Gate Layer activations"), instead of the CATS threshold       */
 };
 
 /* correct_kernel accept modes */
@@ -199,6 +202,16 @@ sirius_status kv_rewrite(sirius_ctx* ctx, const int32_t* start_pos, const int32_
 sirius_status sirius_tree_kernel(sirius_ctx* ctx, const int32_t* pending, const int32_t* start_pos, int32_t gamma,
                                  int32_t width, int32_t branch, float accept_threshold, int32_t accept_mode,
                                  int32_t* n_accept_out, int32_t* next_token_out, int32_t* path_tokens_out);
+
+/* Top-k FSparse (PAPER.md:121 footnote: the paper's own FSparse "uses topk on the
+ * Gate Layer activations"; reading D30): sparse_decode_step(..., SIRIUS_TOPK) keeps, per layer and
+ * sequence, the k = round(keep_fraction * ffn) neurons of largest |SiLU(g)| (exact ties to the lower
+ * index) — gate GEMV, exact radix selection, then only the selected W_up / W_down rows.  Unlike the
+ * threshold the set depends on the whole layer, so TP > 1 would need a global selection: TP 1 only.
+ * keep_fraction 0 disables.
+ * Errors: INVALID_ARG (keep_fraction outside [0, 1]); UNSUPPORTED (tp_size > 1, batch >= 8, k = 0);
+ * CUDA (allocation).  Synchronous. */
+sirius_status sirius_topk_enable(sirius_ctx* ctx, float keep_fraction);
 
 /* CSparse / Griffin-style coarse-grained sparsity (§2.1 "within the
  * same input prompt, the sparsity pattern is fixed for all tokens generated", :182 §3.2 the pattern is

@@ -211,6 +211,16 @@ void mlp_block(Oracle* o, int l, double* x, int sparse, double t, double* gate_o
     mask[i] = plan ? plan[i] : ((!sparse || std::fabs(a[i]) >= t) ? 1 : 0);
     cnt += mask[i];
   }
+  if (sparse == 3) {  // top-k FSparse (PAPER.md:121 footnote "topk on the Gate Layer activations"): t is
+                      // the keep fraction; the k = round(t * ffn) largest |a|, exact ties to the lower index
+    const int k = (int)std::floor(t * F + 0.5);
+    std::vector<int> order(F);
+    for (int i = 0; i < F; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return std::fabs(a[x]) > std::fabs(a[y]); });
+    std::fill(mask.begin(), mask.end(), 0);
+    for (int r = 0; r < k; ++r) mask[order[r]] = 1;
+    cnt = k;
+  }
   const uint16_t* Wu = o->wup[l];
   parallel_rows(F, o->threads, [&](int i) {
     if (!mask[i]) return;
@@ -281,7 +291,8 @@ void oracle_set_layer(void* h, int l, const uint16_t* attn_norm, const uint16_t*
 }
 
 // Full row forward.  sparse: 0 = dense model M_F, 1 = CATS sparse model M_S (thresholds[L], fp32),
-// 2 = CSparse model M_S with the fixed neuron plan[L*ffn] (1 = kept).
+// 2 = CSparse model M_S with the fixed neuron plan[L*ffn] (1 = kept), 3 = top-k FSparse model M_S
+// (thresholds[L] = keep fraction per layer).
 // stage_row < 0: write K/V to cache slot pos; >= 0: write to staging row stage_row (verify).
 // logits: [vocab] fp64 or NULL.  gate_out: [L*ffn] a = SiLU(g) or NULL.  mask_out: [L*ffn] or NULL.
 // n_active: [L] or NULL.  x_out: [d] final residual (pre final-norm) or NULL.
@@ -296,7 +307,7 @@ void oracle_forward_row(void* h, int tok, int pos, int sparse, const float* thre
   for (int k = 0; k < d; ++k) x[k] = bf16_value(o->embed[(size_t)tok * d + k]);  // x = E[tok]
   for (int l = 0; l < o->L; ++l) {
     attention_block(o, l, x.data(), pos, stage_row, false, tree_vis, tree_n_cache);
-    mlp_block(o, l, x.data(), sparse, sparse == 1 ? (double)thresholds[l] : 0.0,
+    mlp_block(o, l, x.data(), sparse, (sparse == 1 || sparse == 3) ? (double)thresholds[l] : 0.0,
               gate_out ? gate_out + (size_t)l * o->ffn : nullptr, mask_out ? mask_out + (size_t)l * o->ffn : nullptr,
               n_active ? n_active + l : nullptr, sparse == 2 ? plan + (size_t)l * o->ffn : nullptr);
   }
@@ -326,7 +337,8 @@ void oracle_prefill_kv_row(void* h, int tok, int pos) {
 // Layer-isolated MLP (kernel-level parity at full shapes): x[d] in/out.  sparse 2: plan[ffn] (CSparse).
 void oracle_mlp(void* h, int l, double* x, int sparse, float threshold, double* gate_out, uint8_t* mask_out,
                 int* n_active, const uint8_t* plan) {
-  mlp_block((Oracle*)h, l, x, sparse, sparse == 1 ? (double)threshold : 0.0, gate_out, mask_out, n_active,
+  mlp_block((Oracle*)h, l, x, sparse, (sparse == 1 || sparse == 3) ? (double)threshold : 0.0, gate_out, mask_out,
+            n_active,
             sparse == 2 ? plan : nullptr);
 }
 

@@ -114,9 +114,11 @@ class OracleModel:
     # ------------------------------------------------------------ one row
     def forward_row(self, tok: int, pos: int, sparse: bool = False, thresholds: Optional[np.ndarray] = None,
                     stage_row: int = -1, want_gate: bool = False, want_mask: bool = False,
-                    plan: Optional[np.ndarray] = None, tree_vis: int = 0, tree_n_cache: int = 0) -> RowOut:
-        """sparse with plan (uint8 [L, ffn], csparse_plan): the CSparse model; sparse with thresholds:
-        the CATS (FSparse) model; else the dense model."""
+                    plan: Optional[np.ndarray] = None, tree_vis: int = 0, tree_n_cache: int = 0,
+                    topk: Optional[np.ndarray] = None) -> RowOut:
+        """sparse with plan (uint8 [L, ffn], csparse_plan): the CSparse model; sparse with topk (keep
+        fraction per layer): the top-k FSparse model (reading D30); sparse with thresholds: the CATS
+        (FSparse) model; else the dense model."""
         cfg = self.cfg
         assert 0 <= tok < cfg.vocab and 0 <= pos < self.max_seq
         assert stage_row < self.max_gamma
@@ -126,7 +128,11 @@ class OracleModel:
         nact = np.empty(cfg.n_layers, dtype=np.int32)
         thr = pl = None
         mode = 0
-        if sparse and plan is not None:
+        if sparse and topk is not None:
+            thr = np.ascontiguousarray(topk, dtype=np.float32)
+            assert thr.shape == (cfg.n_layers,)
+            mode = 3
+        elif sparse and plan is not None:
             pl = np.ascontiguousarray(plan, dtype=np.uint8)
             assert pl.shape == (cfg.n_layers, cfg.ffn_dim)
             mode = 2
@@ -139,7 +145,8 @@ class OracleModel:
                                   int(tree_vis), int(tree_n_cache))
         return RowOut(logits, gate, mask, nact)
 
-    def mlp(self, layer: int, x: np.ndarray, sparse: bool, threshold: float = 0.0, plan: Optional[np.ndarray] = None):
+    def mlp(self, layer: int, x: np.ndarray, sparse: bool, threshold: float = 0.0, plan: Optional[np.ndarray] = None,
+            topk: Optional[float] = None):
         """Layer-isolated MLP on residual x (fp64 [d]); returns (x_out, a, mask, n_active).  With plan
         (uint8 [ffn]) the CSparse MLP of that neuron set."""
         cfg = self.cfg
@@ -148,8 +155,9 @@ class OracleModel:
         mask = np.empty(cfg.ffn_dim, dtype=np.uint8)
         n = np.empty(1, dtype=np.int32)
         pl = None if plan is None else np.ascontiguousarray(plan, dtype=np.uint8)
-        mode = 2 if (sparse and pl is not None) else (1 if sparse else 0)
-        _lib().oracle_mlp(self.h, layer, _ptr(xx), mode, float(threshold), _ptr(gate), _ptr(mask), _ptr(n), _ptr(pl))
+        mode = 3 if (sparse and topk is not None) else (2 if (sparse and pl is not None) else (1 if sparse else 0))
+        _lib().oracle_mlp(self.h, layer, _ptr(xx), mode, float(topk if mode == 3 else threshold), _ptr(gate),
+                          _ptr(mask), _ptr(n), _ptr(pl))
         return xx, gate, mask, int(n[0])
 
     def kv_rewrite(self, T: int, n: int) -> None:
@@ -389,7 +397,7 @@ class GenerateResult:
 def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: int, r: float,
              thresholds: Optional[np.ndarray], accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True,
              interleave: bool = True, rollback: bool = True, csparse_keep: Optional[float] = None,
-             tree_width: Optional[int] = None, tree_branch: int = 3) -> GenerateResult:
+             tree_width: Optional[int] = None, tree_branch: int = 3, topk_keep: Optional[float] = None) -> GenerateResult:
     """The Sirius loop, Algorithm 1, readings D5-D18:
       * dense prefill of the prompt; the first generated token is the dense argmax (D17);
       * kernel size n = gamma: the sparse model drafts gamma-1 tokens after the pending token,
@@ -413,7 +421,9 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
     neuron plan of the prompt (prefill_stats + csparse_plan, reading D28) fixed for the generation.
 
     tree_width: hardware-friendly tree building and verification (tree_kernel)
-    instead of the greedy chain; width 1 is the chain (pinned bitwise)."""
+    instead of the greedy chain; width 1 is the chain (pinned bitwise).
+
+    topk_keep: the sparse model is top-k FSparse (PAPER.md:121 footnote, reading D30) instead of CATS."""
     assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
     P = len(prompt)
     assert P + n_tokens + gamma <= model.max_seq and gamma >= 1
@@ -429,6 +439,7 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
     T = P
     res = GenerateResult(out)
     res.plan = plan
+    topk = None if topk_keep is None else np.full(model.cfg.n_layers, topk_keep, dtype=np.float32)
     while len(out) < n_tokens and tree_width is not None:
         assert rewrite and interleave and rollback, "tree kernels run with every correction component"
         tk = tree_kernel(model, out[-1], T, gamma, r, thresholds, tree_width, tree_branch, accept_mode, plan)
@@ -441,7 +452,7 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
         ins = [out[-1]]
         nact, dmarg = [], []
         for i in range(gamma - 1):  # sparse drafting, greedy (D13)
-            row = model.decode(ins[i], T + i, True, thresholds, plan=plan)
+            row = model.decode(ins[i], T + i, True, thresholds, plan=plan, topk=topk)
             nact.append(row.n_active)
             dmarg.append(top2_margin(row.logits))
             ins.append(argmax_lowest(row.logits))

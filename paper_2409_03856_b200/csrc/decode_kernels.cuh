@@ -60,6 +60,11 @@ struct FfnArgs {
   long long gate_stride;
   int atomic_out;          // 1: partials added into out (pre-zeroed) with float4 atomics, no grid barrier
   unsigned long long* trace;  // debug: [8][1024] %globaltimer stamps per CTA (phase boundaries), or NULL
+  // precomputed-gate mode (top-k FSparse, topk.cu): a = SiLU(g) [B, a_ld] and the selected set as bits
+  // [B, m_ld] words come in; no gate rows are read and the threshold is not applied
+  const float* a_in;
+  const unsigned* mask_in;
+  long long a_ld, m_ld;
 };
 
 

@@ -157,15 +157,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
 
   const uint64_t pol = policy_evict_first();
   RowRegs<CPL> pf;  // first gate row of the warp, requested before the activation prologue
-  row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn, pol);
+  row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn && !a.a_in, pol);
   constexpr int MG = CPL * 2 / NW > 0 ? CPL * 2 / NW : 1;  // prologue float4 groups per thread (d = 256 CPL)
   prologue<B, MG>(a.pro, d, h_s, red_s, cta == 0);
   fstamp(a, 1);
   const float4* hp = reinterpret_cast<const float4*>(h_s);
   const float t = a.dense ? 0.f : *a.threshold;
 
-  // ---- A: dense gate rows: g = h2 . W_gate[n];  a = SiLU(g)
-  for (int i = warp; i < nn; i += kFfnWarps) {
+  // ---- A: dense gate rows: g = h2 . W_gate[n];  a = SiLU(g)  (precomputed-gate mode: loaded)
+  if (a.a_in) {
+    for (int i = tid; i < nn; i += NT)
+#pragma unroll
+      for (int b = 0; b < B; ++b) a_s[b][i] = __ldcg(a.a_in + (size_t)b * a.a_ld + n0 + i);
+  }
+  for (int i = warp; i < nn && !a.a_in; i += kFfnWarps) {
     float acc[B];
     row_finish<B, CPL>(pf, a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc);
     row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + i + kFfnWarps) * d + after_all<B>(acc), CH, lane, i + kFfnWarps < nn,
@@ -186,7 +191,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float av = valid ? a_s[b][i] : 0.f;
-      const bool on = valid && (a.dense || fabsf(av) >= t);
+      bool sel = fabsf(av) >= t;
+      if (a.mask_in && valid) sel = (__ldcg(a.mask_in + (size_t)b * a.m_ld + ((n0 + i) >> 5)) >> ((n0 + i) & 31)) & 1u;
+      const bool on = valid && (a.dense || sel);
       const unsigned mb = __ballot_sync(0xffffffffu, on);
       um |= mb;
       if (lane == 0) act_s[warp][b] = mb;

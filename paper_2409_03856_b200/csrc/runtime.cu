@@ -35,6 +35,8 @@ extern int g_gemm_coarse;
 cudaError_t attn_stage(const StepArgs& a, int l, int B, cudaStream_t st);
 cudaError_t csparse_colsum(const float* a, int M, int F, long long lda, float* stats, cudaStream_t st);
 cudaError_t csparse_select(const float* stats, int L, int F, int k, int32_t* idx, cudaStream_t st);
+cudaError_t topk_select(const float* g, long long ldg, int F, int k, float* a_out, long long lda, unsigned* mask,
+                        long long ldm, int B, cudaStream_t st);
 cudaError_t csparse_gather(const uint16_t* src, const int32_t* idx, int k, int d, uint16_t* dst, int num_sms,
                            cudaStream_t st);
 }  // namespace launch
@@ -106,6 +108,8 @@ struct RankState {
   // CSparse (csparse.cu): prompt statistic [L][Fr], the plan [L][k], a-export of a prefill chunk
   // [MAXM][Fr], compact weights [3][L][k][d] (gate, up, down rows of the kept neurons)
   float *cs_stats = nullptr, *cs_scratch = nullptr;
+  float *tk_g = nullptr, *tk_a = nullptr;  // top-k FSparse (topk.cu): gate pre-activations, a [B][Fr]
+  unsigned* tk_mask = nullptr;             // selected set [B][Fr/32 + 1] bits
   int32_t* cs_idx = nullptr;
   uint16_t* cs_w = nullptr;
 };
@@ -115,6 +119,7 @@ struct sirius_ctx {
   int nranks = 1;  // ranks run by this context (tp_size when emulating, else 1)
   bool emulated = false;
   float cs_keep = 0.f;   // CSparse keep fraction (sirius_csparse_enable); 0 = off
+  int topk_k = 0;        // top-k FSparse: neurons kept per layer (sirius_topk_enable); 0 = off
   int cs_k = 0;          // neurons kept per layer (this rank's shard)
   bool cs_ready = false; // the plan of the last prefill is built
   bool stub_comm = false;  // SIRIUS_DEBUG_STUB_COMM: tp_size > 1 on one GPU with every collective skipped
@@ -375,13 +380,36 @@ sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev,
   return SIRIUS_OK;
 }
 
+sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B);
+
 // ---- the decode CATS FFN of layer l (S4-S6) on residual rows base (+ delta): out = the FFN's
 // contribution to the residual (accumulated into out, which the O-proj GEMV zeroed, in atomic mode)
 sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float* base, const float* delta,
                                 float* res_out, float* out, bool dense, int32_t* n_active_out, int n_active_stride,
-                                float* gate_out, long long gate_stride, bool csparse = false) {
+                                float* gate_out, long long gate_stride, bool csparse = false, bool topk = false) {
   const sirius_config& cf = c->cfg;
   FfnArgs f = {};
+  if (topk) {  // gate GEMV -> exact top-k selection (topk.cu) -> the FFN kernel in precomputed-gate mode
+    GemvArgs gv = {};
+    gv.pro.mode = IN_RESID;
+    gv.pro.base = base;
+    gv.pro.delta = delta;
+    gv.pro.norm_w = R.ffn_norm[l];
+    gv.pro.eps = cf.rms_eps;
+    gv.W = R.w_gate[l];
+    gv.rows = c->Fr;
+    gv.K = cf.d_model;
+    gv.epi = EPI_STORE;
+    gv.out = R.tk_g;
+    gv.ldo = c->Fr;
+    OK(run_gemv(c, gv, cf.batch));
+    const long long mw = c->Fr / 32 + 1;
+    LCU(launch::topk_select(R.tk_g, c->Fr, c->Fr, c->topk_k, R.tk_a, c->Fr, R.tk_mask, mw, cf.batch, c->stream));
+    f.a_in = R.tk_a;
+    f.mask_in = R.tk_mask;
+    f.a_ld = c->Fr;
+    f.m_ld = mw;
+  }
   f.pro.mode = IN_RESID;
   f.pro.base = base;
   f.pro.delta = delta;
@@ -914,6 +942,30 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
   return SIRIUS_OK;
 }
 
+// Top-k FSparse (PAPER.md:121 footnote): SIRIUS_TOPK decode steps keep, per layer
+// and sequence, the k = round(keep_fraction * ffn) neurons of largest |SiLU(g)| (reading D30).
+sirius_status sirius_topk_enable(sirius_ctx* c, float keep_fraction) {
+  if (!c || !(keep_fraction >= 0.f && keep_fraction <= 1.f)) return SIRIUS_ERR_INVALID_ARG;
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  if (keep_fraction == 0.f) {
+    c->topk_k = 0;
+    return SIRIUS_OK;
+  }
+  if (cf.tp_size != 1 || c->decode_rows)
+    return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: TP 1 and the per-stage decode path (batch <= 4)");
+  const int k = (int)std::floor((double)keep_fraction * c->Fr + 0.5);
+  if (k < 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: keep_fraction * ffn rounds to 0");
+  for (auto& R : c->ranks) {
+    if (R.tk_g) continue;
+    if (alloc(c, &R.tk_g, (size_t)cf.batch * c->Fr) || alloc(c, &R.tk_a, (size_t)cf.batch * c->Fr) ||
+        alloc(c, &R.tk_mask, (size_t)cf.batch * (c->Fr / 32 + 1)))
+      return SIRIUS_ERR_CUDA;
+  }
+  c->topk_k = k;
+  return SIRIUS_OK;
+}
+
 // CSparse: allocate the plan and the compact weights; every later sirius_prefill
 // gathers the statistic and builds the plan (reading D28); SIRIUS_CSPARSE decode steps use it.
 sirius_status sirius_csparse_enable(sirius_ctx* c, float keep_fraction) {
@@ -983,10 +1035,11 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
   const int B = cf.batch, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
   const bool dense = flags & SIRIUS_DENSE;
   const bool csparse = flags & SIRIUS_CSPARSE;
+  const bool topk = flags & SIRIUS_TOPK;
   if (c->decode_rows) return enqueue_decode_rows(c, token_in, pos, dense, token_out, logits_out, n_active_out,
                                                  gate_act_out);
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
-  if (c->use_step && !csparse) {  // the whole step in one persistent launch (decode_step.cu)
+  if (c->use_step && !csparse && !topk) {  // the whole step in one persistent launch (decode_step.cu)
     RankState& R = c->ranks[0];
     StepArgs s = {};
     s.d = d;
@@ -1123,7 +1176,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       }
       prof_begin(c, P_FFN);
       OK(launch_decode_ffn(c, R, l, R.resA, R.dA, R.resB, R.dF, dense, n_active_out ? n_active_out + l : nullptr, L,
-                           g_out, g_stride, csparse));
+                           g_out, g_stride, csparse, topk));
       prof_end(c);
     }
     OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
@@ -1165,8 +1218,11 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
 sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const int32_t* pos, uint32_t flags,
                                  int32_t* token_out, float* logits_out, int32_t* n_active_out, float* gate_act_out) {
   if (!c || !token_in || !pos || !token_out) return SIRIUS_ERR_INVALID_ARG;
-  if (flags & ~(uint32_t)(SIRIUS_DENSE | SIRIUS_CSPARSE)) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
-  if ((flags & SIRIUS_CSPARSE) && (flags & SIRIUS_DENSE)) return fail(c, SIRIUS_ERR_INVALID_ARG, "CSPARSE with DENSE");
+  if (flags & ~(uint32_t)(SIRIUS_DENSE | SIRIUS_CSPARSE | SIRIUS_TOPK)) return fail(c, SIRIUS_ERR_INVALID_ARG, "unknown flag");
+  if (__builtin_popcount(flags & (SIRIUS_DENSE | SIRIUS_CSPARSE | SIRIUS_TOPK)) > 1)
+    return fail(c, SIRIUS_ERR_INVALID_ARG, "DENSE, CSPARSE and TOPK are exclusive");
+  if ((flags & SIRIUS_TOPK) && !c->topk_k)
+    return fail(c, SIRIUS_ERR_STATE, "TOPK decode without sirius_topk_enable");
   if ((flags & SIRIUS_CSPARSE) && gate_act_out) return fail(c, SIRIUS_ERR_INVALID_ARG, "CSPARSE exports no gate");
   OK(check_sticky(c));
   if ((flags & SIRIUS_CSPARSE) && !c->cs_ready)

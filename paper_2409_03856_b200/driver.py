@@ -51,13 +51,14 @@ class GenOut:
 
 class Driver:
     def __init__(self, ctx: S.Sirius, rewrite: bool = True, interleave: bool = True, rollback: bool = True,
-                 csparse: bool = False):
+                 csparse: bool = False, topk: bool = False):
         """csparse: the draft model M_S is the CSparse model of the prompt (sirius_csparse_enable must
-        have been called on ctx; the plan is built by every begin()) instead of CATS."""
+        have been called on ctx; the plan is built by every begin()) instead of CATS; topk: the top-k
+        FSparse model (sirius_topk_enable)."""
         import torch
         assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
         self.rewrite, self.interleave, self.rollback = rewrite, interleave, rollback
-        self.sparse_flags = S.SIRIUS_CSPARSE if csparse else 0
+        self.sparse_flags = S.SIRIUS_CSPARSE if csparse else (S.SIRIUS_TOPK if topk else 0)
         self.ctx, self.torch = ctx, torch
         B, gm = ctx.batch, ctx.max_gamma
         dev = "cuda"

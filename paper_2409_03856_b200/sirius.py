@@ -20,12 +20,14 @@ SIRIUS_ERR_CUDA, SIRIUS_ERR_NCCL, SIRIUS_ERR_UNSUPPORTED = -4, -5, -6
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "CAPACITY", -3: "STATE", -4: "CUDA", -5: "NCCL", -6: "UNSUPPORTED"}
 SIRIUS_DENSE = 1
 SIRIUS_CSPARSE = 2
+SIRIUS_TOPK = 4
 ACCEPT_THRESHOLD = 0
 ACCEPT_EXACT_ARGMAX = 1
 
 # every symbol include/sirius.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
-               "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_tree_kernel", "sirius_destroy",
+               "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_tree_kernel", "sirius_topk_enable",
+               "sirius_destroy",
                "sirius_last_error", "sirius_version")
 
 
@@ -80,6 +82,8 @@ def load():
         lib.sirius_verify_row_argmax.restype = I
         lib.sirius_tree_kernel.argtypes = [P, P, P, I, I, I, F, I, P, P, P]
         lib.sirius_tree_kernel.restype = I
+        lib.sirius_topk_enable.argtypes = [P, F]
+        lib.sirius_topk_enable.restype = I
         lib.sirius_csparse_enable.argtypes = [P, F]
         lib.sirius_csparse_enable.restype = I
         lib.sirius_debug_csparse_plan.argtypes = [P, P, P, ctypes.POINTER(I)]
@@ -200,6 +204,9 @@ class Sirius:
         self._check(self.lib.sirius_tree_kernel(self.h, _ptr(pending), _ptr(start_pos), gamma, width, branch,
                                                 accept_threshold, accept_mode, _ptr(n_accept_out),
                                                 _ptr(next_token_out), _ptr(path_tokens_out)))
+
+    def sirius_topk_enable(self, keep_fraction: float):
+        self._check(self.lib.sirius_topk_enable(self.h, float(keep_fraction)))
 
     def sirius_csparse_enable(self, keep_fraction: float):
         self._check(self.lib.sirius_csparse_enable(self.h, float(keep_fraction)))

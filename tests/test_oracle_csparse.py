@@ -112,3 +112,41 @@ def test_csparse_sirius_generate_accounting(tiny):
                      accept_mode=so.ACCEPT_EXACT_ARGMAX, csparse_keep=0.5)
     dense = so.greedy_decode(so.OracleModel(cfg, w, max_seq=128), prompt, 20)
     assert ex.tokens == dense
+
+
+# ------------------------------------------------------------------ top-k FSparse
+def test_topk_fsparse_mlp_brute_force(tiny):
+    """Top-k FSparse (PAPER.md:121 footnote "topk on the Gate Layer activations", reading D30): exactly
+    round(keep * ffn) neurons, the largest |SiLU(g)| with exact ties to the lower index (pure-Python
+    sort of the oracle's own exported a), and the MLP equals the dense MLP with the other up/down rows
+    zeroed."""
+    cfg, w = tiny
+    m = so.OracleModel(cfg, w, max_seq=8)
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal(cfg.d_model) * 2.0
+    for keep in (0.3, 0.5):
+        for l in range(cfg.n_layers):
+            xs, a, mask, n = m.mlp(l, x, True, topk=keep)
+            k = so.csparse_keep_count(cfg.ffn_dim, keep)
+            assert n == k == int(mask.sum())
+            brute = sorted(range(cfg.ffn_dim), key=lambda i: (-abs(a[i]), i))[:k]
+            assert sorted(np.flatnonzero(mask).tolist()) == sorted(brute)
+            w2 = dict(w)
+            for name in ("w_up", "w_down"):
+                z = w[f"layers.{l}.{name}"].copy()
+                z[mask == 0] = 0
+                w2[f"layers.{l}.{name}"] = z
+            xd, _, _, _ = so.OracleModel(cfg, w2, max_seq=8).mlp(l, x, False)
+            np.testing.assert_array_equal(xs, xd)
+
+
+def test_topk_keep_one_equals_dense(tiny):
+    cfg, w = tiny
+    prompt = synth.eval_prompt(cfg, 8, 16)
+    m1, m2 = so.OracleModel(cfg, w, max_seq=32), so.OracleModel(cfg, w, max_seq=32)
+    m1.prefill(prompt)
+    m2.prefill(prompt)
+    r1 = m1.decode(3, 16, True, topk=np.ones(cfg.n_layers, dtype=np.float32), want_mask=True)
+    r2 = m2.decode(3, 16, False)
+    assert r1.mask.all()
+    np.testing.assert_array_equal(r1.logits, r2.logits)
