@@ -61,7 +61,7 @@ typedef enum {
                                   entry point polls (ncclCommGetAsyncError) before enqueuing          */
   SIRIUS_ERR_UNSUPPORTED = -6  /* shape not compiled: head_dim not in {64,128}; d_model % 256;
                                   (n_heads/tp * head_dim) % 64; (ffn_dim/tp) % 8; max_gamma > 64;
-                                  batch * max_gamma > 256; batch not in {1, 2, 4, 8, 16}            */
+                                  batch * max_gamma > 1024; batch not in {1, 2, 4, 8, 16, 32}       */
 } sirius_status;
 
 /* Model shape + runtime capacities.  Llama-3 conventions: rotate-half RoPE with base rope_theta,
@@ -70,7 +70,7 @@ typedef struct {
   int32_t vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn_dim;
   float rope_theta, rms_eps;
   int32_t batch;     /* number of sequences (slots 0..batch-1), fixed for the context's life;
-                        one of 1, 2, 4, 8, 16 (else SIRIUS_ERR_UNSUPPORTED); batch * max_gamma <= 256;
+                        one of 1, 2, 4, 8, 16, 32 (else SIRIUS_ERR_UNSUPPORTED); batch * max_gamma <= 1024;
                         batch >= 8 decodes through the tensor-core row path        */
   int32_t max_seq;   /* KV capacity per sequence (>= prompt + generated + max_gamma)              */
   int32_t max_gamma; /* max verify rows per sequence per correct_kernel call (<= 64)              */

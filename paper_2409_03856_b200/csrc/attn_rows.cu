@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
       pr[lane] = e0;
       pr[lane + 32] = e1;
       const float bs = warp_sum(e0 + e1);
+      __syncwarp();  // every lane has read m_s[r] / l_s[r] before lane 0 rewrites them
       if (lane == 0) {
         const float corr = mold == -INFINITY ? 0.f : expf(mold - mn);
         c_s[r] = corr;

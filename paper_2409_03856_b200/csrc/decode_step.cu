@@ -309,6 +309,7 @@ SIRIUS_DEV void attention_phase(const StepArgs& a, int l, StepSmem<B, HD, G>& sm
       sm.sc[g][lane] = p0v;
       sm.sc[g][lane + 32] = p1v;
       const float bs = warp_sum(p0v + p1v);
+      __syncwarp();  // every lane has read m_s[g] before lane 0 rewrites it
       if (lane == 0) {
         const float corr = mold == -INFINITY ? 0.f : expf(mold - mn);
         sm.c_s[g] = corr;
@@ -752,6 +753,7 @@ cudaError_t attn_stage_b(const StepArgs& a, int l, int B, cudaStream_t st) {
     case 4: return launch_attn_stage<4, HD, G>(a, l, st);
     case 8: return launch_attn_stage<8, HD, G>(a, l, st);
     case 16: return launch_attn_stage<16, HD, G>(a, l, st);
+    case 32: return launch_attn_stage<32, HD, G>(a, l, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -682,8 +682,9 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   if (cf.head_dim != 64 && cf.head_dim != 128) return SIRIUS_ERR_UNSUPPORTED;
   if (cf.d_model % 256 || ((cf.n_heads / cf.tp_size) * cf.head_dim) % 64 || (cf.ffn_dim / cf.tp_size) % 8)
     return SIRIUS_ERR_UNSUPPORTED;
-  if (cf.max_gamma > 64 || (long)cf.batch * cf.max_gamma > 256) return SIRIUS_ERR_UNSUPPORTED;
-  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4 && cf.batch != 8 && cf.batch != 16) return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.max_gamma > 64 || (long)cf.batch * cf.max_gamma > 1024) return SIRIUS_ERR_UNSUPPORTED;
+  if (cf.batch != 1 && cf.batch != 2 && cf.batch != 4 && cf.batch != 8 && cf.batch != 16 && cf.batch != 32)
+    return SIRIUS_ERR_UNSUPPORTED;
   for (int l = 0; l < cf.n_layers; ++l)
     if (!(cats_threshold[l] >= 0.f)) return SIRIUS_ERR_INVALID_ARG;
   const bool emulate = cf.tp_size > 1 && nccl_comm == nullptr;
@@ -702,7 +703,8 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   c->Vr = cf.vocab / cf.tp_size;
   c->G = cf.n_heads / cf.n_kv_heads;
   c->Nqkv = (c->Hr + 2 * c->KVr) * cf.head_dim;
-  c->MAXM = 256;
+  // activation rows: a verify of batch x gamma rows (GEMM launches chunk them by 128), at least 256
+  c->MAXM = std::max(256, round_up(cf.batch * cf.max_gamma, 16));
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -745,7 +747,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       alloc(c, &c->stats, (size_t)c->nranks * c->MAXM * c->accept_splits) ||
       alloc(c, &c->stats_gather, (size_t)cf.tp_size * c->MAXM * c->accept_splits) ||
       alloc(c, &c->dA_ptrs, 64) || alloc(c, &c->dF_ptrs, 64) || alloc(c, &c->pre_start, B) ||
-      alloc(c, &c->dec_nacc, B) || alloc(c, &c->row_argmax, 256) ||
+      alloc(c, &c->dec_nacc, B) || alloc(c, &c->row_argmax, c->MAXM) ||
       alloc(c, &c->scratch_tok, 64) || alloc(c, &c->tree, 1))
     return cleanup_fail(SIRIUS_ERR_CUDA);
   if (cudaHostAlloc(&c->err_host, 64, cudaHostAllocDefault) != cudaSuccess ||

@@ -288,17 +288,20 @@ def test_8b2l_tensor_parallel_emulation(l2, tp):
     gpu_script(ctx, cfg, thr, prompts, refs, 2, GAMMA)
 
 
-def test_tiny_batch8_per_sequence_sets():
-    """Batch 8 (the smallest of BASELINE configs[2]'s batch range): eight independent sequences of
-    different lengths, per-sequence positions, active sets, decisions and rewrites."""
+@pytest.mark.parametrize("batch", [8, 32])
+def test_tiny_batched_per_sequence_sets(batch):
+    """Batch 8 and 32 (the ends of BASELINE configs[2]'s batch range): independent sequences of
+    different lengths, per-sequence positions, active sets, decisions and rewrites; at batch 32 the
+    verify has 32 x 16 = 512 rows (GEMM launches of 128 rows, 512-row activation buffers)."""
     from synth import gpu as sg
     cfg = synth.TINY
     wh = synth.host_weights(cfg)
     thr = synth.layer_thresholds(cfg, 0.5)
-    prompts = [synth.eval_prompt(cfg, 10 + b, 20 + 7 * b) for b in range(8)]
-    refs = [oracle_script(cfg, wh, thr, p, 2, 8, 256) for p in prompts]
-    ctx = make_ctx(cfg, sg.device_weights(cfg), thr, 8, 256)
-    gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
+    gamma = 8 if batch == 8 else 16
+    prompts = [synth.eval_prompt(cfg, 10 + b, 20 + 7 * (b % 9)) for b in range(batch)]
+    refs = [oracle_script(cfg, wh, thr, p, 2, gamma, 256) for p in prompts]
+    ctx = make_ctx(cfg, sg.device_weights(cfg), thr, batch, 256)
+    gpu_script(ctx, cfg, thr, prompts, refs, 2, gamma)
 
 
 # ------------------------------------------------------------------ Llama-3-70B per-layer shapes
@@ -319,7 +322,7 @@ def test_70b_1l_decode_verify(tp):
     gpu_script(ctx, cfg, thr, prompts, refs, 2, 8)
 
 
-@pytest.mark.parametrize("batch", [16])
+@pytest.mark.parametrize("batch", [16, 32])
 def test_8b2l_batched_decode_rows_path(l2, batch):
     """Batched decode (batch >= 8) runs the tensor-core row path with the CATS mask in the SwiGLU
     epilogue: per-sequence logits, active sets and decisions against the oracle at 8B shapes."""
