@@ -18,6 +18,7 @@
  *   sirius_csparse_enable — CSparse draft model: the prompt's fixed neuron set
  *   sirius_tree_kernel  — tree building + tree verification of one kernel
  *   sirius_topk_enable  — top-k FSparse draft model (PAPER.md:121 footnote)
+ *   sirius_set_sampling — temperature sampling of drafted / interleaved tokens
  *   sirius_destroy / sirius_last_error
  *
  * Conventions (all entry points):
@@ -202,6 +203,19 @@ sirius_status kv_rewrite(sirius_ctx* ctx, const int32_t* start_pos, const int32_
 sirius_status sirius_tree_kernel(sirius_ctx* ctx, const int32_t* pending, const int32_t* start_pos, int32_t gamma,
                                  int32_t width, int32_t branch, float accept_threshold, int32_t accept_mode,
                                  int32_t* n_accept_out, int32_t* next_token_out, int32_t* path_tokens_out);
+
+/* Sampled decoding (Alg. 1 "sample" PAPER.md:253 / :267, "the temperature of 0.6
+ * works well" PAPER.md:296; reading D31).  temperature > 0: sparse_decode_step samples its token and
+ * correct_kernel samples the interleaved / bonus token (instead of argmax), each from softmax(l / T)
+ * of the model that produces it, by inverse CDF over the vocabulary in index order with the uniform
+ *   u = (splitmix64(seed ^ splitmix64(b * 2^32 + p)) >> 40) / 2^24
+ * keyed by the sequence b and the absolute position p of the token being placed (a counter-based
+ * generator: the same (seed, b, p) always draws the same u).  The acceptance probability q keeps
+ * temperature 1 (reading D12); the prefill's first token stays greedy (reading D17).  temperature 0
+ * (default) restores greedy decoding.  The decode of a context with sampling never takes the
+ * persistent step kernel.
+ * Errors: INVALID_ARG (temperature < 0 or not finite); UNSUPPORTED (tp_size > 1).  Synchronous. */
+sirius_status sirius_set_sampling(sirius_ctx* ctx, float temperature, uint64_t seed);
 
 /* Top-k FSparse (PAPER.md:121 footnote: the paper's own FSparse "uses topk on the
  * Gate Layer activations"; reading D30): sparse_decode_step(..., SIRIUS_TOPK) keeps, per layer and

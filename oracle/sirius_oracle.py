@@ -235,6 +235,43 @@ def csparse_plan(stats: np.ndarray, keep: float) -> np.ndarray:
     return plan
 
 
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x: int) -> int:
+    """SplitMix64 output function of state x (Steele, Lea, Flood 2014): the counter-based generator of
+    the sampled tokens (reading D31)."""
+    z = (x + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def sample_uniform(seed: int, b: int, p: int) -> float:
+    """u for the token placed at absolute position p of sequence b: 24 bits, exact in fp32."""
+    return float(splitmix64((seed ^ splitmix64(((b << 32) + p) & _M64)) & _M64) >> 40) / 16777216.0
+
+
+def sample_token(l: np.ndarray, temperature: float, u: float) -> int:
+    """Inverse CDF of softmax(l / temperature) in index order (PAPER.md:253, :267 'sample'; reading
+    D31): the smallest v with sum_{w <= v} e_w > u Z, e_w = exp((l_w - max l) / T)."""
+    e = np.exp((l - l.max()) / temperature)
+    c = np.cumsum(e)
+    v = int(np.searchsorted(c, u * c[-1], side="right"))
+    if v >= l.size:
+        v = int(np.flatnonzero(e > 0)[-1])
+    return v
+
+
+def sample_margin(l: np.ndarray, temperature: float, u: float) -> float:
+    """Relative distance of u Z to the nearest CDF boundary (ambiguity of a sampled token under float
+    error, the sampling analogue of the top-2 margin)."""
+    e = np.exp((l - l.max()) / temperature)
+    c = np.cumsum(e)
+    t = u * c[-1]
+    return float(np.min(np.abs(c - t)) / c[-1])
+
+
 def top2_margin(l: np.ndarray) -> float:
     """Largest minus second-largest logit (0 on an exact tie): how far the argmax is from flipping."""
     s = np.partition(l, -2)[-2:]
@@ -397,7 +434,8 @@ class GenerateResult:
 def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: int, r: float,
              thresholds: Optional[np.ndarray], accept_mode: int = ACCEPT_THRESHOLD, rewrite: bool = True,
              interleave: bool = True, rollback: bool = True, csparse_keep: Optional[float] = None,
-             tree_width: Optional[int] = None, tree_branch: int = 3, topk_keep: Optional[float] = None) -> GenerateResult:
+             tree_width: Optional[int] = None, tree_branch: int = 3, topk_keep: Optional[float] = None,
+             temperature: float = 0.0, seed: int = 0) -> GenerateResult:
     """The Sirius loop, Algorithm 1, readings D5-D18:
       * dense prefill of the prompt; the first generated token is the dense argmax (D17);
       * kernel size n = gamma: the sparse model drafts gamma-1 tokens after the pending token,
@@ -423,7 +461,14 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
     tree_width: hardware-friendly tree building and verification (tree_kernel)
     instead of the greedy chain; width 1 is the chain (pinned bitwise).
 
-    topk_keep: the sparse model is top-k FSparse (PAPER.md:121 footnote, reading D30) instead of CATS."""
+    topk_keep: the sparse model is top-k FSparse (PAPER.md:121 footnote, reading D30) instead of CATS.
+
+    temperature > 0: every drafted token and every interleaved / bonus token is sampled (sample_token,
+    uniform sample_uniform(seed, 0, position of the token)) instead of argmax (reading D31); the
+    acceptance q keeps temperature 1."""
+
+    def pick(l, pos):
+        return argmax_lowest(l) if temperature <= 0 else sample_token(l, temperature, sample_uniform(seed, 0, pos))
     assert interleave or not rollback, "rollback without interleave is not a Sirius configuration (Table 4)"
     P = len(prompt)
     assert P + n_tokens + gamma <= model.max_seq and gamma >= 1
@@ -454,13 +499,14 @@ def generate(model: OracleModel, prompt: Sequence[int], n_tokens: int, gamma: in
         for i in range(gamma - 1):  # sparse drafting, greedy (D13)
             row = model.decode(ins[i], T + i, True, thresholds, plan=plan, topk=topk)
             nact.append(row.n_active)
-            dmarg.append(top2_margin(row.logits))
-            ins.append(argmax_lowest(row.logits))
+            dmarg.append(top2_margin(row.logits) if temperature <= 0 else
+                         sample_margin(row.logits, temperature, sample_uniform(seed, 0, T + i + 1)))
+            ins.append(pick(row.logits, T + i + 1))
         lf = model.verify(ins, T)  # full model over the kernel, K/V -> staging
         j, q = accept_scan(lf, ins, r, accept_mode)
         if rollback:
             adv = j + 1
-            nxt = argmax_lowest(lf[j])
+            nxt = pick(lf[j], T + j + 1)
             committed = ins[1:j + 1] + [nxt]
         else:  # no rollback: every position is committed; rejected drafts interleaved (or kept)
             adv = gamma

@@ -37,6 +37,9 @@ cudaError_t csparse_colsum(const float* a, int M, int F, long long lda, float* s
 cudaError_t csparse_select(const float* stats, int L, int F, int k, int32_t* idx, cudaStream_t st);
 cudaError_t topk_select(const float* g, long long ldg, int F, int k, float* a_out, long long lda, unsigned* mask,
                         long long ldm, int B, cudaStream_t st);
+cudaError_t sample_tokens(const float* logits, int ldl, int V, float temperature, unsigned long long seed,
+                          const int32_t* base_pos, const int32_t* jsel, int rows_per_b, int32_t* out, int B,
+                          cudaStream_t st);
 cudaError_t csparse_gather(const uint16_t* src, const int32_t* idx, int k, int d, uint16_t* dst, int num_sms,
                            cudaStream_t st);
 }  // namespace launch
@@ -120,6 +123,8 @@ struct sirius_ctx {
   bool emulated = false;
   float cs_keep = 0.f;   // CSparse keep fraction (sirius_csparse_enable); 0 = off
   int topk_k = 0;        // top-k FSparse: neurons kept per layer (sirius_topk_enable); 0 = off
+  float samp_temp = 0.f; // sampling temperature of drafted / interleaved tokens (sirius_set_sampling); 0 = greedy
+  unsigned long long samp_seed = 0ull;
   int cs_k = 0;          // neurons kept per layer (this rank's shard)
   bool cs_ready = false; // the plan of the last prefill is built
   bool stub_comm = false;  // SIRIUS_DEBUG_STUB_COMM: tp_size > 1 on one GPU with every collective skipped
@@ -944,6 +949,17 @@ sirius_status sirius_prefill(sirius_ctx* c, const int32_t* tokens, const int32_t
   return SIRIUS_OK;
 }
 
+// Sampled decoding (reading D31): temperature > 0 makes
+// sparse_decode_step sample its token and correct_kernel sample the interleaved / bonus token.
+sirius_status sirius_set_sampling(sirius_ctx* c, float temperature, uint64_t seed) {
+  if (!c || !(temperature >= 0.f) || !std::isfinite(temperature)) return SIRIUS_ERR_INVALID_ARG;
+  OK(check_sticky(c));
+  if (temperature > 0.f && c->cfg.tp_size != 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "sampling: TP 1 only");
+  c->samp_temp = temperature;
+  c->samp_seed = seed;
+  return SIRIUS_OK;
+}
+
 // Top-k FSparse (PAPER.md:121 footnote): SIRIUS_TOPK decode steps keep, per layer
 // and sequence, the k = round(keep_fraction * ffn) neurons of largest |SiLU(g)| (reading D30).
 sirius_status sirius_topk_enable(sirius_ctx* c, float keep_fraction) {
@@ -1025,6 +1041,10 @@ static sirius_status enqueue_decode_rows(sirius_ctx* c, const int32_t* token_in,
   prof_begin(c, P_STEP);
   OK(forward_rows(c, token_in, pos, 0, B, 1, ROWS_DECODE, !dense, n_active_out, gate_act_out));
   OK(enqueue_head_argmax(c, token_in, 1, B, logits_out, c->dec_nacc, token_out, nullptr, 0.f, 0));
+  if (c->samp_temp > 0.f) {
+    const float* lo = logits_out ? logits_out : c->ranks[0].logits;
+    LCU(launch::sample_tokens(lo, c->Vr, c->Vr, c->samp_temp, c->samp_seed, pos, nullptr, 1, token_out, B, c->stream));
+  }
   prof_end(c);
   CU(cudaGetLastError());
   return SIRIUS_OK;
@@ -1041,7 +1061,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
   if (c->decode_rows) return enqueue_decode_rows(c, token_in, pos, dense, token_out, logits_out, n_active_out,
                                                  gate_act_out);
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
-  if (c->use_step && !csparse && !topk) {  // the whole step in one persistent launch (decode_step.cu)
+  if (c->use_step && !csparse && !topk && c->samp_temp == 0.f) {  // the whole step in one persistent launch
     RankState& R = c->ranks[0];
     StepArgs s = {};
     s.d = d;
@@ -1194,8 +1214,9 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     a.rows = c->Vr;
     a.K = d;
     a.epi = EPI_ARGMAX;
-    a.out = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0) : nullptr;
-    a.ldo = c->emulated ? cf.vocab : c->Vr;
+    a.out = logits_out ? logits_out + (c->emulated ? (size_t)R.rank * c->Vr : 0)
+                       : (c->samp_temp > 0.f ? R.logits : nullptr);  // sampling needs the logits
+    a.ldo = logits_out ? (c->emulated ? cf.vocab : c->Vr) : c->Vr;
     a.amax = c->amax;
     a.index_offset = (uint32_t)R.rank * c->Vr;
     a.finalize = (cf.tp_size == 1);
@@ -1213,6 +1234,10 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     }
     LCU(launch::argmax_finalize(c->amax, B, token_out, c->stream));
   }
+  if (c->samp_temp > 0.f) {  // sampled draft (reading D31): the token at position pos + 1
+    const float* lo = logits_out ? logits_out : c->ranks[0].logits;
+    LCU(launch::sample_tokens(lo, c->Vr, c->Vr, c->samp_temp, c->samp_seed, pos, nullptr, 1, token_out, B, c->stream));
+  }
   CU(cudaGetLastError());
   return SIRIUS_OK;
 }
@@ -1229,8 +1254,10 @@ sirius_status sparse_decode_step(sirius_ctx* c, const int32_t* token_in, const i
   OK(check_sticky(c));
   if ((flags & SIRIUS_CSPARSE) && !c->cs_ready)
     return fail(c, SIRIUS_ERR_STATE, "CSPARSE decode without a plan (sirius_csparse_enable + sirius_prefill)");
+  uint32_t tbits;
+  memcpy(&tbits, &c->samp_temp, 4);
   GraphKey key = {0xDEC0u, flags, (uintptr_t)token_in, (uintptr_t)pos, (uintptr_t)token_out, (uintptr_t)logits_out,
-                  (uintptr_t)n_active_out, (uintptr_t)gate_act_out};
+                  (uintptr_t)n_active_out, (uintptr_t)gate_act_out, (uintptr_t)tbits, (uintptr_t)c->samp_seed};
   return run_graphed(c, key, [&] {
     OK(enqueue_decode(c, token_in, pos, flags, token_out, logits_out, n_active_out, gate_act_out));
     mirror_err(c);  // a position outside [0, max_seq) is reported by the NEXT call (include/sirius.h)
@@ -1248,6 +1275,11 @@ static sirius_status enqueue_correct(sirius_ctx* c, const int32_t* kernel_tokens
   OK(forward_rows(c, kernel_tokens, start_pos, 0, B, gamma, ROWS_VERIFY));
   OK(enqueue_head_argmax(c, kernel_tokens, gamma, M, logits_out, n_accept_out, next_token_out, q_out,
                          accept_threshold, accept_mode));
+  if (c->samp_temp > 0.f) {  // interleaved / bonus token sampled from the full model's row j (reading D31)
+    const float* lo = logits_out ? logits_out : c->ranks[0].logits;
+    LCU(launch::sample_tokens(lo, c->Vr, c->Vr, c->samp_temp, c->samp_seed, start_pos, n_accept_out, gamma,
+                              next_token_out, B, c->stream));
+  }
   prof_end(c);
   mirror_err(c);
   CU(cudaGetLastError());
@@ -1326,9 +1358,11 @@ sirius_status correct_kernel(sirius_ctx* c, const int32_t* kernel_tokens, const 
   OK(check_sticky(c));
   uint32_t rbits;
   memcpy(&rbits, &accept_threshold, 4);
+  uint32_t tbits;
+  memcpy(&tbits, &c->samp_temp, 4);
   GraphKey key = {0xC0EEu, (uintptr_t)gamma, (uintptr_t)rbits, (uintptr_t)accept_mode, (uintptr_t)kernel_tokens,
                   (uintptr_t)start_pos, (uintptr_t)n_accept_out, (uintptr_t)next_token_out, (uintptr_t)q_out,
-                  (uintptr_t)logits_out};
+                  (uintptr_t)logits_out, (uintptr_t)tbits, (uintptr_t)c->samp_seed};
   OK(run_graphed(c, key, [&] {
     return enqueue_correct(c, kernel_tokens, start_pos, gamma, accept_threshold, accept_mode, n_accept_out,
                            next_token_out, q_out, logits_out);

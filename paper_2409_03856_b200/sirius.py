@@ -27,7 +27,7 @@ ACCEPT_EXACT_ARGMAX = 1
 # every symbol include/sirius.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
                "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_tree_kernel", "sirius_topk_enable",
-               "sirius_destroy",
+               "sirius_set_sampling", "sirius_destroy",
                "sirius_last_error", "sirius_version")
 
 
@@ -82,6 +82,8 @@ def load():
         lib.sirius_verify_row_argmax.restype = I
         lib.sirius_tree_kernel.argtypes = [P, P, P, I, I, I, F, I, P, P, P]
         lib.sirius_tree_kernel.restype = I
+        lib.sirius_set_sampling.argtypes = [P, F, ctypes.c_uint64]
+        lib.sirius_set_sampling.restype = I
         lib.sirius_topk_enable.argtypes = [P, F]
         lib.sirius_topk_enable.restype = I
         lib.sirius_csparse_enable.argtypes = [P, F]
@@ -204,6 +206,9 @@ class Sirius:
         self._check(self.lib.sirius_tree_kernel(self.h, _ptr(pending), _ptr(start_pos), gamma, width, branch,
                                                 accept_threshold, accept_mode, _ptr(n_accept_out),
                                                 _ptr(next_token_out), _ptr(path_tokens_out)))
+
+    def sirius_set_sampling(self, temperature: float, seed: int = 0):
+        self._check(self.lib.sirius_set_sampling(self.h, float(temperature), int(seed) & (2 ** 64 - 1)))
 
     def sirius_topk_enable(self, keep_fraction: float):
         self._check(self.lib.sirius_topk_enable(self.h, float(keep_fraction)))

@@ -150,3 +150,40 @@ def test_topk_keep_one_equals_dense(tiny):
     r2 = m2.decode(3, 16, False)
     assert r1.mask.all()
     np.testing.assert_array_equal(r1.logits, r2.logits)
+
+
+# ------------------------------------------------------------------ sampled decoding (reading D31)
+def test_splitmix64_reference_values():
+    """The counter-based generator is SplitMix64's output function: the published sequence of the
+    generator seeded with 0 starts e220a8397b1dcdaf, 6e789e6aa1b965f4."""
+    assert so.splitmix64(0) == 0xE220A8397B1DCDAF
+    assert so.splitmix64(0x9E3779B97F4A7C15) == 0x6E789E6AA1B965F4
+    u = [so.sample_uniform(7, 0, p) for p in range(2000)]
+    assert all(0.0 <= x < 1.0 for x in u) and abs(np.mean(u) - 0.5) < 0.02
+    assert all(x * 16777216.0 == int(x * 16777216.0) for x in u[:50])  # 24-bit values (exact in fp32)
+
+
+def test_sampler_inverse_cdf_brute_force():
+    """Over an evenly spaced grid of u, each token is drawn with frequency softmax(l / T)_v (to the grid
+    resolution); T -> 0 gives the argmax."""
+    rng = np.random.default_rng(31)
+    l = rng.standard_normal(37) * 3.0
+    for T in (0.6, 1.0):
+        n = 1 << 15
+        counts = np.bincount([so.sample_token(l, T, (i + 0.5) / n) for i in range(n)], minlength=l.size)
+        p = np.exp((l - l.max()) / T)
+        p /= p.sum()
+        assert np.max(np.abs(counts / n - p)) <= 2.0 / n
+    assert so.sample_token(l, 1e-3, 0.999) == so.argmax_lowest(l)
+
+
+def test_sampled_sirius_accounting(tiny):
+    """Sampled Sirius (temperature 0.6): r = 0 accepts every draft; the run is a function of the seed."""
+    cfg, w = tiny
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 9, 24)
+    a = so.generate(so.OracleModel(cfg, w, max_seq=128), prompt, 20, 4, 0.0, thr, temperature=0.6, seed=3)
+    b = so.generate(so.OracleModel(cfg, w, max_seq=128), prompt, 20, 4, 0.0, thr, temperature=0.6, seed=3)
+    c = so.generate(so.OracleModel(cfg, w, max_seq=128), prompt, 20, 4, 0.0, thr, temperature=0.6, seed=4)
+    assert a.tokens == b.tokens and a.tokens != c.tokens
+    assert all(x == 4 for x in a.advances[:-1])
