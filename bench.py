@@ -462,7 +462,11 @@ def main():
     traffic = None
     summ = {}
     try:
-        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")))
+        for tag in ("r02", "r01"):  # the latest committed ncu --set full summary
+            pth = os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.json")
+            if os.path.exists(pth):
+                summ = json.load(open(pth))
+                break
     except Exception:
         pass
     if prof.get("decode_step", (0.0, 0))[1] > 0:

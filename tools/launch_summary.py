@@ -28,7 +28,7 @@ def seg_summary(title, seg):
 # verify segment: from the head gemv before the last accept_finalize
 last = fin[-1]
 j = last
-while j > 0 and names[j] != "gemv_kernel": j -= 1
+while j > 0 and names[j] != "gemv_kernel": j -= 1  # the head GEMV of the last draft step
 seg_summary("correct_kernel (last)", order[j + 1:last + 1])
 # the verify's first layers launch by launch (GEMMs in order: QKV, O, gate+up, down)
 print("   first verify launches:", ", ".join(f"{names[i].replace('_kernel', '')} {launch[order[i]].get('gpu__time_duration.sum', 0) / 1e3:.1f}"

@@ -8,7 +8,7 @@ python tools/ncu_summary.py $TAG gpurun_out/prof_${TAG}_ffn_kernel.ncu-rep gpuru
   gpurun_out/prof_${TAG}_attn_stage_kernel.ncu-rep gpurun_out/prof_${TAG}_gemm_verify.ncu-rep \
   gpurun_out/prof_${TAG}_attn_rows.ncu-rep > gpurun_out/ncu_summary_${TAG}.txt 2>&1
 cp profiles/ncu_summary_${TAG}.json gpurun_out/
-python profiles/launch_summary.py gpurun_out/launches_${TAG}.csv > gpurun_out/${TAG}_launch_summary.txt
+python tools/launch_summary.py gpurun_out/launches_${TAG}.csv > gpurun_out/${TAG}_launch_summary.txt
 gzip -f gpurun_out/launches_${TAG}.csv
 rm -f gpurun_out/prof_${TAG}_gemv_kernel.ncu-rep gpurun_out/prof_${TAG}_attn_stage_kernel.ncu-rep \
   gpurun_out/prof_${TAG}_gemm_verify.ncu-rep gpurun_out/prof_${TAG}_attn_rows.ncu-rep
