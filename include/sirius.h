@@ -19,6 +19,7 @@
  *   sirius_tree_kernel  — tree building + tree verification of one kernel
  *   sirius_topk_enable  — top-k FSparse draft model (PAPER.md:121 footnote)
  *   sirius_set_sampling — temperature sampling of drafted / interleaved tokens
+ *   sirius_par_export / sirius_par_enable / sirius_par_disable — fused NVLink peer all-reduce (TP > 1)
  *   sirius_destroy / sirius_last_error
  *
  * Conventions (all entry points):
@@ -240,6 +241,36 @@ sirius_status sirius_topk_enable(sirius_ctx* ctx, float keep_fraction);
  * Errors: INVALID_ARG (keep_fraction outside [0, 1]); UNSUPPORTED (batch != 1, or k not a positive
  * multiple of 8); CUDA (allocation).  Synchronous. */
 sirius_status sirius_csparse_enable(sirius_ctx* ctx, float keep_fraction);
+
+/* Fused peer all-reduce of the tensor-parallel decode step (SURVEY.md §8(e) phase 2: "fuse the
+ * all-reduce into the O-proj / down-proj epilogue over NVLink peer memory"; the per-layer all-reduces
+ * of S3 and S6 and the LM-head argmax combine of S7 in SURVEY.md §8(a); the paper itself runs on one
+ * GPU).  Each rank owns a comm buffer of identical layout
+ *   slots [2][tp_size][batch * d_model] fp32 | keys [2][tp_size][8] u64 | flags [2][tp_size] u64
+ * that every other rank maps through CUDA IPC.  With the fused path on, sparse_decode_step (the
+ * per-stage path, batch <= 4, or 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the last CTA of
+ * the O-proj GEMV / CATS FFN / LM-head kernel stores the rank partial (or the packed argmax keys)
+ * into its slot on every rank over NVLink and release-stores the sync point's sequence number into
+ * the flags; the activation prologue of the next kernel acquire-waits for all tp_size flags and sums
+ * the slots in rank order, so every rank computes bitwise the same residual.  prefill, correct_kernel
+ * and the batched row path keep the NCCL collectives.
+ *
+ * sirius_par_export: HOST handle_out [SIRIUS_PAR_HANDLE_BYTES] = this rank's cudaIpcMemHandle_t.
+ *   Errors: STATE for an emulated / stub / tp_size 1 context; CUDA.
+ * sirius_par_enable: peer_handles = HOST [tp_size][SIRIUS_PAR_HANDLE_BYTES], every rank's exported
+ *   handle in rank order (the own entry is ignored), or NULL for a single-GPU emulated context (the
+ *   ranks' buffers are all in this process: the emulated ranks run stage by stage, so every wait is
+ *   already satisfied when it starts) or a SIRIUS_DEBUG_STUB_COMM context (loopback timing proxy: every
+ *   peer is the rank's own buffer, the consumer sums tp_size copies scaled by 1 / tp_size).  Every rank
+ *   must call it (collectively, after every rank's sirius_init and export) before its next decode.
+ *   Errors: INVALID_ARG (handles given / missing for the context kind); UNSUPPORTED (tp_size 1 or
+ *   > 8; a peer buffer cannot be mapped); CUDA.  Synchronous.
+ * sirius_par_disable: back to the NCCL collectives (the mappings stay until sirius_destroy); all ranks.
+ * A rank that does not arrive within 10 s makes the waiting ranks' next call return SIRIUS_ERR_NCCL. */
+#define SIRIUS_PAR_HANDLE_BYTES 64
+sirius_status sirius_par_export(sirius_ctx* ctx, void* handle_out);
+sirius_status sirius_par_enable(sirius_ctx* ctx, const void* peer_handles);
+sirius_status sirius_par_disable(sirius_ctx* ctx);
 
 /* The full model's greedy token (argmax, lowest id on ties) of EVERY verify row of the last
  * correct_kernel call — the interleaving candidates of the component ablation without rollback

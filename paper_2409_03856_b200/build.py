@@ -48,11 +48,14 @@ def build_sirius(force: bool = False, verbose: bool = False) -> str:
         return out
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for s in srcs:
-        o = os.path.join(objdir, os.path.basename(s) + ".o")
-        _run([nvcc(), *ARCH, *NVCC_FLAGS, "-c", s, "-o", o], verbose)
-        objs.append(o)
+    objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in srcs]
+    # translation units compile independently: in parallel (SIRIUS_BUILD_JOBS, default: all cores)
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = int(os.environ.get("SIRIUS_BUILD_JOBS", "0")) or os.cpu_count() or 1
+    with ThreadPoolExecutor(max_workers=jobs) as ex:
+        for f in [ex.submit(_run, [nvcc(), *ARCH, *NVCC_FLAGS, "-c", s, "-o", o], verbose)
+                  for s, o in zip(srcs, objs)]:
+            f.result()
     _run([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-ldl"], verbose)
     return out
 

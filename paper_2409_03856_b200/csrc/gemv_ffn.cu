@@ -83,7 +83,10 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
       }
     }
   }
-  if (a.epi != EPI_ARGMAX) return;
+  if (a.epi != EPI_ARGMAX) {
+    if (a.par_produce) par::push_last(a.pro.par, a.out, B * a.ldo, nullptr, 0);  // fused all-reduce (TP > 1)
+    return;
+  }
   if (lane == 0)
     for (int b = 0; b < B; ++b) key_s[warp * B + b] = best[b];
   __syncthreads();
@@ -91,6 +94,10 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
     unsigned long long k = 0ull;
     for (int w = 0; w < kGemvWarps; ++w) k = key_s[w * B + tid] > k ? key_s[w * B + tid] : k;
     atomicMax(a.amax + tid, k);
+  }
+  if (a.par_produce) {  // TP > 1: the rank's packed keys go to every rank; argmax_par_kernel reduces them
+    par::push_last(a.pro.par, nullptr, 0, a.amax, B);
+    return;
   }
   if (a.finalize) {
     __syncthreads();
@@ -119,6 +126,20 @@ __global__ void argmax_finalize_kernel(unsigned long long* amax, int B, int32_t*
     const unsigned long long k = amax[b];
     amax[b] = 0ull;
     token_out[b] = (int32_t)argmax_key_index(k);
+  }
+}
+
+// TP > 1 with the fused peer all-reduce: wait for every rank's packed keys of this sync point and
+// reduce them (max = the global lowest-index argmax, as the NCCL max-all-reduce) -> token
+__global__ void argmax_par_kernel(PeerAr p, int B, int32_t* token_out) {
+  par::wait(p);
+  const int par = (int)(__ldcg(p.seq) & 1ull);
+  const unsigned long long* k = par::keys(p, par);
+  const int b = threadIdx.x;
+  if (b < B) {
+    unsigned long long m = 0ull;
+    for (int r = 0; r < p.world; ++r) m = k[(size_t)r * p.key_n + b] > m ? k[(size_t)r * p.key_n + b] : m;
+    token_out[b] = (int32_t)argmax_key_index(m);
   }
 }
 
@@ -298,6 +319,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
       for (int c = 0; c < nch; ++c) cnt += __popc(act_s[c][tid]);
       if (cnt) atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, cnt);
     }
+    if (a.par_produce) par::push_last(a.pro.par, a.out, B * d, nullptr, 0);  // fused all-reduce (TP > 1)
     fstamp(a, 6);
     return;
   }
@@ -337,6 +359,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
     for (int p = 0; p < G; ++p) tot += __ldcg(a.part_cnt + p * B + tid);
     atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, tot);
   }
+  if (a.par_produce) par::push_last(a.pro.par, a.out, B * d, nullptr, 0);  // fused all-reduce (TP > 1)
 }
 
 }  // namespace
@@ -364,6 +387,11 @@ static cudaError_t gemv_b(const GemvArgs& a, int grid, cudaStream_t st) {
   if (cpl <= 16) return gemv_bc<B, 16>(a, grid, st);
   if (cpl <= 32) return gemv_bc<B, 32>(a, grid, st);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t argmax_par(const PeerAr& p, int B, int32_t* token_out, cudaStream_t st) {
+  argmax_par_kernel<<<1, 32, 0, st>>>(p, B, token_out);
+  return cudaGetLastError();
 }
 
 cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st) {

@@ -24,6 +24,7 @@ int gemv_grid(int rows, int num_sms);
 cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st);
 
 cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st);
+cudaError_t argmax_par(const PeerAr& p, int B, int32_t* token_out, cudaStream_t st);
 int ffn_grid(int F, int num_sms);
 cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st);
 bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms);
@@ -115,6 +116,12 @@ struct RankState {
   unsigned* tk_mask = nullptr;             // selected set [B][Fr/32 + 1] bits
   int32_t* cs_idx = nullptr;
   uint16_t* cs_w = nullptr;
+  // fused peer all-reduce (TP > 1, peer_ar.cuh): the comm buffer peers map, the device array of every
+  // rank's buffer as mapped here, the sync-point counter and the producer arrival counter
+  char* par_buf = nullptr;
+  char** par_peers = nullptr;
+  unsigned long long* par_seq = nullptr;
+  unsigned* par_done = nullptr;
 };
 
 struct sirius_ctx {
@@ -130,6 +137,12 @@ struct sirius_ctx {
   bool stub_comm = false;  // SIRIUS_DEBUG_STUB_COMM: tp_size > 1 on one GPU with every collective skipped
                            // (one rank's compute, timing proxy only: results are rank-local partials)
   void* comm = nullptr;
+  // fused peer all-reduce of the decode step (sirius_par_enable; SURVEY.md §8(e) phase 2)
+  bool par_on = false;
+  bool par_loopback = false;      // stub comm: every peer is this rank's own buffer (timing proxy)
+  int par_slot_n = 0, par_key_n = 0;
+  size_t par_bytes = 0;
+  std::vector<void*> par_opened;  // peer buffers opened through CUDA IPC (closed by sirius_destroy)
   cudaStream_t stream = nullptr;
   int Hr = 0, KVr = 0, Fr = 0, Vr = 0, Nqkv = 0, G = 0, MAXM = 0;
   int num_sms = 148;
@@ -287,6 +300,8 @@ sirius_status check_sticky(sirius_ctx* c) {
   }
   if (*c->err_host != 0) {
     int e = *c->err_host;
+    if (e & 8)
+      return fail(c, SIRIUS_ERR_NCCL, "fused peer all-reduce: a rank did not arrive within 10 s");
     return fail(c, SIRIUS_ERR_CAPACITY,
                 std::string("device-side capacity error (bits ") + std::to_string(e) +
                     "): 1 = decode pos outside [0, max_seq), 2 = verify/prefill row outside capacity, "
@@ -319,6 +334,7 @@ sirius_status run_graphed(sirius_ctx* c, const GraphKey& key0, F enqueue) {
   if (!c->use_graphs) return enqueue();
   GraphKey key = key0;
   key.push_back(c->prof_on ? 1u : 0u);  // profiled graphs carry event-record nodes
+  key.push_back(c->par_on ? 1u : 0u);   // the decode step with the fused peer all-reduce
   for (auto& g : c->graphs)
     if (g.key == key) {
       c->launches += g.kernels;
@@ -387,11 +403,35 @@ sirius_status allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev,
 
 sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B);
 
+// the rank's fused peer all-reduce descriptor (sirius_par_enable)
+PeerAr par_of(const sirius_ctx* c, const RankState& R) {
+  PeerAr p = {};
+  p.world = c->cfg.tp_size;
+  p.rank = R.rank;
+  p.loopback = c->par_loopback ? 1 : 0;
+  p.slot_n = c->par_slot_n;
+  p.key_n = c->par_key_n;
+  p.scale = c->par_loopback ? 1.0f / (float)c->cfg.tp_size : 1.0f;
+  p.peers = R.par_peers;
+  p.self = R.par_buf;
+  p.seq = R.par_seq;
+  p.done = R.par_done;
+  p.err = c->err_dev;
+  return p;
+}
+// consumer prologue: delta = the all-reduced partial of the last sync point
+void par_consume(const sirius_ctx* c, const RankState& R, Prologue& pro) {
+  pro.delta = nullptr;
+  pro.par_consume = 1;
+  pro.par = par_of(c, R);
+}
+
 // ---- the decode CATS FFN of layer l (S4-S6) on residual rows base (+ delta): out = the FFN's
 // contribution to the residual (accumulated into out, which the O-proj GEMV zeroed, in atomic mode)
 sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float* base, const float* delta,
                                 float* res_out, float* out, bool dense, int32_t* n_active_out, int n_active_stride,
-                                float* gate_out, long long gate_stride, bool csparse = false, bool topk = false) {
+                                float* gate_out, long long gate_stride, bool csparse = false, bool topk = false,
+                                bool par_decode = false) {
   const sirius_config& cf = c->cfg;
   FfnArgs f = {};
   if (topk) {  // gate GEMV -> exact top-k selection (topk.cu) -> the FFN kernel in precomputed-gate mode
@@ -443,6 +483,10 @@ sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float*
   f.n_active_out = n_active_out;
   f.n_active_stride = n_active_stride;
   f.atomic_out = c->ffn_atomic ? 1 : 0;
+  if (c->par_on && par_decode) {  // fused peer all-reduce: consume the O-proj sum, push the FFN partial
+    par_consume(c, R, f.pro);
+    f.par_produce = 1;
+  }
   f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
   f.gate_out = gate_out;
   f.gate_stride = gate_stride;
@@ -816,6 +860,14 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
       return cleanup_fail(SIRIUS_ERR_CUDA);
     dA_h.push_back(R.dA);
     dF_h.push_back(R.dF);
+    if (cf.tp_size > 1) {  // fused peer all-reduce buffers (zeroed: flags 0 < every sequence number)
+      c->par_slot_n = round_up(B * d, 4);
+      c->par_key_n = 8;
+      c->par_bytes = (size_t)2 * cf.tp_size * ((size_t)c->par_slot_n * 4 + (size_t)c->par_key_n * 8 + 8);
+      if (alloc(c, &R.par_buf, c->par_bytes) || alloc(c, &R.par_peers, 8) || alloc(c, &R.par_seq, 1) ||
+          alloc(c, &R.par_done, 1))
+        return cleanup_fail(SIRIUS_ERR_CUDA);
+    }
     // transposed W_down ([d, F/tp], K-major in the neuron dim) for the verify down-projection GEMM
     R.w_down_t.resize(L);
     for (int l = 0; l < L; ++l) {
@@ -868,6 +920,7 @@ sirius_status sirius_destroy(sirius_ctx* c) {
     }
   }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  for (void* p : c->par_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocations) cudaFree(p);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->pre_start_host) cudaFreeHost(c->pre_start_host);
@@ -981,6 +1034,64 @@ sirius_status sirius_topk_enable(sirius_ctx* c, float keep_fraction) {
       return SIRIUS_ERR_CUDA;
   }
   c->topk_k = k;
+  return SIRIUS_OK;
+}
+
+// ---- fused peer all-reduce (SURVEY.md §8(e) phase 2; peer_ar.cuh, include/sirius.h)
+sirius_status sirius_par_export(sirius_ctx* c, void* handle_out) {
+  if (!c || !handle_out) return SIRIUS_ERR_INVALID_ARG;
+  OK(check_sticky(c));
+  if (c->cfg.tp_size == 1 || c->emulated || c->stub_comm)
+    return fail(c, SIRIUS_ERR_STATE, "sirius_par_export: only a real tensor-parallel rank (tp_size > 1, NCCL) exports");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, c->ranks[0].par_buf));
+  memcpy(handle_out, &h, sizeof(h));
+  return SIRIUS_OK;
+}
+
+sirius_status sirius_par_enable(sirius_ctx* c, const void* peer_handles) {
+  if (!c) return SIRIUS_ERR_INVALID_ARG;
+  OK(check_sticky(c));
+  const sirius_config& cf = c->cfg;
+  if (cf.tp_size == 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "sirius_par_enable: tp_size 1 has no all-reduce");
+  if (cf.tp_size > 8) return fail(c, SIRIUS_ERR_UNSUPPORTED, "sirius_par_enable: at most 8 ranks");
+  if (c->par_on) return SIRIUS_OK;
+  const bool real = !c->emulated && !c->stub_comm;
+  if (real != (peer_handles != nullptr))
+    return fail(c, SIRIUS_ERR_INVALID_ARG, real ? "sirius_par_enable: a real rank needs the peers' handles"
+                                                : "sirius_par_enable: emulated / stub contexts take no handles");
+  std::vector<char*> peers(cf.tp_size);
+  if (c->emulated) {  // every emulated rank's buffer is in this process
+    for (int r = 0; r < cf.tp_size; ++r) peers[r] = c->ranks[r].par_buf;
+  } else if (c->stub_comm) {
+    for (int r = 0; r < cf.tp_size; ++r) peers[r] = c->ranks[0].par_buf;
+  } else {
+    const cudaIpcMemHandle_t* hs = static_cast<const cudaIpcMemHandle_t*>(peer_handles);
+    for (int r = 0; r < cf.tp_size; ++r) {
+      if (r == cf.tp_rank) {
+        peers[r] = c->ranks[0].par_buf;
+        continue;
+      }
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        for (void* q : c->par_opened) cudaIpcCloseMemHandle(q);
+        c->par_opened.clear();
+        return fail(c, SIRIUS_ERR_UNSUPPORTED, "sirius_par_enable: cudaIpcOpenMemHandle failed (no peer access?)");
+      }
+      c->par_opened.push_back(p);
+      peers[r] = static_cast<char*>(p);
+    }
+  }
+  for (auto& R : c->ranks) CU(cudaMemcpy(R.par_peers, peers.data(), sizeof(char*) * peers.size(), cudaMemcpyHostToDevice));
+  c->par_loopback = c->stub_comm;
+  c->par_on = true;
+  return SIRIUS_OK;
+}
+
+sirius_status sirius_par_disable(sirius_ctx* c) {
+  if (!c) return SIRIUS_ERR_INVALID_ARG;
+  c->par_on = false;  // the peers stay mapped (sirius_destroy unmaps); the sequence numbers keep counting
   return SIRIUS_OK;
 }
 
@@ -1120,6 +1231,9 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     CU(cudaGetLastError());
     return SIRIUS_OK;
   }
+  // TP > 1 with sirius_par_enable: the all-reduces are fused into the producing kernels' epilogues and
+  // the consuming kernels' prologues (peer_ar.cuh) instead of NCCL launches between them
+  const bool par = c->par_on && cf.tp_size > 1;
   for (int l = 0; l < L; ++l) {
     for (auto& R : c->ranks) {
       GemvArgs a = {};
@@ -1132,6 +1246,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
         a.pro.mode = IN_RESID;
         a.pro.base = R.resB;
         a.pro.delta = R.dF;
+        if (par) par_consume(c, R, a.pro);
       }
       a.pro.norm_w = R.attn_norm[l];
       a.pro.eps = cf.rms_eps;
@@ -1183,11 +1298,15 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
         o.zero_out = R.dF;
         o.zero_n = B * d;
       }
+      if (par) {  // push the O-proj partial to every rank (the FFN prologue sums them)
+        o.pro.par = par_of(c, R);
+        o.par_produce = 1;
+      }
       prof_begin(c, P_OPROJ);
       OK(run_gemv(c, o, B));
       prof_end(c);
     }
-    OK(allreduce(c, &RankState::dA, c->dA_ptrs, B));
+    if (!par) OK(allreduce(c, &RankState::dA, c->dA_ptrs, B));
     for (auto& R : c->ranks) {
       float* g_out = nullptr;
       long long g_stride = 0;
@@ -1198,10 +1317,10 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
       }
       prof_begin(c, P_FFN);
       OK(launch_decode_ffn(c, R, l, R.resA, R.dA, R.resB, R.dF, dense, n_active_out ? n_active_out + l : nullptr, L,
-                           g_out, g_stride, csparse, topk));
+                           g_out, g_stride, csparse, topk, par));
       prof_end(c);
     }
-    OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
+    if (!par) OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
   }
   for (auto& R : c->ranks) {
     GemvArgs a = {};
@@ -1222,11 +1341,17 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     a.finalize = (cf.tp_size == 1);
     a.done_counter = R.head_cnt;
     a.token_out = token_out;
+    if (par) {  // consume the last FFN sum, push the rank's packed argmax keys
+      par_consume(c, R, a.pro);
+      a.par_produce = 1;
+    }
     prof_begin(c, P_HEAD);
     OK(run_gemv(c, a, B));
     prof_end(c);
   }
-  if (cf.tp_size > 1) {
+  if (par) {
+    for (auto& R : c->ranks) LCU(launch::argmax_par(par_of(c, R), B, token_out, c->stream));
+  } else if (cf.tp_size > 1) {
     if (!c->emulated && !c->stub_comm) {
       NcclApi& api = nccl();
       int r = api.allReduce(c->amax, c->amax, B, kNcclUint64, kNcclMax, c->comm, c->stream);

@@ -23,11 +23,13 @@ SIRIUS_CSPARSE = 2
 SIRIUS_TOPK = 4
 ACCEPT_THRESHOLD = 0
 ACCEPT_EXACT_ARGMAX = 1
+PAR_HANDLE_BYTES = 64  # include/sirius.h SIRIUS_PAR_HANDLE_BYTES (sizeof(cudaIpcMemHandle_t))
 
 # every symbol include/sirius.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("sirius_init", "sirius_prefill", "sparse_decode_step", "correct_kernel", "kv_rewrite",
                "sirius_verify_row_argmax", "sirius_csparse_enable", "sirius_tree_kernel", "sirius_topk_enable",
-               "sirius_set_sampling", "sirius_destroy",
+               "sirius_set_sampling", "sirius_par_export", "sirius_par_enable", "sirius_par_disable",
+               "sirius_destroy",
                "sirius_last_error", "sirius_version")
 
 
@@ -86,6 +88,12 @@ def load():
         lib.sirius_set_sampling.restype = I
         lib.sirius_topk_enable.argtypes = [P, F]
         lib.sirius_topk_enable.restype = I
+        lib.sirius_par_export.argtypes = [P, P]
+        lib.sirius_par_export.restype = I
+        lib.sirius_par_enable.argtypes = [P, P]
+        lib.sirius_par_enable.restype = I
+        lib.sirius_par_disable.argtypes = [P]
+        lib.sirius_par_disable.restype = I
         lib.sirius_csparse_enable.argtypes = [P, F]
         lib.sirius_csparse_enable.restype = I
         lib.sirius_debug_csparse_plan.argtypes = [P, P, P, ctypes.POINTER(I)]
@@ -212,6 +220,26 @@ class Sirius:
 
     def sirius_topk_enable(self, keep_fraction: float):
         self._check(self.lib.sirius_topk_enable(self.h, float(keep_fraction)))
+
+    def sirius_par_export(self) -> bytes:
+        """This rank's comm-buffer IPC handle (SIRIUS_PAR_HANDLE_BYTES bytes) for sirius_par_enable."""
+        buf = ctypes.create_string_buffer(PAR_HANDLE_BYTES)
+        self._check(self.lib.sirius_par_export(self.h, buf))
+        return buf.raw
+
+    def sirius_par_enable(self, peer_handles: Optional[Sequence[bytes]] = None):
+        """Fused NVLink peer all-reduce of the TP decode step.  peer_handles: every rank's exported
+        handle in rank order (real ranks), None for emulated / stub contexts."""
+        arg = None
+        if peer_handles is not None:
+            blob = b"".join(peer_handles)
+            if len(blob) != PAR_HANDLE_BYTES * len(peer_handles):
+                raise ValueError("each handle must be PAR_HANDLE_BYTES bytes")
+            arg = ctypes.create_string_buffer(blob, len(blob))
+        self._check(self.lib.sirius_par_enable(self.h, arg))
+
+    def sirius_par_disable(self):
+        self._check(self.lib.sirius_par_disable(self.h))
 
     def sirius_csparse_enable(self, keep_fraction: float):
         self._check(self.lib.sirius_csparse_enable(self.h, float(keep_fraction)))

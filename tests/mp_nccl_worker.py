@@ -26,6 +26,9 @@ def main():
     prompt = synth.eval_prompt(cfg, 0, 128)
     ctx = S.Sirius(cfg, sg.device_weights(cfg, world, rank), thr, batch=1, max_seq=256, max_gamma=16,
                    tp_size=world, tp_rank=rank, nccl_comm=comm)
+    par = os.environ.get("SIRIUS_TEST_PAR", "0") == "1"
+    if par:  # fused NVLink peer all-reduce of the decode step (CUDA-IPC mapped comm buffers)
+        TP.par_bootstrap(ctx)
     out = driver.Driver(ctx).sirius([prompt], 48, 16, 0.3)
     res = {"rank": rank, "tokens": out.tokens[0], "advances": out.advances(0)}
     allres = [None] * world
@@ -36,7 +39,7 @@ def main():
                           0.3, thr)
         ok = all(r["tokens"] == ref.tokens for r in allres) and \
             all(r["advances"] == ref.advances[:len(r["advances"])] for r in allres)
-        print(json.dumps({"world": world, "ok": ok, "tokens_equal_across_ranks":
+        print(json.dumps({"world": world, "par": par, "ok": ok, "tokens_equal_across_ranks":
                           all(r["tokens"] == allres[0]["tokens"] for r in allres)}), flush=True)
         if not ok:
             sys.exit(1)

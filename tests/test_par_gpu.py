@@ -1,0 +1,161 @@
+"""Fused peer all-reduce of the tensor-parallel decode step (SURVEY.md §8(e) phase 2; include/sirius.h
+sirius_par_enable; csrc/peer_ar.cuh) on one GPU.
+
+One GPU cannot host ranks whose kernels wait on one another (B200_PROFILING.md), so the ranks are
+emulated in one context: every rank's kernel of a stage runs before any rank's kernel of the next
+stage, so each consumer's flag wait is already satisfied when it starts — the pushes, the slot /
+flag addressing, the sequence numbers, the parities and the rank-order sums all run as on a real
+TP group, through the same kernels.
+
+  * bitwise: with the deterministic FFN reduction, the fused path reproduces the in-order-sum
+    emulation (the NCCL stand-in) bit for bit — tokens, logits, active counts, gate activations —
+    across decode steps interleaved with correct_kernel / kv_rewrite (whose collectives are not
+    fused: the sequence numbers must survive them);
+  * oracle: the whole Sirius loop free-running at 8B-2L shapes, TP 2, fused path with the default
+    atomic FFN, token-exact against the TP-1 oracle;
+  * loopback stub (the per-rank timing proxy): runs, finite, no device error;
+  * ABI errors.
+The real multi-process path (CUDA IPC handles) is tests/test_tp_nccl_gpu.py (>= 2 GPUs).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import sirius_oracle as so
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def i32(x):
+    return torch.tensor(np.asarray(x, dtype=np.int32), device="cuda")
+
+
+def make_ctx(cfg, w, thr, tp, max_seq=256, max_gamma=16):
+    from paper_2409_03856_b200 import sirius as S
+    return S.Sirius(cfg, w, thr, batch=1, max_seq=max_seq, max_gamma=max_gamma, tp_size=tp)
+
+
+def script(ctx, cfg, prompt, steps=10, gamma=4):
+    """prefill -> decode steps (sparse, one dense) -> correct_kernel + kv_rewrite -> more decode
+    steps; returns every output of every call (host arrays)."""
+    from paper_2409_03856_b200 import sirius as S
+    L, F, V = cfg.n_layers, cfg.ffn_dim, cfg.vocab
+    outs = []
+    first = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [len(prompt)], first)
+    tok, T = int(first.item()), len(prompt)
+    drafts = [tok]
+    for i in range(steps):
+        if i == gamma:  # verify the first gamma drafts, commit, continue after the accepted prefix
+            na = torch.zeros(1, dtype=torch.int32, device="cuda")
+            nx = torch.zeros(1, dtype=torch.int32, device="cuda")
+            q = torch.zeros((1, gamma), dtype=torch.float32, device="cuda")
+            ctx.correct_kernel(i32([drafts[:gamma]]), i32([len(prompt)]), gamma, 0.3, 0, na, nx, q, None)
+            ctx.kv_rewrite(i32([len(prompt)]), na + 1)
+            torch.cuda.synchronize()
+            outs.append(("verify", na.cpu().numpy(), nx.cpu().numpy(), q.cpu().numpy()))
+            T = len(prompt) + int(na.item()) + 1
+            tok = int(nx.item())
+        to = torch.zeros(1, dtype=torch.int32, device="cuda")
+        lo = torch.zeros((1, V), dtype=torch.float32, device="cuda")
+        na = torch.zeros((1, L), dtype=torch.int32, device="cuda")
+        ga = torch.zeros((1, L, F), dtype=torch.float32, device="cuda")
+        flags = S.SIRIUS_DENSE if i == 2 else 0
+        ctx.sparse_decode_step(i32([tok]), i32([T]), flags, to, lo, na, ga)
+        torch.cuda.synchronize()
+        outs.append(("decode", to.cpu().numpy(), lo.cpu().numpy(), na.cpu().numpy(), ga.cpu().numpy()))
+        tok, T = int(to.item()), T + 1
+        drafts.append(tok)
+    return outs
+
+
+@pytest.fixture(scope="module")
+def l2():
+    cfg = synth.LLAMA3_8B.with_layers(2)
+    return cfg, synth.host_weights(cfg)
+
+
+@pytest.mark.parametrize("model,tp", [("tiny", 2), ("8b2l", 2), ("8b2l", 8)])
+def test_par_emulated_bitwise_equals_inorder_sum(monkeypatch, model, tp):
+    from synth import gpu as sg
+    monkeypatch.setenv("SIRIUS_FFN_ATOMIC", "0")  # deterministic FFN: both runs bitwise reproducible
+    cfg = synth.TINY if model == "tiny" else synth.LLAMA3_8B.with_layers(2)
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 3, 41)
+    shards = [sg.device_weights(cfg, tp, r) for r in range(tp)]
+    ref_ctx = make_ctx(cfg, shards, thr, tp)
+    ref = script(ref_ctx, cfg, prompt)
+    ctx = make_ctx(cfg, shards, thr, tp)
+    ctx.sirius_par_enable(None)
+    got = script(ctx, cfg, prompt)
+    assert len(got) == len(ref)
+    for a, b in zip(got, ref):
+        assert a[0] == b[0]
+        for x, y in zip(a[1:], b[1:]):
+            np.testing.assert_array_equal(x, y)
+
+    # the fused path really ran: per decode step it launches no in-order-sum kernel (2 per layer)
+    # and one argmax_par per rank instead of one argmax_finalize
+    def step_launches(c):
+        to = torch.zeros(1, dtype=torch.int32, device="cuda")
+        n0 = c.launches()
+        c.sparse_decode_step(i32([1]), i32([len(prompt) + 20]), 0, to)
+        torch.cuda.synchronize()
+        return c.launches() - n0
+    assert step_launches(ref_ctx) - step_launches(ctx) == 2 * cfg.n_layers + 1 - tp
+
+
+def test_par_emulated_tp2_free_running_token_exact(l2):
+    """Sirius free-running at 8B-2L shapes, TP 2 emulated with the fused all-reduce and the default
+    (atomic) FFN: tokens and per-kernel advances identical to the TP-1 oracle (prompt chosen free of
+    ambiguity events, as in test_parity_8b_gpu.test_8b2l_free_running_token_exact)."""
+    from paper_2409_03856_b200 import driver
+    from synth import gpu as sg
+    from test_parity_8b_gpu import GAMMA, ambiguity_events
+    cfg, wh = l2
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompt = synth.eval_prompt(cfg, 9, 128)
+    ref = so.generate(so.OracleModel(cfg, wh, max_seq=256, max_gamma=GAMMA), prompt, 48, GAMMA, 0.3, thr)
+    assert ambiguity_events(ref, 0.3) == 0
+    ctx = make_ctx(cfg, [sg.device_weights(cfg, 2, r) for r in range(2)], thr, 2)
+    ctx.sirius_par_enable(None)
+    out = driver.Driver(ctx).sirius([prompt], 48, GAMMA, 0.3)
+    assert out.tokens[0] == ref.tokens
+    assert out.advances(0) == ref.advances[:len(out.kernels)]
+
+
+def test_par_loopback_stub_runs(monkeypatch):
+    """SIRIUS_DEBUG_STUB_COMM + sirius_par_enable: one rank's TP-8 shard with every push looped back
+    into its own buffer (the per-rank timing proxy of tools/tp_proxy.py): runs, no device error."""
+    from synth import gpu as sg
+    monkeypatch.setenv("SIRIUS_DEBUG_STUB_COMM", "1")
+    cfg = synth.LLAMA3_8B.with_layers(2)
+    thr = synth.layer_thresholds(cfg, 0.5)
+    from paper_2409_03856_b200 import sirius as S
+    # stub contexts take a dummy communicator handle (never used: every collective is skipped)
+    ctx = S.Sirius(cfg, sg.device_weights(cfg, 8, 0), thr, batch=1, max_seq=256, max_gamma=16, tp_size=8,
+                   tp_rank=0, nccl_comm=1)
+    ctx.sirius_par_enable(None)
+    outs = script(ctx, cfg, synth.eval_prompt(cfg, 2, 30), steps=6)
+    for o in outs:
+        if o[0] == "decode":
+            assert np.isfinite(o[2]).all()
+
+
+def test_par_abi_errors():
+    from paper_2409_03856_b200 import sirius as S
+    from synth import gpu as sg
+    cfg = synth.TINY
+    thr = synth.layer_thresholds(cfg, 0.5)
+    one = make_ctx(cfg, sg.device_weights(cfg), thr, 1)
+    with pytest.raises(S.SiriusError) as e:
+        one.sirius_par_enable(None)
+    assert e.value.status == -6  # UNSUPPORTED: tp_size 1
+    emu = make_ctx(cfg, [sg.device_weights(cfg, 2, r) for r in range(2)], thr, 2)
+    with pytest.raises(S.SiriusError) as e:
+        emu.sirius_par_export()
+    assert e.value.status == -3  # STATE: nothing to export from an emulated group
+    with pytest.raises(S.SiriusError) as e:
+        emu.sirius_par_enable([b"\0" * S.PAR_HANDLE_BYTES] * 2)
+    assert e.value.status == -1  # INVALID_ARG: emulated contexts take no handles

@@ -45,6 +45,9 @@ def _rank_main(rank, world, port, q):
         uid = TP.broadcast_id(rank, lambda: bytes(range(128)))
         assert uid == bytes(range(128))
         assert TP.max_over_ranks(1.5 + rank) == 1.5 + world - 1
+        # fused peer all-reduce bootstrap: every rank's IPC handle, in rank order, everywhere
+        hs = TP.exchange_handles(bytes([rank]) * 64, 64)
+        assert hs == [bytes([r]) * 64 for r in range(world)]
         TP.barrier()
         # ---- sharded CATS MLP, all-reduced
         cfg = synth.TINY

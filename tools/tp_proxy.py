@@ -7,7 +7,11 @@ multi-GPU measurement: the all-reduce latency must be added (6
 kernel shape fixed (advance = gamma) and the Sirius number is reported per committed token at
 AAL = gamma and, as a model, at the TP-1 bench's AAL.
 
-    python tools/tp_proxy.py --model llama3-8b --tp 8 [--batch 1] [--gamma 16] [--steps 8]
+    python tools/tp_proxy.py --model llama3-8b --tp 8 [--batch 1] [--gamma 16] [--steps 8] [--par]
+
+--par: the fused peer all-reduce in loopback (sirius_par_enable on a stub context): the decode step's
+pushes, flag stores and waits run on-chip against the rank's own buffer (every "peer" is itself), so
+the proxy then includes the fused all-reduce's in-kernel cost — all but the NVLink transfer latency.
 """
 import argparse, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -27,6 +31,7 @@ ap.add_argument("--steps", type=int, default=8)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--rho", type=float, default=0.5)
 ap.add_argument("--out", default=None)
+ap.add_argument("--par", action="store_true")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.model]
 t0 = time.time()
@@ -35,6 +40,8 @@ thr = synth.layer_thresholds(cfg, a.rho)
 B, g = a.batch, a.gamma
 max_seq = a.prompt + (a.warmup + a.steps + 4) * g + 256
 ctx = S.Sirius(cfg, w, thr, batch=B, max_seq=max_seq, max_gamma=g, tp_size=a.tp, tp_rank=0, nccl_comm=1)
+if a.par:
+    ctx.sirius_par_enable(None)
 drv = driver.Driver(ctx)
 prompts = [synth.eval_prompt(cfg, b, a.prompt) for b in range(B)]
 drv.begin(prompts)
@@ -67,14 +74,17 @@ ck = clk.stop()
 tp_per_rank = dict(ffn=cfg.ffn_dim // a.tp, heads=cfg.n_heads // a.tp, kv_heads=cfg.n_kv_heads // a.tp,
                    vocab=cfg.vocab // a.tp)
 dense_bytes = bench.step_bytes(cfg, a.tp, drv.T[0], None, B)
-res = {"what": f"{a.model} TP{a.tp} per-rank compute proxy on 1 B200 (collectives skipped)", "batch": B,
+what = (f"{a.model} TP{a.tp} per-rank proxy on 1 B200, decode all-reduces fused + looped back on-chip "
+        "(verify collectives skipped)") if a.par else f"{a.model} TP{a.tp} per-rank compute proxy on 1 B200 (collectives skipped)"
+res = {"what": what, "fused_peer_allreduce_loopback": a.par, "batch": B,
        "gamma": g, "prompt": a.prompt, "shard": tp_per_rank,
        "dense_ms_per_token": base["dense"], "cs_only_ms_per_token": base["cs_only"],
        "sirius_ms_per_kernel": t_kernel, "sirius_ms_per_token_at_aal_gamma": t_kernel / g,
        "dense_hbm_gbs": dense_bytes / (base["dense"] / 1e3) / 1e9,
        "dense_bytes_per_rank": dense_bytes,
        "allreduces_per_token": 2 * cfg.n_layers + 1,
-       "note": "add the NVLink all-reduce latency per call (not measured: one GPU)",
+       "note": ("add the NVLink transfer latency of each fused push (not measured: one GPU)" if a.par else
+                "add the NVLink all-reduce latency per call (not measured: one GPU)"),
        "clocks": ck, "setup_s": setup}
 print(json.dumps(res))
 if a.out:
