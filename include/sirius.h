@@ -248,20 +248,22 @@ sirius_status sirius_csparse_enable(sirius_ctx* ctx, float keep_fraction);
  * GPU).  Each rank owns a comm buffer of identical layout
  *   slots [2][tp_size][batch * d_model] fp32 | keys [2][tp_size][8] u64 | flags [2][tp_size] u64
  * that every other rank maps through CUDA IPC.  With the fused path on, sparse_decode_step (the
- * per-stage path, batch <= 4, or 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the last CTA of
- * the O-proj GEMV / CATS FFN / LM-head kernel stores the rank partial (or the packed argmax keys)
- * into its slot on every rank over NVLink and release-stores the sync point's sequence number into
- * the flags; the activation prologue of the next kernel acquire-waits for all tp_size flags and sums
- * the slots in rank order, so every rank computes bitwise the same residual.  prefill, correct_kernel
- * and the batched row path keep the NCCL collectives.
+ * per-stage path, batch <= 4, or 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the CTA that
+ * completes the rank partial of the O-proj GEMV / CATS FFN (or the packed argmax keys of the LM head)
+ * stores it into its slot on every rank over NVLink, release-stores the sync point's sequence number
+ * into the flags, acquire-waits for every rank's flag and writes the rank-order sum over the partial
+ * (the head: the global argmax token), so every rank computes bitwise the same residual and the next
+ * kernel reads it as at TP 1.  prefill, correct_kernel and the batched row path keep the NCCL
+ * collectives.
  *
  * sirius_par_export: HOST handle_out [SIRIUS_PAR_HANDLE_BYTES] = this rank's cudaIpcMemHandle_t.
  *   Errors: STATE for an emulated / stub / tp_size 1 context; CUDA.
  * sirius_par_enable: peer_handles = HOST [tp_size][SIRIUS_PAR_HANDLE_BYTES], every rank's exported
  *   handle in rank order (the own entry is ignored), or NULL for a single-GPU emulated context (the
- *   ranks' buffers are all in this process: the emulated ranks run stage by stage, so every wait is
- *   already satisfied when it starts) or a SIRIUS_DEBUG_STUB_COMM context (loopback timing proxy: every
- *   peer is the rank's own buffer, the consumer sums tp_size copies scaled by 1 / tp_size).  Every rank
+ *   ranks' buffers are all in this process; the emulated ranks run one after another, so each one's
+ *   wait + reduction runs in a separate kernel once all have pushed) or a SIRIUS_DEBUG_STUB_COMM
+ *   context (loopback timing proxy of the fused form: every peer is the rank's own buffer, the
+ *   reduction sums tp_size copies scaled by 1 / tp_size).  Every rank
  *   must call it (collectively, after every rank's sirius_init and export) before its next decode.
  *   Errors: INVALID_ARG (handles given / missing for the context kind); UNSUPPORTED (tp_size 1 or
  *   > 8; a peer buffer cannot be mapped); CUDA.  Synchronous.

@@ -15,20 +15,25 @@ enum InMode : int {
 // sirius_par_enable).  Every rank owns one comm buffer of the same layout, mapped by its
 // peers through CUDA IPC:
 //   slots [2][world][slot_n] fp32 | keys [2][world][key_n] u64 | flags [2][world] u64
-// indexed (parity of the sync point, SOURCE rank).  A producer kernel's last CTA pushes its rank partial
-// into slot (par, rank) of every rank, then release-stores the sync point's sequence number s into flag
-// (par, rank) of every rank; a consumer prologue acquires flags (par, 0..world-1) >= s and sums the
-// slots in rank order (the same order on every rank: identical residuals everywhere).  s counts this
-// rank's sync points (device word, incremented by each producer's last CTA); all ranks make the same
-// sequence of calls, so s agrees.  Two parities suffice: a rank pushes s + 2 only after consuming
-// s + 1, which needs every rank's push of s + 1, which each rank makes only after consuming s.
+// indexed (parity of the sync point, SOURCE rank).  The producer kernel's last CTA (the one that
+// completes the rank partial) pushes it into slot (par, rank) of every rank, release-stores the sync
+// point's sequence number s into flag (par, rank) of every rank, acquire-waits for flags
+// (par, 0..world-1) >= s on its own buffer and writes the sum of the slots, in rank order, over the
+// partial (the same order on every rank: identical residuals everywhere) — so the next kernel reads
+// an all-reduced delta with its usual prologue.  s counts this rank's sync points (device word); all
+// ranks make the same sequence of calls, so s agrees.  Two parities suffice: a rank pushes s + 2 only
+// after reducing s + 1, which needs every rank's push of s + 1, which each rank makes only after
+// reducing s (tests/test_par_protocol.py model-checks this).
 struct PeerAr {
   int world;                   // 0: off
   int rank;                    // source index of this rank's pushes
+  int fused;                   // 1: the producer's last CTA also waits + reduces (real ranks, loopback);
+                               // 0: push only, par_reduce_kernel reduces (single-GPU emulation: the
+                               //    emulated ranks' producers run one after another, none may wait)
   int loopback;                // timing proxy (stub comm): every "peer" is this rank's own buffer and
                                // push q lands in source slot q (same stores, no NVLink)
   int slot_n, key_n;           // floats per slot, u64 keys per key slot
-  float scale;                 // consumer: delta = scale * sum_r slot_r (1; 1 / world in loopback)
+  float scale;                 // reduce: sum_r slot_r * scale (1; 1 / world in loopback)
   char* const* peers;          // DEV [world]: every rank's comm buffer as mapped in this process
   char* self;                  // this rank's comm buffer
   unsigned long long* seq;     // this rank's sync-point counter
@@ -47,8 +52,6 @@ struct Prologue {
   const uint16_t* norm_w;   // [K]
   float eps;
   float* res_out;           // if non-NULL, CTA 0 stores x [B, K] here (never aliases base)
-  int par_consume;          // IN_RESID: delta = the fused peer all-reduce of the last sync point (par)
-  PeerAr par;               // the rank's peer all-reduce (consumer side here; producers: par_produce)
 };
 
 // ---- streaming GEMV: out[b, r] = sum_k W[r, k] * h[b, k]
@@ -68,8 +71,9 @@ struct GemvArgs {
   int32_t* token_out;           // EPI_ARGMAX + finalize: [B]
   float* zero_out;              // if non-NULL: the grid zeroes zero_n floats here (the next FFN's accumulator)
   int zero_n;
-  int par_produce;              // EPI_STORE: the last CTA pushes out [B, d] (ldo == d) to every rank
-                                // (pro.par); EPI_ARGMAX: pushes the packed keys amax [B] and resets them
+  PeerAr par;                   // fused all-reduce (world > 0): EPI_STORE: out [B, d] (ldo == d) is
+                                // all-reduced in place; EPI_ARGMAX: the packed keys amax [B] are
+                                // max-reduced over the ranks (reset to 0) and, fused, -> token_out
 };
 
 // ---- fused CATS FFN (gate GEMV + SiLU + threshold + ballot compaction + up/down gathers)
@@ -94,7 +98,7 @@ struct FfnArgs {
   const float* a_in;
   const unsigned* mask_in;
   long long a_ld, m_ld;
-  int par_produce;         // the last CTA pushes out [B, d] to every rank (pro.par)
+  PeerAr par;              // fused all-reduce (world > 0): out [B, d] is all-reduced in place
 };
 
 

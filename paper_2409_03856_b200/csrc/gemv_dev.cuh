@@ -4,7 +4,6 @@
 #pragma once
 #include "common.cuh"
 #include "decode_kernels.cuh"
-#include "peer_ar.cuh"
 
 namespace sirius {
 namespace dev {
@@ -22,8 +21,6 @@ SIRIUS_DEV void prologue(const Prologue& p, int K, float* h_s, float* red_s, boo
   const int CH = K / 8, NG = K / 4;
   float4* hp = reinterpret_cast<float4*>(h_s);
   auto slot = [&](int b, int g) { return (b * 2 + (g & 1)) * CH + (g >> 1); };  // group g = elements 4g..4g+3
-  // fused peer all-reduce (TP > 1): delta = sum over source ranks of the pushed partials, rank order
-  const float* par_slots = (p.mode == IN_RESID && p.par_consume) ? par::wait(p.par) : nullptr;
   for (int b = 0; b < B; ++b) {
     float4 x[MG];
     if (p.mode == IN_F32) {
@@ -62,28 +59,6 @@ SIRIUS_DEV void prologue(const Prologue& p, int K, float* h_s, float* red_s, boo
         if (g < NG) {
           x[j] = __ldcg(base + g);
           dl[j] = delta ? __ldcg(delta + g) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-      if (par_slots) {  // same order as the emulated in-order sum: ((s_0 + s_1) + s_2) + ..., then x + delta
-        for (int r = 0; r < p.par.world; ++r) {
-          const float4* sr = reinterpret_cast<const float4*>(par_slots + (size_t)r * p.par.slot_n + (size_t)b * K);
-#pragma unroll
-          for (int j = 0; j < MG; ++j) {
-            const int g = tid + NT * j;
-            if (g < NG) {
-              const float4 v = __ldcg(sr + g);
-              if (r == 0) {
-                dl[j] = v;
-              } else {
-                dl[j].x += v.x; dl[j].y += v.y; dl[j].z += v.z; dl[j].w += v.w;
-              }
-            }
-          }
-        }
-        const float sc = p.par.scale;
-#pragma unroll
-        for (int j = 0; j < MG; ++j) {
-          dl[j].x *= sc; dl[j].y *= sc; dl[j].z *= sc; dl[j].w *= sc;
         }
       }
 #pragma unroll

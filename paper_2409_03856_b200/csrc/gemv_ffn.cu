@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "decode_kernels.cuh"
 #include "gemv_dev.cuh"
+#include "peer_ar.cuh"
 
 namespace sirius {
 namespace {
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
     }
   }
   if (a.epi != EPI_ARGMAX) {
-    if (a.par_produce) par::push_last(a.pro.par, a.out, B * a.ldo, nullptr, 0);  // fused all-reduce (TP > 1)
+    if (a.par.world) par::push_last(a.par, a.out, B * a.ldo, nullptr, 0, nullptr);  // fused all-reduce (TP > 1)
     return;
   }
   if (lane == 0)
@@ -95,8 +96,8 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
     for (int w = 0; w < kGemvWarps; ++w) k = key_s[w * B + tid] > k ? key_s[w * B + tid] : k;
     atomicMax(a.amax + tid, k);
   }
-  if (a.par_produce) {  // TP > 1: the rank's packed keys go to every rank; argmax_par_kernel reduces them
-    par::push_last(a.pro.par, nullptr, 0, a.amax, B);
+  if (a.par.world) {  // TP > 1: the rank's packed keys go to every rank, max-reduced -> token (fused)
+    par::push_last(a.par, nullptr, 0, a.amax, B, a.token_out);
     return;
   }
   if (a.finalize) {
@@ -129,18 +130,13 @@ __global__ void argmax_finalize_kernel(unsigned long long* amax, int B, int32_t*
   }
 }
 
-// TP > 1 with the fused peer all-reduce: wait for every rank's packed keys of this sync point and
-// reduce them (max = the global lowest-index argmax, as the NCCL max-all-reduce) -> token
-__global__ void argmax_par_kernel(PeerAr p, int B, int32_t* token_out) {
-  par::wait(p);
-  const int par = (int)(__ldcg(p.seq) & 1ull);
-  const unsigned long long* k = par::keys(p, par);
-  const int b = threadIdx.x;
-  if (b < B) {
-    unsigned long long m = 0ull;
-    for (int r = 0; r < p.world; ++r) m = k[(size_t)r * p.key_n + b] > m ? k[(size_t)r * p.key_n + b] : m;
-    token_out[b] = (int32_t)argmax_key_index(m);
-  }
+// Single-GPU TP emulation of the fused all-reduce (PeerAr.fused = 0): after every emulated rank's
+// producer has pushed, each rank's reduction runs here — the same wait + rank-order reduction the
+// producer's last CTA runs when fused (dst: the partial, all-reduced in place; keys -> token_out)
+__global__ void par_reduce_kernel(PeerAr p, float* dst, int n, int nk, int32_t* token_out) {
+  const unsigned long long s = __ldcg(p.seq);
+  par::wait_flags(p, s);
+  par::reduce(p, (int)(s & 1ull), dst, n, nk, nullptr, token_out);
 }
 
 // ===================================================================== fused CATS FFN
@@ -319,7 +315,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
       for (int c = 0; c < nch; ++c) cnt += __popc(act_s[c][tid]);
       if (cnt) atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, cnt);
     }
-    if (a.par_produce) par::push_last(a.pro.par, a.out, B * d, nullptr, 0);  // fused all-reduce (TP > 1)
+    if (a.par.world) par::push_last(a.par, a.out, B * d, nullptr, 0, nullptr);  // fused all-reduce (TP > 1)
     fstamp(a, 6);
     return;
   }
@@ -359,7 +355,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
     for (int p = 0; p < G; ++p) tot += __ldcg(a.part_cnt + p * B + tid);
     atomicAdd(a.n_active_out + (size_t)tid * a.n_active_stride, tot);
   }
-  if (a.par_produce) par::push_last(a.pro.par, a.out, B * d, nullptr, 0);  // fused all-reduce (TP > 1)
+  if (a.par.world) par::push_last(a.par, a.out, B * d, nullptr, 0, nullptr);  // fused all-reduce (TP > 1)
 }
 
 }  // namespace
@@ -389,8 +385,8 @@ static cudaError_t gemv_b(const GemvArgs& a, int grid, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t argmax_par(const PeerAr& p, int B, int32_t* token_out, cudaStream_t st) {
-  argmax_par_kernel<<<1, 32, 0, st>>>(p, B, token_out);
+cudaError_t par_reduce(const PeerAr& p, float* dst, int n, int nk, int32_t* token_out, cudaStream_t st) {
+  par_reduce_kernel<<<1, 256, 0, st>>>(p, dst, n, nk, token_out);
   return cudaGetLastError();
 }
 

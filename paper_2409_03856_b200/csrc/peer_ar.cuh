@@ -1,10 +1,9 @@
 // peer_ar.cuh — the fused peer all-reduce of the tensor-parallel decode step (SURVEY.md §8(e) phase 2;
 // the all-reduces of S3 / S6 / S7 in SURVEY.md §8(a)): device side of the protocol documented at
-// PeerAr (decode_kernels.cuh).  The producer half runs in the epilogue of the kernel that computes the
-// rank partial (O-proj GEMV, CATS FFN, LM-head argmax), the consumer half in the activation prologue of
-// the kernel that needs the sum (FFN, next layer's QKV GEMV, LM head) — no separate collective launch:
-// the push goes out over NVLink (peer stores through CUDA-IPC mappings) the moment the partial is
-// complete, and the consumer's wait overlaps its first weight rows already in flight.
+// PeerAr (decode_kernels.cuh).  It runs in the tail of the kernel that computes the rank partial
+// (O-proj GEMV, CATS FFN, LM-head argmax): the CTA that completes the partial pushes it over NVLink
+// (peer stores through CUDA-IPC mappings), waits for the peers' pushes and reduces them in place — no
+// collective launch, and the next kernel's prologue reads the all-reduced delta as at TP 1.
 #pragma once
 #include "common.cuh"
 #include "decode_kernels.cuh"
@@ -32,13 +31,10 @@ SIRIUS_DEV unsigned long long globaltimer() {
   return t;
 }
 
-// Consumer: every thread of the CTA calls it.  Waits until every source rank's push of this rank's
-// current sync point s (= *seq, incremented by the producer kernel that ran just before in stream
-// order) has landed, then returns this rank's slot array of parity s & 1 ([world][slot_n], local
-// memory).  A rank that does not arrive within 10 s sets kErrTimeout and the wait gives up (the
-// results are then garbage, the next ABI call reports the error).
-SIRIUS_DEV const float* wait(const PeerAr& p) {
-  const unsigned long long s = __ldcg(p.seq);
+// threads < world acquire-wait for flags (par, 0..world-1) >= s on this rank's buffer; CTA barrier.
+// A rank that does not arrive within 10 s sets kErrTimeout and the wait gives up (the results are
+// then garbage, the next ABI call reports SIRIUS_ERR_NCCL).
+SIRIUS_DEV void wait_flags(const PeerAr& p, unsigned long long s) {
   const int par = (int)(s & 1ull);
   if (threadIdx.x < (unsigned)p.world) {
     const unsigned long long* f =
@@ -58,19 +54,55 @@ SIRIUS_DEV const float* wait(const PeerAr& p) {
     }
   }
   __syncthreads();
-  return reinterpret_cast<const float*>(p.self) + (size_t)par * p.world * p.slot_n;
 }
 
-// this rank's received key slots of parity par ([world][key_n])
-SIRIUS_DEV const unsigned long long* keys(const PeerAr& p, int par) {
-  return reinterpret_cast<const unsigned long long*>(p.self + off_keys(p)) + (size_t)par * p.world * p.key_n;
+// every thread of the CTA: dst[0, n) = scale * ((slot_0 + slot_1) + ... + slot_{world-1}) of parity par
+// (rank order, as the emulated in-order sum), and for the keys: the max over the ranks -> token_out
+// (argmax_key_index) when token_out != NULL, else -> keys_out
+SIRIUS_DEV void reduce(const PeerAr& p, int par, float* dst, int n, int nk, unsigned long long* keys_out,
+                       int32_t* token_out) {
+  const int W = p.world;
+  const float* slots = reinterpret_cast<const float*>(p.self) + (size_t)par * W * p.slot_n;
+  constexpr int GU = 2;  // float4 groups per thread per round: GU * kMaxWorld loads in flight
+  for (int i0 = threadIdx.x; i0 < n / 4; i0 += GU * blockDim.x) {
+    float4 v[GU][kMaxWorld];
+#pragma unroll
+    for (int u = 0; u < GU; ++u)
+#pragma unroll
+      for (int r = 0; r < kMaxWorld; ++r) {
+        const int i = i0 + u * blockDim.x;
+        if (r < W && i < n / 4) v[u][r] = __ldcg(reinterpret_cast<const float4*>(slots + (size_t)r * p.slot_n) + i);
+      }
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= n / 4) continue;
+      float4 a = v[u][0];
+#pragma unroll
+      for (int r = 1; r < kMaxWorld; ++r)
+        if (r < W) {
+          a.x += v[u][r].x; a.y += v[u][r].y; a.z += v[u][r].z; a.w += v[u][r].w;
+        }
+      a.x *= p.scale; a.y *= p.scale; a.z *= p.scale; a.w *= p.scale;
+      reinterpret_cast<float4*>(dst)[i] = a;
+    }
+  }
+  const unsigned long long* ks =
+      reinterpret_cast<const unsigned long long*>(p.self + off_keys(p)) + (size_t)par * W * p.key_n;
+  for (int b = threadIdx.x; b < nk; b += blockDim.x) {
+    unsigned long long m = 0ull;
+    for (int r = 0; r < W; ++r) m = ks[(size_t)r * p.key_n + b] > m ? ks[(size_t)r * p.key_n + b] : m;
+    if (token_out) token_out[b] = (int32_t)argmax_key_index(m);
+    else keys_out[b] = m;
+  }
 }
 
 // Producer: every thread of every CTA calls it once the CTA's contribution to src (n floats, n % 4 ==
 // 0, written by plain stores or atomics) / to the packed keys (nk words, atomicMax) is complete.  The
 // CTA that arrives last pushes src and keys to every rank (the keys are reset to 0 for the next step),
-// then publishes the new sequence number.
-SIRIUS_DEV void push_last(const PeerAr& p, const float* src, int n, unsigned long long* keys_io, int nk) {
+// publishes the new sequence number and, fused, waits for every rank's push and writes the reduced
+// sum over src (keys: the global argmax -> token_out).
+SIRIUS_DEV void push_last(const PeerAr& p, float* src, int n, unsigned long long* keys_io, int nk, int32_t* token_out) {
   __shared__ unsigned last_s;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -92,13 +124,24 @@ SIRIUS_DEV void push_last(const PeerAr& p, const float* src, int n, unsigned lon
   const unsigned long long s = __ldcg(p.seq) + 1ull;
   const int par = (int)(s & 1ull);
   const size_t slot0 = (size_t)par * W * p.slot_n;
-  for (int i = threadIdx.x; i < n / 4; i += blockDim.x) {
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(src) + i);
+  constexpr int GU = 8;  // float4 groups per thread loaded before any store
+  for (int i0 = threadIdx.x; i0 < n / 4; i0 += GU * blockDim.x) {
+    float4 v[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n / 4) v[u] = __ldcg(reinterpret_cast<const float4*>(src) + i);
+    }
 #pragma unroll
     for (int q = 0; q < kMaxWorld; ++q)
       if (q < W) {
-        const int si = p.loopback ? q : p.rank;
-        reinterpret_cast<float4*>(reinterpret_cast<float*>(pb[q]) + slot0 + (size_t)si * p.slot_n)[i] = v;
+        float4* dq = reinterpret_cast<float4*>(reinterpret_cast<float*>(pb[q]) + slot0 +
+                                               (size_t)(p.loopback ? q : p.rank) * p.slot_n);
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int i = i0 + u * blockDim.x;
+          if (i < n / 4) dq[i] = v[u];
+        }
       }
   }
   for (int i = threadIdx.x; i < nk; i += blockDim.x) {
@@ -110,13 +153,17 @@ SIRIUS_DEV void push_last(const PeerAr& p, const float* src, int n, unsigned lon
         reinterpret_cast<unsigned long long*>(pb[q] + off_keys(p))[((size_t)par * W + si) * p.key_n + i] = k;
       }
   }
-  __threadfence_system();
+  // the CTA barrier orders every thread's stores before the flag threads' sys-scope release stores
+  // (PTX memory model: bar.sync is morally strong, a release is cumulative over what it observed)
   __syncthreads();
   if (threadIdx.x < (unsigned)W) {
     const int q = threadIdx.x, si = p.loopback ? q : p.rank;
     st_release_sys(reinterpret_cast<unsigned long long*>(pb[q] + off_flags(p)) + (size_t)par * W + si, s);
   }
   if (threadIdx.x == 0) *p.seq = s;
+  if (!p.fused) return;
+  wait_flags(p, s);
+  reduce(p, par, src, n, nk, keys_io, token_out);
 }
 
 }  // namespace par

@@ -24,7 +24,7 @@ int gemv_grid(int rows, int num_sms);
 cudaError_t gemv(const GemvArgs& a, int B, int grid, cudaStream_t st);
 
 cudaError_t argmax_finalize(unsigned long long* amax, int B, int32_t* token_out, cudaStream_t st);
-cudaError_t argmax_par(const PeerAr& p, int B, int32_t* token_out, cudaStream_t st);
+cudaError_t par_reduce(const PeerAr& p, float* dst, int n, int nk, int32_t* token_out, cudaStream_t st);
 int ffn_grid(int F, int num_sms);
 cudaError_t ffn(const FfnArgs& a, int B, int grid, cudaStream_t st);
 bool decode_step_supported(int d, int H, int KV, int hd, int F, int num_sms);
@@ -408,6 +408,7 @@ PeerAr par_of(const sirius_ctx* c, const RankState& R) {
   PeerAr p = {};
   p.world = c->cfg.tp_size;
   p.rank = R.rank;
+  p.fused = c->emulated ? 0 : 1;  // emulated ranks run one after another: none may wait (par_reduce)
   p.loopback = c->par_loopback ? 1 : 0;
   p.slot_n = c->par_slot_n;
   p.key_n = c->par_key_n;
@@ -419,11 +420,13 @@ PeerAr par_of(const sirius_ctx* c, const RankState& R) {
   p.err = c->err_dev;
   return p;
 }
-// consumer prologue: delta = the all-reduced partial of the last sync point
-void par_consume(const sirius_ctx* c, const RankState& R, Prologue& pro) {
-  pro.delta = nullptr;
-  pro.par_consume = 1;
-  pro.par = par_of(c, R);
+// the all-reduce of the partials buf [B, d] of every rank of this context: fused into the producer
+// (nothing to launch), the emulated reduction (every emulated rank has pushed), or NCCL / in-order sums
+sirius_status par_or_allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev, int B, bool par) {
+  if (!par) return allreduce(c, buf, ptrs_dev, B);
+  if (c->emulated)
+    for (auto& R : c->ranks) LCU(launch::par_reduce(par_of(c, R), R.*buf, B * c->cfg.d_model, 0, nullptr, c->stream));
+  return SIRIUS_OK;
 }
 
 // ---- the decode CATS FFN of layer l (S4-S6) on residual rows base (+ delta): out = the FFN's
@@ -483,10 +486,7 @@ sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float*
   f.n_active_out = n_active_out;
   f.n_active_stride = n_active_stride;
   f.atomic_out = c->ffn_atomic ? 1 : 0;
-  if (c->par_on && par_decode) {  // fused peer all-reduce: consume the O-proj sum, push the FFN partial
-    par_consume(c, R, f.pro);
-    f.par_produce = 1;
-  }
+  if (c->par_on && par_decode) f.par = par_of(c, R);  // fused peer all-reduce of the FFN partial
   f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
   f.gate_out = gate_out;
   f.gate_stride = gate_stride;
@@ -1246,7 +1246,6 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
         a.pro.mode = IN_RESID;
         a.pro.base = R.resB;
         a.pro.delta = R.dF;
-        if (par) par_consume(c, R, a.pro);
       }
       a.pro.norm_w = R.attn_norm[l];
       a.pro.eps = cf.rms_eps;
@@ -1298,15 +1297,12 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
         o.zero_out = R.dF;
         o.zero_n = B * d;
       }
-      if (par) {  // push the O-proj partial to every rank (the FFN prologue sums them)
-        o.pro.par = par_of(c, R);
-        o.par_produce = 1;
-      }
+      if (par) o.par = par_of(c, R);  // fused peer all-reduce of the O-proj partial
       prof_begin(c, P_OPROJ);
       OK(run_gemv(c, o, B));
       prof_end(c);
     }
-    if (!par) OK(allreduce(c, &RankState::dA, c->dA_ptrs, B));
+    OK(par_or_allreduce(c, &RankState::dA, c->dA_ptrs, B, par));
     for (auto& R : c->ranks) {
       float* g_out = nullptr;
       long long g_stride = 0;
@@ -1320,7 +1316,7 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
                            g_out, g_stride, csparse, topk, par));
       prof_end(c);
     }
-    if (!par) OK(allreduce(c, &RankState::dF, c->dF_ptrs, B));
+    OK(par_or_allreduce(c, &RankState::dF, c->dF_ptrs, B, par));
   }
   for (auto& R : c->ranks) {
     GemvArgs a = {};
@@ -1341,16 +1337,14 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
     a.finalize = (cf.tp_size == 1);
     a.done_counter = R.head_cnt;
     a.token_out = token_out;
-    if (par) {  // consume the last FFN sum, push the rank's packed argmax keys
-      par_consume(c, R, a.pro);
-      a.par_produce = 1;
-    }
+    if (par) a.par = par_of(c, R);  // the packed argmax keys max-reduced over the ranks -> token
     prof_begin(c, P_HEAD);
     OK(run_gemv(c, a, B));
     prof_end(c);
   }
   if (par) {
-    for (auto& R : c->ranks) LCU(launch::argmax_par(par_of(c, R), B, token_out, c->stream));
+    if (c->emulated)
+      for (auto& R : c->ranks) LCU(launch::par_reduce(par_of(c, R), nullptr, 0, B, token_out, c->stream));
   } else if (cf.tp_size > 1) {
     if (!c->emulated && !c->stub_comm) {
       NcclApi& api = nccl();

@@ -2,10 +2,13 @@
 sirius_par_enable; csrc/peer_ar.cuh) on one GPU.
 
 One GPU cannot host ranks whose kernels wait on one another (B200_PROFILING.md), so the ranks are
-emulated in one context: every rank's kernel of a stage runs before any rank's kernel of the next
-stage, so each consumer's flag wait is already satisfied when it starts — the pushes, the slot /
-flag addressing, the sequence numbers, the parities and the rank-order sums all run as on a real
-TP group, through the same kernels.
+emulated in one context: every emulated rank's producer kernel (O-proj GEMV, CATS FFN, LM head)
+pushes as on a real rank, and the wait + rank-order reduction that a real rank's last CTA runs
+right after its push (PeerAr.fused) runs, for each emulated rank, in par_reduce_kernel once all of
+them have pushed — the same device code (csrc/peer_ar.cuh), so the pushes, the slot / flag
+addressing, the sequence numbers, the parities and the reduction order are exercised as on a real
+TP group.  The fused form itself (push, wait and reduce in the producer's last CTA) runs on one GPU
+in loopback (every peer is the rank's own buffer).
 
   * bitwise: with the deterministic FFN reduction, the fused path reproduces the in-order-sum
     emulation (the NCCL stand-in) bit for bit — tokens, logits, active counts, gate activations —
@@ -13,7 +16,7 @@ TP group, through the same kernels.
     fused: the sequence numbers must survive them);
   * oracle: the whole Sirius loop free-running at 8B-2L shapes, TP 2, fused path with the default
     atomic FFN, token-exact against the TP-1 oracle;
-  * loopback stub (the per-rank timing proxy): runs, finite, no device error;
+  * loopback stub (the per-rank timing proxy, fused form): runs, finite, no device error;
   * ABI errors.
 The real multi-process path (CUDA IPC handles) is tests/test_tp_nccl_gpu.py (>= 2 GPUs).
 """
@@ -95,15 +98,15 @@ def test_par_emulated_bitwise_equals_inorder_sum(monkeypatch, model, tp):
         for x, y in zip(a[1:], b[1:]):
             np.testing.assert_array_equal(x, y)
 
-    # the fused path really ran: per decode step it launches no in-order-sum kernel (2 per layer)
-    # and one argmax_par per rank instead of one argmax_finalize
+    # the peer all-reduce really ran: per decode step, instead of 2 in-order sums per layer and one
+    # argmax_finalize, one par_reduce per emulated rank at each of the 2 L + 1 sync points
     def step_launches(c):
         to = torch.zeros(1, dtype=torch.int32, device="cuda")
         n0 = c.launches()
         c.sparse_decode_step(i32([1]), i32([len(prompt) + 20]), 0, to)
         torch.cuda.synchronize()
         return c.launches() - n0
-    assert step_launches(ref_ctx) - step_launches(ctx) == 2 * cfg.n_layers + 1 - tp
+    assert step_launches(ctx) - step_launches(ref_ctx) == (2 * cfg.n_layers + 1) * (tp - 1)
 
 
 def test_par_emulated_tp2_free_running_token_exact(l2):

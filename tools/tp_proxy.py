@@ -70,6 +70,12 @@ for name, dense in (("dense", True), ("cs_only", False)):
     f1.record(st)
     torch.cuda.synchronize()
     base[name] = f0.elapsed_time(f1) / 64
+# per kernel class: device us per CS decode step (CUDA events around every launch, graphs on)
+ctx.profile(True)
+drv.greedy_run(drv.pending, T0, 16, False)
+torch.cuda.synchronize()
+prof = {k: v[0] * 1e3 / 16 for k, v in ctx.profile_read().items() if v[1]}
+ctx.profile(False)
 ck = clk.stop()
 tp_per_rank = dict(ffn=cfg.ffn_dim // a.tp, heads=cfg.n_heads // a.tp, kv_heads=cfg.n_kv_heads // a.tp,
                    vocab=cfg.vocab // a.tp)
@@ -85,6 +91,7 @@ res = {"what": what, "fused_peer_allreduce_loopback": a.par, "batch": B,
        "allreduces_per_token": 2 * cfg.n_layers + 1,
        "note": ("add the NVLink transfer latency of each fused push (not measured: one GPU)" if a.par else
                 "add the NVLink all-reduce latency per call (not measured: one GPU)"),
+       "cs_step_device_us_by_kernel_class": prof,
        "clocks": ck, "setup_s": setup}
 print(json.dumps(res))
 if a.out:
