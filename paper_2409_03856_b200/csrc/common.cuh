@@ -75,7 +75,10 @@ SIRIUS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); 
 SIRIUS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 namespace launch {
-extern bool g_chain_pdl;  // verify / prefill chain launched with PDL (runtime.cu; SIRIUS_VERIFY_PDL)
+extern bool g_chain_pdl;   // verify / prefill chain launched with PDL (runtime.cu; SIRIUS_VERIFY_PDL)
+extern bool g_decode_pdl;  // per-stage decode chain (QKV / O / head GEMV, attention, CATS FFN) with PDL
+                           // (runtime.cu; SIRIUS_DECODE_PDL): each kernel streams its first weight rows
+                           // before griddepcontrol.wait and triggers its dependent right after it
 // <<<grid, block, smem, st>>> with the programmatic-stream-serialization attribute when g_chain_pdl
 template <class... KArgs, class... Args>
 inline cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -92,7 +95,28 @@ inline cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, s
   cfg.numAttrs = g_chain_pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
 }
+// the same with an explicit PDL switch
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
 }  // namespace launch
+
+// L2 prefetch of a contiguous byte range (bulk; bytes % 16 == 0): no registers, no completion
+SIRIUS_DEV void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // ------------------------------------------------------------------ loads
 SIRIUS_DEV uint4 ld_nc_v4(const void* p) {

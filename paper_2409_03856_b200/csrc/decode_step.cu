@@ -732,6 +732,10 @@ __global__ void __launch_bounds__(kNT, 1) attn_stage_kernel(StepArgs a, int l) {
   constexpr int NL = kKB * HD / 8 / kNT > 0 ? kKB * HD / 8 / kNT : 1;
   uint4 kv[NL], vv[NL];
   if (it.active && it.k0 < it.k1) attn_load_block<HD>(a, l, it, it.k0, kv, vv);
+  // PDL (decode chain): the positions are inputs of the step and the cached K/V rows below pos were
+  // final before the step; the q / k / v of the QKV GEMV (the predecessor) only after the wait
+  pdl_wait();
+  pdl_trigger();
   attention_phase<B, HD, G, true>(a, l, sm, it, kv, vv);
 }
 
@@ -741,8 +745,7 @@ cudaError_t launch_attn_stage(const StepArgs& a, int l, cudaStream_t st) {
   const size_t smem = (sizeof(StepSmem<B, HD, G>) + 127) / 128 * 128;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<B * a.KVr * a.splits, kNT, smem, st>>>(a, l);
-  return cudaGetLastError();
+  return launch::launch_pdl(launch::g_decode_pdl, kern, dim3(B * a.KVr * a.splits), dim3(kNT), smem, st, a, l);
 }
 
 template <int HD, int G>

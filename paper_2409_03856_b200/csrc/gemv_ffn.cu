@@ -55,6 +55,13 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
   // it); afterwards each row's loads go out before the previous row's reduction
   RowRegs<CPL> pf;
   row_issue<CPL>(pf, a.W + (size_t)(r0 + warp) * K, CH, lane, r0 + warp < r1, pol);
+  if (a.pf_rows > 0 && tid == 0) {  // the next rows of the CTA (contiguous) into L2 while waiting
+    const int p0 = r0 + kGemvWarps, p1 = min(r1, p0 + a.pf_rows);
+    if (p1 > p0) prefetch_l2_bulk(a.W + (size_t)p0 * K, (uint32_t)((size_t)(p1 - p0) * K * 2));
+  }
+  // PDL (decode chain): everything above reads weights only; the predecessor's outputs after the wait
+  pdl_wait();
+  pdl_trigger();
   if (a.zero_out) {  // the next FFN's accumulator (its previous contents were consumed upstream)
     const int z0 = (int)((long long)a.zero_n * blockIdx.x / gridDim.x);
     const int z1 = (int)((long long)a.zero_n * (blockIdx.x + 1) / gridDim.x);
@@ -175,6 +182,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   const uint64_t pol = policy_evict_first();
   RowRegs<CPL> pf;  // first gate row of the warp, requested before the activation prologue
   row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn && !a.a_in, pol);
+  if (a.pf_rows > 0 && tid == 0 && !a.a_in) {  // the next gate rows of the CTA into L2 while waiting
+    const int p0 = n0 + NW, p1 = min(n1, p0 + a.pf_rows);
+    if (p1 > p0) prefetch_l2_bulk(a.w_gate + (size_t)p0 * d, (uint32_t)((size_t)(p1 - p0) * d * 2));
+  }
+  pdl_wait();  // PDL (decode chain): only weights were read above
+  pdl_trigger();
   constexpr int MG = CPL * 2 / NW > 0 ? CPL * 2 / NW : 1;  // prologue float4 groups per thread (d = 256 CPL)
   prologue<B, MG>(a.pro, d, h_s, red_s, cta == 0);
   fstamp(a, 1);
@@ -369,8 +382,7 @@ static cudaError_t gemv_bc(const GemvArgs& a, int grid, cudaStream_t st) {
   const size_t smem = (size_t)B * a.K * 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kGemvWarps * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(g_decode_pdl, kern, dim3(grid), dim3(kGemvWarps * 32), smem, st, a);
 }
 
 template <int B>
@@ -433,7 +445,12 @@ static cudaError_t ffn_bc(const FfnArgs& a, int grid, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier (deterministic mode)
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = a.atomic_out ? 0 : 1;
+  cfg.numAttrs = 1;
+  if (a.atomic_out) {  // no grid barrier: PDL instead of the cooperative attribute (decode chain)
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = g_decode_pdl ? 1 : 0;
+  }
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -311,6 +311,7 @@ __global__ void sum_ranks_kernel(float* const* bufs, int nranks, size_t n, size_
 namespace launch {
 
 bool g_chain_pdl = true;
+bool g_decode_pdl = true;  // measured: Sirius 2.653 -> 2.572 ms/token (tools/ab_env.sh)
 #define LAUNCH_CHECK(x)                 \
   do {                                  \
     const cudaError_t e_ = (x);         \
