@@ -100,6 +100,9 @@ struct FfnArgs {
   const unsigned* mask_in;
   long long a_ld, m_ld;
   int pf_rows;             // PDL: gate rows after the first batch prefetched into L2 before the wait
+  int pf_down;             // first active down rows prefetched into L2 at the start of the up phase
+  int pf_mode;             // L2 prefetch of active rows: 1 up rows during the gate phase, 2 down rows
+                           // during the up phase, 4 down rows during the gate phase
   PeerAr par;              // fused all-reduce (world > 0): out [B, d] is all-reduced in place
 };
 

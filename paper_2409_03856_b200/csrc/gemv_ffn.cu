@@ -205,10 +205,19 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
     row_finish<B, CPL>(pf, a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc);
     row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + i + kFfnWarps) * d + after_all<B>(acc), CH, lane, i + kFfnWarps < nn,
                    pol);
+    bool on = false;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float g = warp_sum(acc[b]);
-      if (lane == 0) a_s[b][i] = g / (1.0f + expf(-g));
+      const float av = g / (1.0f + expf(-g));
+      if (lane == 0) a_s[b][i] = av;
+      on = on || fabsf(av) >= t;
+    }
+    // an active neuron's W_up (and W_down) rows go to L2 the moment the gate row decides it, so the
+    // up / down phases find them there (SIRIUS_FFN_PF bits 0 / 2; same bytes, issued earlier)
+    if ((a.pf_mode & 5) && lane == 0 && on && !a.dense && !a.mask_in) {
+      if (a.pf_mode & 1) prefetch_l2_bulk(a.w_up + (size_t)(n0 + i) * d, (uint32_t)d * 2);
+      if (a.pf_mode & 4) prefetch_l2_bulk(a.w_down + (size_t)(n0 + i) * d, (uint32_t)d * 2);
     }
   }
   __syncthreads();
@@ -255,6 +264,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   // ---- C: active up rows only: u = h2 . W_up[n];  m = a * u  (inactive (b, n) pairs contribute 0)
   // (each warp's next up row requested before the current row's reduction, as for the gate rows)
   row_issue<CPL>(pf, a.w_up + (size_t)(n0 + list_s[warp < nact ? warp : 0]) * d, CH, lane, warp < nact, pol);
+  // the first active down rows into L2 while the up rows stream (fills the up -> down phase bubble)
+  if (a.pf_down > 0 && tid < a.pf_down && tid < nact)
+    prefetch_l2_bulk(a.w_down + (size_t)(n0 + list_s[tid]) * d, (uint32_t)d * 2);
   for (int k = warp; k < nact; k += kFfnWarps) {
     const int i = list_s[k];
     float acc[B];
@@ -267,6 +279,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
       const float u = warp_sum(acc[b]);
       if (lane == 0) m_s[b][k] = ((bits_s[k] >> b) & 1u) ? a_s[b][i] * u : 0.f;
     }
+    if ((a.pf_mode & 2) && lane == 0) prefetch_l2_bulk(a.w_down + (size_t)(n0 + i) * d, (uint32_t)d * 2);
   }
   __syncthreads();
   fstamp(a, 4);
