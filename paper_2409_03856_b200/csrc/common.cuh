@@ -113,11 +113,6 @@ inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
 }
 }  // namespace launch
 
-// L2 prefetch of a contiguous byte range (bulk; bytes % 16 == 0): no registers, no completion
-SIRIUS_DEV void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 // ------------------------------------------------------------------ loads
 SIRIUS_DEV uint4 ld_nc_v4(const void* p) {
   uint4 r;

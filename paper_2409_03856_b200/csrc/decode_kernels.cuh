@@ -71,7 +71,6 @@ struct GemvArgs {
   int32_t* token_out;           // EPI_ARGMAX + finalize: [B]
   float* zero_out;              // if non-NULL: the grid zeroes zero_n floats here (the next FFN's accumulator)
   int zero_n;
-  int pf_rows;                  // PDL: weight rows after the first batch prefetched into L2 before the wait
   PeerAr par;                   // fused all-reduce (world > 0): EPI_STORE: out [B, d] (ldo == d) is
                                 // all-reduced in place; EPI_ARGMAX: the packed keys amax [B] are
                                 // max-reduced over the ranks (reset to 0) and, fused, -> token_out
@@ -99,10 +98,6 @@ struct FfnArgs {
   const float* a_in;
   const unsigned* mask_in;
   long long a_ld, m_ld;
-  int pf_rows;             // PDL: gate rows after the first batch prefetched into L2 before the wait
-  int pf_down;             // first active down rows prefetched into L2 at the start of the up phase
-  int pf_mode;             // L2 prefetch of active rows: 1 up rows during the gate phase, 2 down rows
-                           // during the up phase, 4 down rows during the gate phase
   PeerAr par;              // fused all-reduce (world > 0): out [B, d] is all-reduced in place
 };
 

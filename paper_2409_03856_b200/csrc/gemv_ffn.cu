@@ -55,10 +55,6 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(GemvArgs a) {
   // it); afterwards each row's loads go out before the previous row's reduction
   RowRegs<CPL> pf;
   row_issue<CPL>(pf, a.W + (size_t)(r0 + warp) * K, CH, lane, r0 + warp < r1, pol);
-  if (a.pf_rows > 0 && tid == 0) {  // the next rows of the CTA (contiguous) into L2 while waiting
-    const int p0 = r0 + kGemvWarps, p1 = min(r1, p0 + a.pf_rows);
-    if (p1 > p0) prefetch_l2_bulk(a.W + (size_t)p0 * K, (uint32_t)((size_t)(p1 - p0) * K * 2));
-  }
   // PDL (decode chain): everything above reads weights only; the predecessor's outputs after the wait
   pdl_wait();
   pdl_trigger();
@@ -182,10 +178,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   const uint64_t pol = policy_evict_first();
   RowRegs<CPL> pf;  // first gate row of the warp, requested before the activation prologue
   row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + warp) * d, CH, lane, warp < nn && !a.a_in, pol);
-  if (a.pf_rows > 0 && tid == 0 && !a.a_in) {  // the next gate rows of the CTA into L2 while waiting
-    const int p0 = n0 + NW, p1 = min(n1, p0 + a.pf_rows);
-    if (p1 > p0) prefetch_l2_bulk(a.w_gate + (size_t)p0 * d, (uint32_t)((size_t)(p1 - p0) * d * 2));
-  }
   pdl_wait();  // PDL (decode chain): only weights were read above
   pdl_trigger();
   constexpr int MG = CPL * 2 / NW > 0 ? CPL * 2 / NW : 1;  // prologue float4 groups per thread (d = 256 CPL)
@@ -205,19 +197,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
     row_finish<B, CPL>(pf, a.w_gate + (size_t)(n0 + i) * d, hp, CH, lane, acc);
     row_issue<CPL>(pf, a.w_gate + (size_t)(n0 + i + kFfnWarps) * d + after_all<B>(acc), CH, lane, i + kFfnWarps < nn,
                    pol);
-    bool on = false;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const float g = warp_sum(acc[b]);
-      const float av = g / (1.0f + expf(-g));
-      if (lane == 0) a_s[b][i] = av;
-      on = on || fabsf(av) >= t;
-    }
-    // an active neuron's W_up (and W_down) rows go to L2 the moment the gate row decides it, so the
-    // up / down phases find them there (SIRIUS_FFN_PF bits 0 / 2; same bytes, issued earlier)
-    if ((a.pf_mode & 5) && lane == 0 && on && !a.dense && !a.mask_in) {
-      if (a.pf_mode & 1) prefetch_l2_bulk(a.w_up + (size_t)(n0 + i) * d, (uint32_t)d * 2);
-      if (a.pf_mode & 4) prefetch_l2_bulk(a.w_down + (size_t)(n0 + i) * d, (uint32_t)d * 2);
+      if (lane == 0) a_s[b][i] = g / (1.0f + expf(-g));
     }
   }
   __syncthreads();
@@ -264,9 +247,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
   // ---- C: active up rows only: u = h2 . W_up[n];  m = a * u  (inactive (b, n) pairs contribute 0)
   // (each warp's next up row requested before the current row's reduction, as for the gate rows)
   row_issue<CPL>(pf, a.w_up + (size_t)(n0 + list_s[warp < nact ? warp : 0]) * d, CH, lane, warp < nact, pol);
-  // the first active down rows into L2 while the up rows stream (fills the up -> down phase bubble)
-  if (a.pf_down > 0 && tid < a.pf_down && tid < nact)
-    prefetch_l2_bulk(a.w_down + (size_t)(n0 + list_s[tid]) * d, (uint32_t)d * 2);
   for (int k = warp; k < nact; k += kFfnWarps) {
     const int i = list_s[k];
     float acc[B];
@@ -279,7 +259,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) ffn_kernel(FfnArgs a
       const float u = warp_sum(acc[b]);
       if (lane == 0) m_s[b][k] = ((bits_s[k] >> b) & 1u) ? a_s[b][i] * u : 0.f;
     }
-    if ((a.pf_mode & 2) && lane == 0) prefetch_l2_bulk(a.w_down + (size_t)(n0 + i) * d, (uint32_t)d * 2);
   }
   __syncthreads();
   fstamp(a, 4);

@@ -150,9 +150,6 @@ struct sirius_ctx {
   size_t gemm_smem = 0;
   bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   int ffn_split = 2;       // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)
-  int pf_rows = 0;         // decode PDL: rows per CTA prefetched into L2 before the wait (SIRIUS_PDL_PF_ROWS)
-  int pf_down = 0;         // CATS FFN: first active down rows per CTA prefetched into L2 (SIRIUS_FFN_PF_DOWN)
-  int ffn_pf_mode = 0;     // CATS FFN: L2 prefetch of active up / down rows (SIRIUS_FFN_PF, FfnArgs.pf_mode)
   bool decode_rows = false;  // batched decode through the tensor-core row path (batch >= 8; SIRIUS_DECODE_ROWS)
   int32_t* dec_nacc = nullptr;
   int attn_stage_splits = 1;
@@ -489,9 +486,6 @@ sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float*
   f.n_active_out = n_active_out;
   f.n_active_stride = n_active_stride;
   f.atomic_out = c->ffn_atomic ? 1 : 0;
-  if (launch::g_decode_pdl && c->ffn_atomic) f.pf_rows = c->pf_rows;
-  f.pf_down = c->pf_down;
-  f.pf_mode = c->ffn_pf_mode;
   if (c->par_on && par_decode) f.par = par_of(c, R);  // fused peer all-reduce of the FFN partial
   f.trace = (c->trace && l == c->trace_layer && c->trace_ffn) ? c->trace : nullptr;
   f.gate_out = gate_out;
@@ -503,9 +497,7 @@ sirius_status launch_decode_ffn(sirius_ctx* c, RankState& R, int l, const float*
 }
 
 // ---- one GEMV (decode) launch
-sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a0, int B) {
-  GemvArgs a = a0;
-  if (launch::g_decode_pdl) a.pf_rows = c->pf_rows;
+sirius_status run_gemv(sirius_ctx* c, const GemvArgs& a, int B) {
   LCU(launch::gemv(a, B, launch::gemv_grid(a.rows, c->num_sms), c->stream));
   return SIRIUS_OK;
 }
@@ -792,9 +784,6 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_DECODE_PDL")) launch::g_decode_pdl = atoi(e) != 0;
-  if (const char* e = getenv("SIRIUS_PDL_PF_ROWS")) c->pf_rows = std::max(0, atoi(e));
-  if (const char* e = getenv("SIRIUS_FFN_PF_DOWN")) c->pf_down = std::max(0, atoi(e));
-  if (const char* e = getenv("SIRIUS_FFN_PF")) c->ffn_pf_mode = std::max(0, atoi(e));
   if (const char* e = getenv("SIRIUS_GEMM_KBOX")) launch::g_gemm_kbox = atoi(e);
   if (const char* e = getenv("SIRIUS_GEMM_COARSE")) launch::g_gemm_coarse = atoi(e);
   auto cleanup_fail = [&](sirius_status s) {
