@@ -1028,6 +1028,7 @@ sirius_status sirius_topk_enable(sirius_ctx* c, float keep_fraction) {
     return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: TP 1 and the per-stage decode path (batch <= 4)");
   const int k = (int)std::floor((double)keep_fraction * c->Fr + 0.5);
   if (k < 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: keep_fraction * ffn rounds to 0");
+  if (c->Fr > 32768) return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: at most 32768 neurons per layer");
   for (auto& R : c->ranks) {
     if (R.tk_g) continue;
     if (alloc(c, &R.tk_g, (size_t)cf.batch * c->Fr) || alloc(c, &R.tk_a, (size_t)cf.batch * c->Fr) ||
@@ -1730,6 +1731,16 @@ int sirius_debug_ffn(sirius_ctx* c, int layer, const float* x, int dense, float*
   OK(launch_decode_ffn(c, c->ranks[0], layer, x, nullptr, nullptr, out, dense != 0, n_active, 1, gate_out, c->Fr));
   CU(cudaStreamSynchronize(c->stream));
   return SIRIUS_OK;
+}
+
+// ---------------------------------------------------------------- test-only entry: top-k selection
+// the exact top-k FSparse selection kernel (topk.cu) on B given gate pre-activation rows g [B, F]:
+// a_out [B, F] = SiLU(g), mask [B, F / 32 + 1] = the k largest |a| (ties to the lower index).
+// Synchronous.  Returns cudaError_t.
+int sirius_debug_topk(const float* g, int F, int k, int B, float* a_out, unsigned* mask) {
+  cudaError_t e = launch::topk_select(g, F, F, k, a_out, F, mask, F / 32 + 1, B, 0);
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaDeviceSynchronize();
 }
 
 // ---------------------------------------------------------------- test-only entry: the decode GEMV

@@ -124,6 +124,8 @@ def load():
         lib.sirius_debug_profile_read.argtypes = [P, P, P]
         lib.sirius_debug_profile_read.restype = I
         lib.sirius_debug_gemm.restype = I
+        lib.sirius_debug_topk.argtypes = [P, I, I, I, P, P]
+        lib.sirius_debug_topk.restype = I
         lib.sirius_debug_gemv.argtypes = [P, I, I, P, I, P, P, P, P, P, P, P, I]
         lib.sirius_debug_gemv.restype = I
         lib.sirius_nccl_available.restype = I
@@ -305,6 +307,16 @@ def debug_gemm(X, W, out, M: int, W2=None) -> None:
     r = lib.sirius_debug_gemm(X.data_ptr(), nterms, rows, W.data_ptr(), _ptr(W2), out.data_ptr(), M, N, K)
     if r != 0:
         raise RuntimeError(f"sirius_debug_gemm failed: {r}")
+
+
+def debug_topk(g, k: int, a_out, mask) -> None:
+    """Test-only: the top-k FSparse selection kernel on g (fp32 [B, F]): a_out [B, F] = SiLU(g), mask
+    (int32 [B, F // 32 + 1], bit i of word i >> 5) = the k largest |a|, ties to the lower index."""
+    lib = load()
+    B, F = g.shape
+    r = lib.sirius_debug_topk(g.data_ptr(), F, int(k), B, a_out.data_ptr(), mask.data_ptr())
+    if r != 0:
+        raise RuntimeError(f"sirius_debug_topk failed: {r}")
 
 
 def debug_gemv(W, x, out, argmax=None, delta=None, norm_w=None, res_out=None, tokens=None, embed=None) -> None:

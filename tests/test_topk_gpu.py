@@ -108,3 +108,34 @@ def test_topk_sirius_free_running_token_exact(r):
     out = driver.Driver(_ctx(cfg, thr, 0.5), topk=True).sirius([prompt], 32, 4, r)
     assert out.tokens[0] == ref.tokens
     assert out.advances(0) == ref.advances[:len(out.kernels)]
+
+
+@pytest.mark.parametrize("F,k,ties", [(14336, 7168, 0), (14336, 7168, 40), (28672, 1000, 7), (688, 344, 5),
+                                      (100, 1, 0), (3000, 3000, 0)])
+def test_topk_select_kernel_exact_with_forced_ties(F, k, ties):
+    """The selection kernel alone (both of its paths): with `ties` > 0 several neurons get exactly the
+    k-th largest |a| (the lowest-index ones must win), else the k-th value is unique.  The mask must
+    be the rule applied to the kernel's own a (bit-exact)."""
+    from paper_2409_03856_b200 import sirius as S
+    rng = np.random.default_rng(F + k + ties)
+    g = rng.standard_normal((2, F)).astype(np.float32) * 0.7
+    for b in range(2):
+        if ties:
+            a = g[b] / (1.0 + np.exp(-g[b].astype(np.float64)))
+            kth = np.sort(np.abs(a))[::-1][k - 1]
+            j = int(np.argmin(np.abs(np.abs(a) - kth)))
+            idx = rng.choice(F, size=ties, replace=False)
+            g[b, idx] = g[b, j]  # same g -> same a (same kernel arithmetic) -> a tie at the boundary
+    gd = torch.tensor(g, device="cuda")
+    ad = torch.zeros_like(gd)
+    md = torch.zeros((2, F // 32 + 1), dtype=torch.int32, device="cuda")
+    S.debug_topk(gd, k, ad, md)
+    a = ad.cpu().numpy()
+    m = md.cpu().numpy().view(np.uint32)
+    for b in range(2):
+        order = np.lexsort((np.arange(F), -np.abs(a[b]).astype(np.float64)))
+        want = np.zeros(F, dtype=bool)
+        want[order[:k]] = True
+        got = ((m[b][np.arange(F) >> 5] >> (np.arange(F) & 31)) & 1).astype(bool)
+        assert got.sum() == k
+        np.testing.assert_array_equal(got, want)
