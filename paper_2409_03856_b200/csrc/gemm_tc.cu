@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "gemm_tc.cuh"
+#include "peer_ar.cuh"
 
 namespace sirius {
 
@@ -89,8 +90,14 @@ SIRIUS_DEV void tmem_ld16(uint32_t taddr, float* v) {
 // last CTA owning work item x (CTA c owns [floor(W c / G), floor(W (c+1) / G)))
 SIRIUS_DEV int owner_of(long long x, long long W, int G) { return (int)(((x + 1) * G + W - 1) / W) - 1; }
 
+// fused all-reduce destinations of this CTA's epilogue (read once, after the PDL wait): this rank's
+// slot of parity (s + 1) on every rank
+struct ParDst {
+  float* slot[8];
+};
+
 template <bool DUAL>
-SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
+SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1, const ParDst* pd = nullptr) {
   if (j >= g.M || n >= g.N) return;
   if (DUAL) {
     const float av = v0 / (1.0f + expf(-v0));  // a = SiLU(gate)
@@ -101,6 +108,12 @@ SIRIUS_DEV void epi_store(const GemmArgs& g, int j, int n, float v0, float v1) {
     store_split3(reinterpret_cast<uint16_t*>(g.out), g.out_plane, (size_t)j * g.ldc + n, m);
   } else {
     reinterpret_cast<float*>(g.out)[(size_t)j * g.ldc + n] = v0;
+    if (pd) {  // fused all-reduce: this rank's element into its slot on every rank
+      const size_t off = (size_t)j * g.ldc + n;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < g.par.world) pd->slot[q][off] = v0;
+    }
   }
 }
 
@@ -305,6 +318,18 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {  // ---------------- epilogue warps 0-3 (thread = TMEM lane = weight row of the tile)
     pdl_wait();
+    ParDst pdst;
+    const ParDst* pd = nullptr;
+    if (!DUAL && g.par.world) {
+      const unsigned long long s1 = __ldcg(g.par.seq) + 1ull;  // written by the previous producer
+      const size_t base = (size_t)(s1 & 1ull) * g.par.world * g.par.slot_n;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        pdst.slot[q] = q < g.par.world ? reinterpret_cast<float*>(g.par.peers[q]) + base +
+                                             (size_t)(g.par.loopback ? q : g.par.rank) * g.par.slot_n
+                                       : nullptr;
+      pd = &pdst;
+    }
     int sidx = 0;
     for (long long w = w0; w < w1; ++sidx) {
       const int t = (int)(w / g.kb);
@@ -334,7 +359,7 @@ __global__ void __launch_bounds__(192, 1)
           acc_ld(0, j0, v0);
           if (DUAL) acc_ld(1, j0, v1);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, v0[j], DUAL ? v1[j] : 0.f);
+          for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, v0[j], DUAL ? v1[j] : 0.f, pd);
         }
         tc_fence_before();
         __syncwarp();
@@ -371,7 +396,7 @@ __global__ void __launch_bounds__(192, 1)
               }
             }
 #pragma unroll
-            for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, s0[j], s1[j]);
+            for (int j = 0; j < 16; ++j) epi_store<DUAL>(g, j0 + j, n, s0[j], s1[j], pd);
           }
         }
       }
@@ -381,6 +406,23 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   if (tid == 0) gstamp(g, 5);  // all segments (epilogue + fix-up) done
+  if (g.par.world && tid == 0) {  // fused all-reduce: the last CTA with work publishes the sync point
+    __threadfence_system();       // this CTA's peer stores (ordered before by the barrier above)
+    const unsigned old = atomicAdd(g.par.done, 1u);
+    if (old == (unsigned)g.par_ctas - 1) {
+      atomicExch(g.par.done, 0u);
+      // one sys-scope fence (every CTA's stores: their fences precede their arrivals), then the W flags
+      // as relaxed stores (a release pattern: strong writes after a release fence) — not W releases
+      __threadfence_system();
+      const unsigned long long s1 = __ldcg(g.par.seq) + 1ull;
+      const int W = g.par.world;
+      for (int q = 0; q < W; ++q)
+        par::st_relaxed_sys(reinterpret_cast<unsigned long long*>(g.par.peers[q] + par::off_flags(g.par)) +
+                                (size_t)(s1 & 1ull) * W + (g.par.loopback ? q : g.par.rank),
+                            s1);
+      *g.par.seq = s1;
+    }
+  }
   if (warp == 5) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
@@ -472,6 +514,7 @@ static cudaError_t gemm_k(const void* w0, const void* w1, const void* x, GemmArg
   const size_t smem = (size_t)stages * stage_bytes + extra;
   const long long W = (long long)g.n_tiles * g.kb;
   const int grid = (int)(W < num_sms ? W : num_sms);
+  g.par_ctas = grid;  // every CTA of the grid has work (W >= grid)
   auto kern = gemm_tc_kernel<DUAL, KBOX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "decode_kernels.cuh"  // PeerAr
+
 namespace sirius {
 
 struct GemmArgs {
@@ -27,6 +29,13 @@ struct GemmArgs {
   int n_active_stride;
   float* gate_out;         // [M rows] stride gate_stride, or NULL
   long long gate_stride;
+  // single (fp32 out, ldc == d) only: fused peer all-reduce of the verify / batched-row forward
+  // (SURVEY.md §8(e) phase 2; peer_ar.cuh): every output element is also stored into this rank's slot
+  // on every rank over NVLink as the epilogue writes it; the last of par_ctas CTAs (those with work)
+  // release-stores the sync point's sequence number into every rank's flag.  The consumer (norm_rows)
+  // waits for the flags and sums the slots in rank order.
+  PeerAr par;
+  int par_ctas;
 };
 
 namespace launch {

@@ -140,6 +140,7 @@ struct sirius_ctx {
   // fused peer all-reduce of the decode step (sirius_par_enable; SURVEY.md §8(e) phase 2)
   bool par_on = false;
   bool par_loopback = false;      // stub comm: every peer is this rank's own buffer (timing proxy)
+  bool rows_par = false;          // the last forward_rows fused its all-reduces (its head norm consumes)
   int par_slot_n = 0, par_key_n = 0;
   size_t par_bytes = 0;
   std::vector<void*> par_opened;  // peer buffers opened through CUDA IPC (closed by sirius_destroy)
@@ -420,6 +421,13 @@ PeerAr par_of(const sirius_ctx* c, const RankState& R) {
   p.err = c->err_dev;
   return p;
 }
+// a norm_rows consumer of the last fused sync point (forward_rows with GemmArgs.par producers)
+void par_consume_rows(const sirius_ctx* c, const RankState& R, NormRowsArgs& na) {
+  na.delta = nullptr;
+  na.par_consume = 1;
+  na.par = par_of(c, R);
+}
+
 // the all-reduce of the partials buf [B, d] of every rank of this context: fused into the producer
 // (nothing to launch), the emulated reduction (every emulated rank has pushed), or NCCL / in-order sums
 sirius_status par_or_allreduce(sirius_ctx* c, float* RankState::*buf, float** ptrs_dev, int B, bool par) {
@@ -512,10 +520,15 @@ struct GemmMask {  // CATS mask of the dual (SwiGLU) GEMM in the batched sparse 
 
 // out: fp32 [M, ldc] (single) or, dual (wb != NULL), the SwiGLU product's three bf16 term planes
 // (plane stride MAXM * ldc).  x: the activation's three term planes ([3 * MAXM, K] map).
+
 sirius_status run_gemm(sirius_ctx* c, RankState& R, const void* wa, const void* wb, const void* x, int N, int K,
-                       int M, void* out, int ldc, unsigned long long* trace = nullptr, const GemmMask* mask = nullptr) {
+                       int M, void* out, int ldc, unsigned long long* trace = nullptr, const GemmMask* mask = nullptr,
+                       bool par = false) {
   GemmArgs g = {};
   g.trace = trace;
+  if (par) {  // fused peer all-reduce of the fp32 output (forward_rows: one launch, M <= 128, ldc == d)
+    g.par = par_of(c, R);
+  }
   if (mask) {
     g.thr = mask->thr;
     g.n_active = mask->n_active;
@@ -570,6 +583,12 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
   const bool to_cache = mode != ROWS_VERIFY;
   const sirius_config& cf = c->cfg;
   const int M = nseq * rows_per_seq, d = cf.d_model, hd = cf.head_dim, L = cf.n_layers;
+  // TP > 1 with sirius_par_enable: the O-proj / down-proj GEMMs push their outputs to every rank in the
+  // epilogue and the next norm_rows sums them (no collective launch) — verify and batched-row forwards
+  // (one GEMM launch of <= 128 rows); the prefill keeps the NCCL all-reduce
+  const bool par = c->par_on && cf.tp_size > 1 && mode != ROWS_PREFILL && M <= 128 &&
+                   (size_t)M * d <= (size_t)c->par_slot_n;
+  c->rows_par = par;
   for (int l = 0; l < L; ++l) {
     for (auto& R : c->ranks) {
       NormRowsArgs na = {};
@@ -579,6 +598,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       } else {
         na.base = R.resB;
         na.delta = R.dF;
+        if (par) par_consume_rows(c, R, na);
       }
       na.vocab = cf.vocab;
       na.d = d;
@@ -616,7 +636,7 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
         sa.group_bar = R.attn_bar;
         sa.err = c->err_dev;
         LCU(launch::attn_stage(sa, l, cf.batch, c->stream));
-        OK(run_gemm(c, R, R.w_o[l], nullptr, R.ob3, d, c->Hr * hd, M, R.dA, d));
+        OK(run_gemm(c, R, R.w_o[l], nullptr, R.ob3, d, c->Hr * hd, M, R.dA, d, nullptr, nullptr, par));
         continue;
       }
       RopeStoreArgs ra = {};
@@ -666,13 +686,15 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       int splits = launch::attn_rows_splits(nseq, c->KVr, row_blocks, cf.max_seq, c->num_sms);
       while (splits > 1 && nseq * c->KVr * row_blocks * splits > kAttnRowUnits) --splits;  // workspace bound
       LCU(launch::attn_rows(aa, nseq, hd, splits, row_blocks, c->stream));
-      OK(run_gemm(c, R, R.w_o[l], nullptr, R.ob3, d, c->Hr * hd, M, R.dA, d, gtr ? gtr + 8 * 1024 : nullptr));
+      OK(run_gemm(c, R, R.w_o[l], nullptr, R.ob3, d, c->Hr * hd, M, R.dA, d, gtr ? gtr + 8 * 1024 : nullptr, nullptr,
+                  par));
     }
-    OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
+    if (!par) OK(allreduce(c, &RankState::dA, c->dA_ptrs, M));
     for (auto& R : c->ranks) {
       NormRowsArgs na = {};
       na.base = R.resA;
       na.delta = R.dA;
+      if (par) par_consume_rows(c, R, na);
       na.vocab = cf.vocab;
       na.d = d;
       na.norm_w = R.ffn_norm[l];
@@ -700,9 +722,10 @@ sirius_status forward_rows(sirius_ctx* c, const int32_t* tokens, const int32_t* 
       }
       OK(run_gemm(c, R, R.w_gate[l], R.w_up[l], R.xn3, c->Fr, d, M, R.mb3, c->Fr, gtr2, &mk));
       if (cs_stats) LCU(launch::csparse_colsum(R.cs_scratch, M, c->Fr, c->Fr, R.cs_stats + (size_t)l * c->Fr, c->stream));
-      OK(run_gemm(c, R, R.w_down_t[l], nullptr, R.mb3, d, c->Fr, M, R.dF, d, gtr2 ? gtr2 + 8 * 1024 : nullptr));
+      OK(run_gemm(c, R, R.w_down_t[l], nullptr, R.mb3, d, c->Fr, M, R.dF, d, gtr2 ? gtr2 + 8 * 1024 : nullptr,
+                  nullptr, par));
     }
-    OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
+    if (!par) OK(allreduce(c, &RankState::dF, c->dF_ptrs, M));
   }
   return SIRIUS_OK;
 }
@@ -862,7 +885,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     dA_h.push_back(R.dA);
     dF_h.push_back(R.dF);
     if (cf.tp_size > 1) {  // fused peer all-reduce buffers (zeroed: flags 0 < every sequence number)
-      c->par_slot_n = round_up(B * d, 4);
+      c->par_slot_n = round_up(std::max(B, std::min(B * cf.max_gamma, 128)) * d, 4);  // decode / verify rows
       c->par_key_n = 8;
       c->par_bytes = (size_t)2 * cf.tp_size * ((size_t)c->par_slot_n * 4 + (size_t)c->par_key_n * 8 + 8);
       if (alloc(c, &R.par_buf, c->par_bytes) || alloc(c, &R.par_peers, 8) || alloc(c, &R.par_seq, 1) ||
@@ -1418,6 +1441,7 @@ static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* kernel_to
     NormRowsArgs na = {};
     na.base = R.resB;
     na.delta = R.dF;
+    if (c->rows_par) par_consume_rows(c, R, na);  // the last forward_rows fused its all-reduces
     na.vocab = cf.vocab;
     na.d = d;
     na.norm_w = R.final_norm;
@@ -1503,6 +1527,7 @@ static sirius_status head_rows(sirius_ctx* c, RankState& R, int M) {  // final R
   NormRowsArgs na = {};
   na.base = R.resB;
   na.delta = R.dF;
+  if (c->rows_par) par_consume_rows(c, R, na);  // the last forward_rows fused its all-reduces
   na.vocab = cf.vocab;
   na.d = cf.d_model;
   na.norm_w = R.final_norm;

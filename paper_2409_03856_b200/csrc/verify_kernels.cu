@@ -11,6 +11,7 @@
 //  * transpose / rank-sum helpers
 #include "common.cuh"
 #include "verify_kernels.cuh"
+#include "peer_ar.cuh"
 
 namespace sirius {
 
@@ -45,6 +46,36 @@ __global__ void __launch_bounds__(256) norm_rows_kernel(NormRowsArgs a) {
       if (g < NG) {
         x[j] = __ldcg(base + g);
         dl[j] = delta ? __ldcg(delta + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (a.par_consume) {  // fused peer all-reduce: ((s_0 + s_1) + ...) * scale, as the in-order sum
+      const unsigned long long s = __ldcg(a.par.seq);
+      par::wait_flags(a.par, s);
+      const float* slots = reinterpret_cast<const float*>(a.par.self) + (size_t)(s & 1ull) * a.par.world * a.par.slot_n;
+      for (int r0 = 0; r0 < a.par.world; r0 += 2) {  // two ranks' rows in flight per round
+        float4 v[2][MG];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float4* sr = reinterpret_cast<const float4*>(slots + (size_t)(r0 + u) * a.par.slot_n + (size_t)m * d);
+#pragma unroll
+          for (int j = 0; j < MG; ++j)
+            if (r0 + u < a.par.world && tid + 256 * j < NG) v[u][j] = __ldcg(sr + tid + 256 * j);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int j = 0; j < MG; ++j)
+            if (r0 + u < a.par.world && tid + 256 * j < NG) {
+              if (r0 + u == 0) {
+                dl[j] = v[u][j];
+              } else {
+                dl[j].x += v[u][j].x; dl[j].y += v[u][j].y; dl[j].z += v[u][j].z; dl[j].w += v[u][j].w;
+              }
+            }
+      }
+#pragma unroll
+      for (int j = 0; j < MG; ++j) {
+        dl[j].x *= a.par.scale; dl[j].y *= a.par.scale; dl[j].z *= a.par.scale; dl[j].w *= a.par.scale;
       }
     }
 #pragma unroll

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "decode_kernels.cuh"  // PeerAr
+
 namespace sirius {
 
 struct NormRowsArgs {
@@ -17,6 +19,8 @@ struct NormRowsArgs {
   float* res_out;          // [M, d] or NULL
   uint16_t* out3;          // [3][plane] bf16: h = t0 + t1 + t2 (split3: fp32 h exactly, as three bf16
   size_t plane;            //          terms for the tensor-core B operand); row m at m * d of each plane
+  int par_consume;         // delta = the fused peer all-reduce of the last sync point (GemmArgs.par):
+  PeerAr par;              //   wait for every rank's flag, sum the slots of row m in rank order
 };
 
 struct RopeStoreArgs {

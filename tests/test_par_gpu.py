@@ -162,3 +162,47 @@ def test_par_abi_errors():
     with pytest.raises(S.SiriusError) as e:
         emu.sirius_par_enable([b"\0" * S.PAR_HANDLE_BYTES] * 2)
     assert e.value.status == -1  # INVALID_ARG: emulated contexts take no handles
+
+
+def test_par_emulated_batched_rows_bitwise(monkeypatch):
+    """Batch 8 (the tensor-core row path for decode; verify of 8 x 4 rows): the fused all-reduce of the
+    row forwards (O / down GEMM epilogues push over peer memory, norm_rows sums) reproduces the in-order
+    sums bit for bit, tiny TP 2, deterministic FFN."""
+    from paper_2409_03856_b200 import sirius as S
+    from synth import gpu as sg
+    monkeypatch.setenv("SIRIUS_FFN_ATOMIC", "0")
+    cfg, tp, B, gamma = synth.TINY, 2, 8, 4
+    thr = synth.layer_thresholds(cfg, 0.5)
+    prompts = [synth.eval_prompt(cfg, 20 + b, 9 + 3 * b) for b in range(B)]
+    shards = [sg.device_weights(cfg, tp, r) for r in range(tp)]
+
+    def run(par):
+        ctx = S.Sirius(cfg, shards, thr, batch=B, max_seq=128, max_gamma=16, tp_size=tp)
+        if par:
+            ctx.sirius_par_enable(None)
+        first = torch.zeros(B, dtype=torch.int32, device="cuda")
+        ctx.sirius_prefill(i32(np.concatenate(prompts)), [len(p) for p in prompts], first)
+        T = np.array([len(p) for p in prompts], dtype=np.int32)
+        tok = first.clone()
+        outs, drafts = [], [first.cpu().numpy()]
+        for i in range(gamma - 1):
+            to = torch.zeros(B, dtype=torch.int32, device="cuda")
+            lo = torch.zeros((B, cfg.vocab), dtype=torch.float32, device="cuda")
+            ctx.sparse_decode_step(tok, i32(T + i), 0, to, lo)
+            torch.cuda.synchronize()
+            outs += [to.cpu().numpy(), lo.cpu().numpy()]
+            drafts.append(to.cpu().numpy())
+            tok = to
+        kt = np.stack(drafts, axis=1).astype(np.int32)  # [B, gamma]: pending, d_1 .. d_{gamma-1}
+        na = torch.zeros(B, dtype=torch.int32, device="cuda")
+        nx = torch.zeros(B, dtype=torch.int32, device="cuda")
+        q = torch.zeros((B, gamma), dtype=torch.float32, device="cuda")
+        lo = torch.zeros((B, gamma, cfg.vocab), dtype=torch.float32, device="cuda")
+        ctx.correct_kernel(i32(kt), i32(T), gamma, 0.3, 0, na, nx, q, lo)
+        torch.cuda.synchronize()
+        outs += [na.cpu().numpy(), nx.cpu().numpy(), q.cpu().numpy(), lo.cpu().numpy()]
+        return outs
+
+    ref, got = run(False), run(True)
+    for x, y in zip(got, ref):
+        np.testing.assert_array_equal(x, y)

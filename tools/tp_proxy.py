@@ -76,6 +76,13 @@ drv.greedy_run(drv.pending, T0, 16, False)
 torch.cuda.synchronize()
 prof = {k: v[0] * 1e3 / 16 for k, v in ctx.profile_read().items() if v[1]}
 ctx.profile(False)
+ctx.profile(True)  # the correction kernel (verify forward + accept), per call
+for _ in range(3):
+    drv.step(g, 0.0)
+torch.cuda.synchronize()
+pr = ctx.profile_read()
+verify_us = pr["correct_kernel"][0] * 1e3 / max(1, pr["correct_kernel"][1])
+ctx.profile(False)
 ck = clk.stop()
 tp_per_rank = dict(ffn=cfg.ffn_dim // a.tp, heads=cfg.n_heads // a.tp, kv_heads=cfg.n_kv_heads // a.tp,
                    vocab=cfg.vocab // a.tp)
@@ -92,6 +99,7 @@ res = {"what": what, "fused_peer_allreduce_loopback": a.par, "batch": B,
        "note": ("add the NVLink transfer latency of each fused push (not measured: one GPU)" if a.par else
                 "add the NVLink all-reduce latency per call (not measured: one GPU)"),
        "cs_step_device_us_by_kernel_class": prof,
+       "correct_kernel_device_us": verify_us,
        "clocks": ck, "setup_s": setup}
 print(json.dumps(res))
 if a.out:
