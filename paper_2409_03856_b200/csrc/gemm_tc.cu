@@ -406,21 +406,27 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   if (tid == 0) gstamp(g, 5);  // all segments (epilogue + fix-up) done
-  if (g.par.world && tid == 0) {  // fused all-reduce: the last CTA with work publishes the sync point
-    __threadfence_system();       // this CTA's peer stores (ordered before by the barrier above)
-    const unsigned old = atomicAdd(g.par.done, 1u);
-    if (old == (unsigned)g.par_ctas - 1) {
-      atomicExch(g.par.done, 0u);
-      // one sys-scope fence (every CTA's stores: their fences precede their arrivals), then the W flags
-      // as relaxed stores (a release pattern: strong writes after a release fence) — not W releases
-      __threadfence_system();
+  if (g.par.world && warp == 0) {  // fused all-reduce: the last CTA with work publishes the sync point
+    unsigned last = 0u;
+    if (lane == 0) {
+      __threadfence_system();  // this CTA's peer stores (ordered before by the barrier above)
+      const unsigned old = atomicAdd(g.par.done, 1u);
+      last = old == (unsigned)g.par_ctas - 1 ? 1u : 0u;
+      if (last) {
+        atomicExch(g.par.done, 0u);
+        __threadfence_system();  // every CTA's stores: their fences precede their arrivals
+      }
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);  // warp-synchronising: lane 0's observations reach the lanes
+    if (last) {
       const unsigned long long s1 = __ldcg(g.par.seq) + 1ull;
       const int W = g.par.world;
-      for (int q = 0; q < W; ++q)
-        par::st_relaxed_sys(reinterpret_cast<unsigned long long*>(g.par.peers[q] + par::off_flags(g.par)) +
-                                (size_t)(s1 & 1ull) * W + (g.par.loopback ? q : g.par.rank),
+      if (lane < W)  // lanes 0..W-1 release the W flags in one instruction
+        par::st_release_sys(reinterpret_cast<unsigned long long*>(g.par.peers[lane] + par::off_flags(g.par)) +
+                                (size_t)(s1 & 1ull) * W + (g.par.loopback ? lane : g.par.rank),
                             s1);
-      *g.par.seq = s1;
+      __syncwarp();
+      if (lane == 0) *g.par.seq = s1;
     }
   }
   if (warp == 5) {

@@ -20,14 +20,6 @@ SIRIUS_DEV size_t off_flags(const PeerAr& p) { return off_keys(p) + (size_t)2 * 
 SIRIUS_DEV void st_release_sys(unsigned long long* a, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
-SIRIUS_DEV void st_relaxed_sys(unsigned long long* a, unsigned long long v) {  // after a sys-scope fence
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
-}
-SIRIUS_DEV unsigned long long ld_relaxed_sys(const unsigned long long* a) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
-  return v;
-}
 SIRIUS_DEV unsigned long long ld_acquire_sys(const unsigned long long* a) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
@@ -47,12 +39,12 @@ SIRIUS_DEV void wait_flags(const PeerAr& p, unsigned long long s) {
   if (threadIdx.x < (unsigned)p.world) {
     const unsigned long long* f =
         reinterpret_cast<const unsigned long long*>(p.self + off_flags(p)) + (size_t)par * p.world + threadIdx.x;
-    // relaxed polling, then one acquire fence (an acquire pattern); the CTA barrier orders the other
-    // threads' slot reads after it
-    if (ld_relaxed_sys(f) < s) {
+    // acquire polling (measured faster than relaxed polling + a fence); the CTA barrier orders the
+    // other threads' slot reads after it
+    if (ld_acquire_sys(f) < s) {
       const unsigned long long t0 = globaltimer();
       int n = 0;
-      while (ld_relaxed_sys(f) < s) {
+      while (ld_acquire_sys(f) < s) {
         if (++n == 4096) {
           n = 0;
           if (globaltimer() - t0 > 10000000000ull) {
@@ -62,7 +54,6 @@ SIRIUS_DEV void wait_flags(const PeerAr& p, unsigned long long s) {
         }
       }
     }
-    __threadfence_system();
   }
   __syncthreads();
 }
@@ -164,16 +155,15 @@ SIRIUS_DEV void push_last(const PeerAr& p, float* src, int n, unsigned long long
         reinterpret_cast<unsigned long long*>(pb[q] + off_keys(p))[((size_t)par * W + si) * p.key_n + i] = k;
       }
   }
-  // the CTA barrier orders every thread's stores before thread 0's sys-scope fence, which is cumulative
-  // over them; the W flags follow as relaxed stores (a release pattern) — one fence, not W releases
+  // the CTA barrier orders every thread's stores before the flag lanes' sys-scope release stores (PTX
+  // memory model: bar.sync is morally strong, a release is cumulative over what its thread observed);
+  // lanes 0..W-1 of warp 0 release in one instruction (measured: faster than one fence + W relaxed
+  // stores by one thread, tools/tp_proxy.py A/B on one box)
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int q = 0; q < W; ++q)
-      st_relaxed_sys(reinterpret_cast<unsigned long long*>(pb[q] + off_flags(p)) + (size_t)par * W + (p.loopback ? q : p.rank),
-                     s);
-    *p.seq = s;
-  }
+  if (threadIdx.x < (unsigned)W)
+    st_release_sys(reinterpret_cast<unsigned long long*>(pb[threadIdx.x] + off_flags(p)) + (size_t)par * W +
+                       (p.loopback ? threadIdx.x : p.rank), s);
+  if (threadIdx.x == 0) *p.seq = s;
   if (!p.fused) return;
   wait_flags(p, s);
   reduce(p, par, src, n, nk, keys_io, token_out);
