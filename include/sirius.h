@@ -247,14 +247,16 @@ sirius_status sirius_csparse_enable(sirius_ctx* ctx, float keep_fraction);
  * of S3 and S6 and the LM-head argmax combine of S7 in SURVEY.md §8(a); the paper itself runs on one
  * GPU).  Each rank owns a comm buffer of identical layout
  *   slots [2][tp_size][batch * d_model] fp32 | keys [2][tp_size][8] u64 | flags [2][tp_size] u64
- * that every other rank maps through CUDA IPC.  With the fused path on, sparse_decode_step (the
- * per-stage path, batch <= 4, or 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the CTA that
- * completes the rank partial of the O-proj GEMV / CATS FFN (or the packed argmax keys of the LM head)
- * stores it into its slot on every rank over NVLink, release-stores the sync point's sequence number
- * into the flags, acquire-waits for every rank's flag and writes the rank-order sum over the partial
- * (the head: the global argmax token), so every rank computes bitwise the same residual and the next
- * kernel reads it as at TP 1.  prefill, correct_kernel and the batched row path keep the NCCL
- * collectives.
+ * that every other rank maps through CUDA IPC.  With the fused path on, sparse_decode_step (per-stage
+ * path, batch <= 4, or 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the CTA that completes the
+ * rank partial of the O-proj GEMV / CATS FFN (or the packed argmax keys of the LM head) stores it into
+ * its slot on every rank over NVLink, release-stores the sync point's sequence number into the flags,
+ * acquire-waits for every rank's flag and writes the rank-order sum over the partial (the head: the
+ * global argmax token), so every rank computes bitwise the same residual and the next kernel reads it
+ * as at TP 1.  The verify / batched-row forward (correct_kernel, the tree kernel, batched decode: at
+ * most 128 rows and batch * max_gamma rows) does the same from the O-proj / down-proj tcgen05 GEMM
+ * epilogues, and the next row-norm kernel waits and sums.  The prefill's all-reduces and
+ * correct_kernel's all-gather of per-row softmax statistics stay on NCCL.
  *
  * sirius_par_export: HOST handle_out [SIRIUS_PAR_HANDLE_BYTES] = this rank's cudaIpcMemHandle_t.
  *   Errors: STATE for an emulated / stub / tp_size 1 context; CUDA.
