@@ -73,7 +73,7 @@ typedef struct {
   float rope_theta, rms_eps;
   int32_t batch;     /* number of sequences (slots 0..batch-1), fixed for the context's life;
                         one of 1, 2, 4, 8, 16, 32 (else SIRIUS_ERR_UNSUPPORTED); batch * max_gamma <= 1024;
-                        batch >= 8 decodes through the tensor-core row path        */
+                        batch >= 4 decodes through the tensor-core row path        */
   int32_t max_seq;   /* KV capacity per sequence (>= prompt + generated + max_gamma)              */
   int32_t max_gamma; /* max verify rows per sequence per correct_kernel call (<= 64)              */
   int32_t tp_size, tp_rank; /* n_heads, n_kv_heads, ffn_dim, vocab divisible by tp_size (else
@@ -224,7 +224,7 @@ sirius_status sirius_set_sampling(sirius_ctx* ctx, float temperature, uint64_t s
  * index) — gate GEMV, exact radix selection, then only the selected W_up / W_down rows.  Unlike the
  * threshold the set depends on the whole layer, so TP > 1 would need a global selection: TP 1 only.
  * keep_fraction 0 disables.
- * Errors: INVALID_ARG (keep_fraction outside [0, 1]); UNSUPPORTED (tp_size > 1, batch >= 8, k = 0);
+ * Errors: INVALID_ARG (keep_fraction outside [0, 1]); UNSUPPORTED (tp_size > 1, batch > 4, k = 0);
  * CUDA (allocation).  Synchronous. */
 sirius_status sirius_topk_enable(sirius_ctx* ctx, float keep_fraction);
 
@@ -248,7 +248,7 @@ sirius_status sirius_csparse_enable(sirius_ctx* ctx, float keep_fraction);
  * GPU).  Each rank owns a comm buffer of identical layout
  *   slots [2][tp_size][batch * d_model] fp32 | keys [2][tp_size][8] u64 | flags [2][tp_size] u64
  * that every other rank maps through CUDA IPC.  With the fused path on, sparse_decode_step (per-stage
- * path, batch <= 4, or 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the CTA that completes the
+ * path: batch <= 2, or <= 8 with SIRIUS_DECODE_ROWS=0) launches no collective: the CTA that completes the
  * rank partial of the O-proj GEMV / CATS FFN (or the packed argmax keys of the LM head) stores it into
  * its slot on every rank over NVLink, release-stores the sync point's sequence number into the flags,
  * acquire-waits for every rank's flag and writes the rank-order sum over the partial (the head: the

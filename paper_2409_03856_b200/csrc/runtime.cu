@@ -151,7 +151,7 @@ struct sirius_ctx {
   size_t gemm_smem = 0;
   bool ffn_atomic = true;  // CATS FFN partials via float4 atomics, no grid barrier (SIRIUS_FFN_ATOMIC=0: deterministic)
   int ffn_split = 2;       // atomic-mode FFN CTAs per SM (SIRIUS_FFN_SPLIT; 2 measured best of 1-8)
-  bool decode_rows = false;  // batched decode through the tensor-core row path (batch >= 8; SIRIUS_DECODE_ROWS)
+  bool decode_rows = false;  // batched decode through the tensor-core row path (batch >= 4; SIRIUS_DECODE_ROWS)
   int32_t* dec_nacc = nullptr;
   int attn_stage_splits = 1;
   int accept_splits = 8;
@@ -798,7 +798,9 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
     return s;
   }
   if (const char* e = getenv("SIRIUS_FFN_ATOMIC")) c->ffn_atomic = atoi(e) != 0;
-  c->decode_rows = cf.batch >= 8;
+  // measured (profiles/batch_r02): batch 4 dense 5.81 ms per step on the per-stage CUDA-core kernels vs
+  // 4.30 on the row path; batch 2 3.62 vs 4.10 — the row path from batch 4 on
+  c->decode_rows = cf.batch >= 4;
   if (const char* e = getenv("SIRIUS_DECODE_ROWS")) c->decode_rows = atoi(e) != 0;
   if (cf.batch > 8) c->decode_rows = true;  // the per-stage decode kernels are instantiated up to batch 8
   if (const char* e = getenv("SIRIUS_FFN_SPLIT")) c->ffn_split = std::max(1, atoi(e));
@@ -1047,7 +1049,7 @@ sirius_status sirius_topk_enable(sirius_ctx* c, float keep_fraction) {
     c->topk_k = 0;
     return SIRIUS_OK;
   }
-  if (cf.tp_size != 1 || c->decode_rows)
+  if (cf.tp_size != 1 || cf.batch > 4)
     return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: TP 1 and the per-stage decode path (batch <= 4)");
   const int k = (int)std::floor((double)keep_fraction * c->Fr + 0.5);
   if (k < 1) return fail(c, SIRIUS_ERR_UNSUPPORTED, "top-k FSparse: keep_fraction * ffn rounds to 0");
@@ -1194,7 +1196,9 @@ static sirius_status enqueue_decode(sirius_ctx* c, const int32_t* token_in, cons
   const bool dense = flags & SIRIUS_DENSE;
   const bool csparse = flags & SIRIUS_CSPARSE;
   const bool topk = flags & SIRIUS_TOPK;
-  if (c->decode_rows) return enqueue_decode_rows(c, token_in, pos, dense, token_out, logits_out, n_active_out,
+  // top-k / CSparse steps run the per-stage kernels (batch <= 4) even where dense / CATS steps take the rows
+  if (c->decode_rows && !topk && !csparse)
+    return enqueue_decode_rows(c, token_in, pos, dense, token_out, logits_out, n_active_out,
                                                  gate_act_out);
   if (n_active_out) CU(cudaMemsetAsync(n_active_out, 0, sizeof(int32_t) * B * L, c->stream));
   if (c->use_step && !csparse && !topk && c->samp_temp == 0.f) {  // the whole step in one persistent launch
