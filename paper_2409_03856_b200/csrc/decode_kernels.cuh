@@ -39,6 +39,7 @@ struct PeerAr {
   unsigned long long* seq;     // this rank's sync-point counter
   unsigned* done;              // producer CTA arrivals (reset by the last CTA)
   int* err;                    // device error word (a peer that never arrives: timeout)
+  unsigned long long timeout_ns;  // wait bound (10 s; SIRIUS_PAR_TIMEOUT_MS)
 };
 
 struct Prologue {

@@ -32,8 +32,9 @@ SIRIUS_DEV unsigned long long globaltimer() {
 }
 
 // threads < world acquire-wait for flags (par, 0..world-1) >= s on this rank's buffer; CTA barrier.
-// A rank that does not arrive within 10 s sets kErrTimeout and the wait gives up (the results are
-// then garbage, the next ABI call reports SIRIUS_ERR_NCCL).
+// A rank that does not arrive within timeout_ns (10 s) sets kErrTimeout and the wait gives up (the
+// results are then garbage, the next ABI call reports SIRIUS_ERR_NCCL); once the bit is set every
+// later wait gives up at once, so a dead peer costs one timeout, not one per sync point.
 SIRIUS_DEV void wait_flags(const PeerAr& p, unsigned long long s) {
   const int par = (int)(s & 1ull);
   if (threadIdx.x < (unsigned)p.world) {
@@ -41,13 +42,13 @@ SIRIUS_DEV void wait_flags(const PeerAr& p, unsigned long long s) {
         reinterpret_cast<const unsigned long long*>(p.self + off_flags(p)) + (size_t)par * p.world + threadIdx.x;
     // acquire polling (measured faster than relaxed polling + a fence); the CTA barrier orders the
     // other threads' slot reads after it
-    if (ld_acquire_sys(f) < s) {
+    if (ld_acquire_sys(f) < s && !(*(volatile const int*)p.err & kErrTimeout)) {
       const unsigned long long t0 = globaltimer();
       int n = 0;
       while (ld_acquire_sys(f) < s) {
         if (++n == 4096) {
           n = 0;
-          if (globaltimer() - t0 > 10000000000ull) {
+          if (globaltimer() - t0 > p.timeout_ns || (*(volatile const int*)p.err & kErrTimeout)) {
             atomicOr(p.err, kErrTimeout);
             break;
           }

@@ -141,6 +141,7 @@ struct sirius_ctx {
   bool par_on = false;
   bool par_loopback = false;      // stub comm: every peer is this rank's own buffer (timing proxy)
   bool rows_par = false;          // the last forward_rows fused its all-reduces (its head norm consumes)
+  unsigned long long par_timeout_ns = 10000000000ull;  // a peer missing this long -> SIRIUS_ERR_NCCL
   int par_slot_n = 0, par_key_n = 0;
   size_t par_bytes = 0;
   std::vector<void*> par_opened;  // peer buffers opened through CUDA IPC (closed by sirius_destroy)
@@ -419,6 +420,7 @@ PeerAr par_of(const sirius_ctx* c, const RankState& R) {
   p.seq = R.par_seq;
   p.done = R.par_done;
   p.err = c->err_dev;
+  p.timeout_ns = c->par_timeout_ns;
   return p;
 }
 // a norm_rows consumer of the last fused sync point (forward_rows with GemmArgs.par producers)
@@ -809,6 +811,7 @@ sirius_status sirius_init(const sirius_config* cfgp, const sirius_weights* w, co
   // verify / prefill chain with programmatic dependent launch (SIRIUS_VERIFY_PDL=0 disables)
   if (const char* e = getenv("SIRIUS_VERIFY_PDL")) launch::g_chain_pdl = atoi(e) != 0;
   if (const char* e = getenv("SIRIUS_DECODE_PDL")) launch::g_decode_pdl = atoi(e) != 0;
+  if (const char* e = getenv("SIRIUS_PAR_TIMEOUT_MS")) c->par_timeout_ns = (unsigned long long)std::max(1, atoi(e)) * 1000000ull;
   if (const char* e = getenv("SIRIUS_GEMM_KBOX")) launch::g_gemm_kbox = atoi(e);
   if (const char* e = getenv("SIRIUS_GEMM_COARSE")) launch::g_gemm_coarse = atoi(e);
   auto cleanup_fail = [&](sirius_status s) {
@@ -1760,6 +1763,18 @@ int sirius_debug_ffn(sirius_ctx* c, int layer, const float* x, int dense, float*
   OK(launch_decode_ffn(c, c->ranks[0], layer, x, nullptr, nullptr, out, dense != 0, n_active, 1, gate_out, c->Fr));
   CU(cudaStreamSynchronize(c->stream));
   return SIRIUS_OK;
+}
+
+// ---------------------------------------------------------------- test-only entry: peer all-reduce skew
+// adds delta to rank `rank`'s sync-point counter of the fused peer all-reduce (emulated / stub contexts):
+// its next wait then expects a sequence number no peer will publish — the timeout path.  Synchronous.
+int sirius_debug_par_skew(sirius_ctx* c, int rank, int delta) {
+  if (!c || rank < 0 || rank >= (int)c->ranks.size() || !c->ranks[rank].par_seq) return -1;
+  cudaStreamSynchronize(c->stream);
+  unsigned long long v = 0;
+  if (cudaMemcpy(&v, c->ranks[rank].par_seq, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  v += (unsigned long long)(long long)delta;
+  return cudaMemcpy(c->ranks[rank].par_seq, &v, 8, cudaMemcpyHostToDevice) == cudaSuccess ? 0 : -1;
 }
 
 // ---------------------------------------------------------------- test-only entry: top-k selection

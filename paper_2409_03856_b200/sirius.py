@@ -124,6 +124,8 @@ def load():
         lib.sirius_debug_profile_read.argtypes = [P, P, P]
         lib.sirius_debug_profile_read.restype = I
         lib.sirius_debug_gemm.restype = I
+        lib.sirius_debug_par_skew.argtypes = [P, I, I]
+        lib.sirius_debug_par_skew.restype = I
         lib.sirius_debug_topk.argtypes = [P, I, I, I, P, P]
         lib.sirius_debug_topk.restype = I
         lib.sirius_debug_gemv.argtypes = [P, I, I, P, I, P, P, P, P, P, P, P, I]

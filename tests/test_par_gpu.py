@@ -206,3 +206,32 @@ def test_par_emulated_batched_rows_bitwise(monkeypatch):
     ref, got = run(False), run(True)
     for x, y in zip(got, ref):
         np.testing.assert_array_equal(x, y)
+
+
+def test_par_missing_peer_times_out_to_nccl_error(monkeypatch):
+    """A rank that never publishes (emulated: rank 0's sync-point counter skewed by 2, so its waits
+    expect a sequence number nobody writes): the wait gives up after SIRIUS_PAR_TIMEOUT_MS, every
+    later wait gives up at once, and the next call returns SIRIUS_ERR_NCCL (sticky)."""
+    from paper_2409_03856_b200 import sirius as S
+    from synth import gpu as sg
+    monkeypatch.setenv("SIRIUS_PAR_TIMEOUT_MS", "200")
+    cfg = synth.TINY
+    thr = synth.layer_thresholds(cfg, 0.5)
+    ctx = make_ctx(cfg, [sg.device_weights(cfg, 2, r) for r in range(2)], thr, 2)
+    ctx.graphs(False)
+    ctx.sirius_par_enable(None)
+    prompt = synth.eval_prompt(cfg, 1, 20)
+    first = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sirius_prefill(i32(prompt), [len(prompt)], first)
+    to = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.sparse_decode_step(first, i32([len(prompt)]), 0, to)
+    torch.cuda.synchronize()
+    assert ctx.lib.sirius_debug_par_skew(ctx.h, 0, 2) == 0
+    import time
+    t0 = time.time()
+    ctx.sparse_decode_step(to, i32([len(prompt) + 1]), 0, first)
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 5.0  # one timeout, not one per sync point
+    with pytest.raises(S.SiriusError) as e:
+        ctx.sparse_decode_step(first, i32([len(prompt) + 2]), 0, to)
+    assert e.value.status == -5  # SIRIUS_ERR_NCCL
