@@ -48,6 +48,19 @@ def _rank_main(rank, world, port, q):
         # fused peer all-reduce bootstrap: every rank's IPC handle, in rank order, everywhere
         hs = TP.exchange_handles(bytes([rank]) * 64, 64)
         assert hs == [bytes([r]) * 64 for r in range(world)]
+
+        class FakeCtx:  # the two ABI calls par_bootstrap makes (sirius_par_export / sirius_par_enable)
+            got = None
+
+            def sirius_par_export(self):
+                return bytes([0xA0 + rank]) * 64
+
+            def sirius_par_enable(self, handles):
+                self.got = list(handles)
+
+        fc = FakeCtx()
+        TP.par_bootstrap(fc)
+        assert fc.got == [bytes([0xA0 + r]) * 64 for r in range(world)]
         TP.barrier()
         # ---- sharded CATS MLP, all-reduced
         cfg = synth.TINY
