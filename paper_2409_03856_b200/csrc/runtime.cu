@@ -1073,6 +1073,7 @@ sirius_status sirius_par_export(sirius_ctx* c, void* handle_out) {
   OK(check_sticky(c));
   if (c->cfg.tp_size == 1 || c->emulated || c->stub_comm)
     return fail(c, SIRIUS_ERR_STATE, "sirius_par_export: only a real tensor-parallel rank (tp_size > 1, NCCL) exports");
+  CU(cudaDeviceSynchronize());  // the buffer's zeroing (flags 0) is complete before any peer can map it
   cudaIpcMemHandle_t h;
   CU(cudaIpcGetMemHandle(&h, c->ranks[0].par_buf));
   memcpy(handle_out, &h, sizeof(h));
