@@ -6,7 +6,7 @@
 // in the staging area; prefill: already in the cache).  grid (S splits, KVr x row_blocks, nseq),
 // 256 threads, cooperative (one wave, all CTAs co-resident).  Each CTA walks its key range in
 // 64-key blocks staged in shared memory:
-//   scores   thread -> (key t % 64, 16 rows)          k rows padded: conflict-free, q broadcast
+//   scores   thread -> (keys lane, lane + 32; 8 rows)  k rows padded: conflict-free, q broadcast
 //   softmax  warp   -> 8 rows, online (running max / sum per row)
 //   P.V      thread -> (4 dims, 8 rows)               v: 8-byte reads, p broadcast
 // then writes its partial (M, L, A) per row; after a barrier among the S splits of the group, split s
@@ -34,8 +34,6 @@ SIRIUS_DEV void rstamp(const AttnRowsArgs& a, int slot) {  // debug phase stamps
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, float scale) {
   constexpr int KROW = HD + 8;                     // padded bf16 K row (elements)
-  constexpr int RPT = kRows * kKB / kThreads;      // score rows per thread (16)
-  constexpr int RSTEP = kThreads / kKB;            // 4
   constexpr int DPL = HD / 32;                     // P.V dims per thread (4 for HD=128)
   constexpr int RPW = kRows / (kThreads / 32);     // P.V rows per thread (8)
   extern __shared__ __align__(16) uint8_t smem[];
@@ -125,37 +123,56 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
     __syncthreads();
     rstamp(a, 2);
     // ---- scores s[r][kk] = q_r . k_kk  (masked: key p visible to row i iff p <= T + i)
+    // thread -> keys (lane, lane + 32) x rows (warp + 8 j): per 8 dims 2 k reads (conflict-free rows)
+    // and 2 q reads per row (warp-uniform: broadcast) feed 16 dot products; every dot product sums its
+    // dims in ascending order
     {
-      const int kk = tid % kKB, r0 = tid / kKB;
-      float s[RPT];
+      constexpr int KPT = kThreads / kKB == 4 ? 2 : 1;  // keys per thread
+      constexpr int RW = kRows / (kThreads / 32);       // rows per thread (8)
+      static_assert(KPT == 2 && RW == 8, "scores mapping: 256 threads, 64 rows x 64 keys");
+      const int kk0 = lane, rr0 = warp;
+      float s2[KPT][RW];
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) s[j] = 0.f;
-      if (kk < nb) {
-        const uint16_t* kr = k_s + kk * KROW;
+      for (int c = 0; c < KPT; ++c)
+#pragma unroll
+        for (int j = 0; j < RW; ++j) s2[c][j] = 0.f;
+      if (kk0 < nb) {
+        const uint16_t* kr0 = k_s + kk0 * KROW;
+        const uint16_t* kr1 = k_s + (kk0 + 32) * KROW;  // rows >= nb hold stale data: masked below
 #pragma unroll 2
         for (int e = 0; e < HD / 8; ++e) {
-          const uint4 w = *reinterpret_cast<const uint4*>(kr + e * 8);
-          const float kf8[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
-                                bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+          float kf[KPT][8];
 #pragma unroll
-          for (int j = 0; j < RPT; ++j) {
-            const float4 qa = *reinterpret_cast<const float4*>(q_s + (r0 + RSTEP * j) * HD + e * 8);
-            const float4 qb = *reinterpret_cast<const float4*>(q_s + (r0 + RSTEP * j) * HD + e * 8 + 4);
-            float t = s[j];
-            t = fmaf(kf8[0], qa.x, t); t = fmaf(kf8[1], qa.y, t); t = fmaf(kf8[2], qa.z, t); t = fmaf(kf8[3], qa.w, t);
-            t = fmaf(kf8[4], qb.x, t); t = fmaf(kf8[5], qb.y, t); t = fmaf(kf8[6], qb.z, t); t = fmaf(kf8[7], qb.w, t);
-            s[j] = t;
+          for (int c = 0; c < KPT; ++c) {
+            const uint4 w = *reinterpret_cast<const uint4*>((c == 0 ? kr0 : kr1) + e * 8);
+            kf[c][0] = bf16_lo(w.x); kf[c][1] = bf16_hi(w.x); kf[c][2] = bf16_lo(w.y); kf[c][3] = bf16_hi(w.y);
+            kf[c][4] = bf16_lo(w.z); kf[c][5] = bf16_hi(w.z); kf[c][6] = bf16_lo(w.w); kf[c][7] = bf16_hi(w.w);
+          }
+#pragma unroll
+          for (int j = 0; j < RW; ++j) {
+            const float4 qa = *reinterpret_cast<const float4*>(q_s + (rr0 + 8 * j) * HD + e * 8);
+            const float4 qb = *reinterpret_cast<const float4*>(q_s + (rr0 + 8 * j) * HD + e * 8 + 4);
+#pragma unroll
+            for (int c = 0; c < KPT; ++c) {
+              float t = s2[c][j];
+              t = fmaf(kf[c][0], qa.x, t); t = fmaf(kf[c][1], qa.y, t); t = fmaf(kf[c][2], qa.z, t);
+              t = fmaf(kf[c][3], qa.w, t); t = fmaf(kf[c][4], qb.x, t); t = fmaf(kf[c][5], qb.y, t);
+              t = fmaf(kf[c][6], qb.z, t); t = fmaf(kf[c][7], qb.w, t);
+              s2[c][j] = t;
+            }
           }
         }
       }
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int r = r0 + RSTEP * j;
-        const int i = (r_base + r) / G, p = p0 + kk;
-        bool vis = kk < nb && r < nr;
-        if (p >= T) vis = vis && (a.tree_vis ? ((a.tree_vis[a.stage_base + i] >> (p - T)) & 1ull) != 0 : p <= T + i);
-        p_s[r * (kKB + 1) + kk] = vis ? s[j] : -INFINITY;
-      }
+      for (int c = 0; c < KPT; ++c)
+#pragma unroll
+        for (int j = 0; j < RW; ++j) {
+          const int kk = kk0 + 32 * c, r = rr0 + 8 * j;
+          const int i = (r_base + r) / G, p = p0 + kk;
+          bool vis = kk < nb && r < nr;
+          if (p >= T) vis = vis && (a.tree_vis ? ((a.tree_vis[a.stage_base + i] >> (p - T)) & 1ull) != 0 : p <= T + i);
+          p_s[r * (kKB + 1) + kk] = vis ? s2[c][j] : -INFINITY;
+        }
     }
     __syncthreads();
     rstamp(a, 3);
