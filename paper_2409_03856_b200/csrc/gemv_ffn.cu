@@ -16,6 +16,10 @@
 //                  partials added into the pre-zeroed output with float4 atomics.  SIRIUS_FFN_ATOMIC=0:
 //                  16-warp CTAs, one per SM, cooperative launch, grid barrier and a deterministic
 //                  fixed-order column reduction of the per-CTA partials.
+// Decode chain: both kernels are launched with programmatic dependent launch; each warp's
+// first weight row is requested before griddepcontrol.wait (weights only), the dependent is triggered
+// right after it.  TP > 1 with sirius_par_enable: the rank partial is all-reduced in the kernel's tail
+// over NVLink peer memory (peer_ar.cuh).
 // Design note: 1-D bulk-copy (TMA) staging of 8 KB rows caps at ~3.3 TB/s with a reader
 // (TMA ops have a fixed per-op cost; tools/bw_probe.cu, profiles/r02_bw_probe*.txt), direct 128-bit
 // loads with many rows in flight reach ~7.3 TB/s.

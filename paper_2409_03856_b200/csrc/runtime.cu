@@ -1170,7 +1170,7 @@ static sirius_status enqueue_head_argmax(sirius_ctx* c, const int32_t* tokens, i
                                          int32_t* n_accept_out, int32_t* next_token_out, float* q_out,
                                          float accept_threshold, int32_t accept_mode);
 
-// Batched decode (batch >= 8) through the tensor-core row path: one row per sequence at pos[b] (K/V
+// Batched decode (batch >= 4) through the tensor-core row path: one row per sequence at pos[b] (K/V
 // straight into the cache), CATS mask in the SwiGLU epilogue (sparse) — at these batch sizes the
 // union of the per-sequence active sets covers ~all neurons (SURVEY.md §7 hard part 7), so every
 // W_up / W_down row is read anyway and inactive (b, n) pairs contribute exact zeros (reading D19) —
