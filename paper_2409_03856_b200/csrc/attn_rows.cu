@@ -244,40 +244,57 @@ __global__ void __launch_bounds__(kThreads, 1) attn_rows_kernel(AttnRowsArgs a, 
   // ---- distributed combine: split s finalises rows [64 s / S, 64 (s+1) / S)
   const int s_active = chunk > 0 ? (nkeys + chunk - 1) / chunk : 0;
   const int ra = kRows * split / S, rz = kRows * (split + 1) / S, nrow = rz - ra;
-  // every output (row, dim): the partial values AND (M_s, L_s) of its row for all splits requested
-  // together (one round trip per 32 splits), then M = max M_s, o = sum e^(M_s-M) A_s / sum e^(M_s-M) L_s
-  for (int idx = tid; idx < nrow * HD; idx += kThreads) {
+  // (a) this thread's first two outputs' partial values A_s, requested before anything else (they do
+  // not depend on the weights); (b) per-row weights w_s = e^(M_s - M) / sum_s e^(M_s - M) L_s, one warp
+  // per row, into shared memory (p_s is free after P.V); (c) o = sum_s w_s A_s in split order
+  const int nout = nrow * HD;
+  float av[2][32];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int idx = tid + kThreads * q, rl = idx / HD, d = idx % HD, r = ra + rl;
+    const bool ok = idx < nout && r < nr;
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      av[q][u] = (ok && u < s_active) ? __ldcg(pbase + ((size_t)u * kRows + r) * (HD + 2) + 2 + d) : 0.f;
+  }
+  float* wt = p_s;  // [nrow][kKB] (s_active <= S <= kKB)
+  for (int rl = warp; rl < nrow; rl += kThreads / 32) {
+    const int r = ra + rl;
+    if (r >= nr) continue;  // warp-uniform
+    const float* pr0 = pbase + ((size_t)lane * kRows + r) * (HD + 2);
+    const float* pr1 = pbase + ((size_t)(lane + 32) * kRows + r) * (HD + 2);
+    const float m0 = lane < s_active ? __ldcg(pr0) : -INFINITY, l0 = lane < s_active ? __ldcg(pr0 + 1) : 0.f;
+    const float m1 = lane + 32 < s_active ? __ldcg(pr1) : -INFINITY, l1 = lane + 32 < s_active ? __ldcg(pr1 + 1) : 0.f;
+    const float M = warp_max(fmaxf(m0, m1));
+    const float f0 = m0 == -INFINITY ? 0.f : expf(m0 - M), f1 = m1 == -INFINITY ? 0.f : expf(m1 - M);
+    const float Ls = warp_sum(l0 * f0 + l1 * f1);
+    const float inv = Ls > 0.f ? 1.0f / Ls : 0.f;
+    wt[rl * kKB + lane] = f0 * inv;
+    wt[rl * kKB + lane + 32] = f1 * inv;
+  }
+  __syncthreads();
+  auto emit = [&](int idx, float val) {
     const int rl = idx / HD, d = idx % HD, r = ra + rl;
-    if (r >= nr) continue;
-    float M = -INFINITY, Ls = 0.f, o = 0.f;
-    for (int sp0 = 0; sp0 < s_active; sp0 += 32) {
-      float mv[32], lv[32], av[32];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const float* ps = pbase + ((size_t)(sp0 + u) * kRows + r) * (HD + 2);
-        const bool ok = sp0 + u < s_active;
-        mv[u] = ok ? __ldcg(ps) : -INFINITY;
-        lv[u] = ok ? __ldcg(ps + 1) : 0.f;
-        av[u] = ok ? __ldcg(ps + 2 + d) : 0.f;
-      }
-      float Mb = M;
-#pragma unroll
-      for (int u = 0; u < 32; ++u) Mb = fmaxf(Mb, mv[u]);
-      const float sc = M == -INFINITY ? 0.f : expf(M - Mb);  // rescale earlier batches (s_active > 32)
-      Ls *= sc;
-      o *= sc;
-#pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const float f = mv[u] == -INFINITY ? 0.f : expf(mv[u] - Mb);
-        Ls += lv[u] * f;
-        o += av[u] * f;
-      }
-      M = Mb;
-    }
-    const float val = Ls > 0.f ? o / Ls : 0.f;
     const int rr = r_base + r, i = rr / G, g = rr % G;
     const size_t off = (size_t)(bz * rows + i) * a.Hr * HD + (kvh * G + g) * HD + d;
     store_split3(a.out3, a.plane, off, val);
+  };
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int idx = tid + kThreads * q, rl = idx / HD, d = idx % HD, r = ra + rl;
+    if (idx >= nout || r >= nr) continue;
+    float o = 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) o = fmaf(wt[rl * kKB + u], av[q][u], o);
+    for (int u = 32; u < s_active; ++u) o = fmaf(wt[rl * kKB + u], __ldcg(pbase + ((size_t)u * kRows + r) * (HD + 2) + 2 + d), o);
+    emit(idx, o);
+  }
+  for (int idx = tid + 2 * kThreads; idx < nout; idx += kThreads) {  // few splits: more rows per split
+    const int rl = idx / HD, d = idx % HD, r = ra + rl;
+    if (r >= nr) continue;
+    float o = 0.f;
+    for (int u = 0; u < s_active; ++u) o = fmaf(wt[rl * kKB + u], __ldcg(pbase + ((size_t)u * kRows + r) * (HD + 2) + 2 + d), o);
+    emit(idx, o);
   }
   rstamp(a, 7);
 }
